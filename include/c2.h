@@ -1,0 +1,176 @@
+/* include/c2.h -- C ABI of the B200 (sm_100a) Cluster-and-Conquer (C^2) hot path.
+ *
+ * Problem (paper P:133-172, "P:n" = line n of PAPER.md, arXiv 2010.11497): users U with
+ * item sets P_u; build an approximate KNN graph where each user gets k neighbours under
+ * Jaccard similarity J(u,v) = |P_u ∩ P_v| / |P_u ∪ P_v|.  C^2 computes it in three
+ * steps, one entry point each:
+ *   c2_fastrandomhash  Step 1: FastRandomHash clustering, t configurations of b buckets,
+ *                      H(u) = min_{i in P_u} h(i) (Alg. 1), clusters
+ *                      larger than N recursively split with H\eta.
+ *   c2_local_knn       Step 2: brute-force KNN inside every cluster (Alg. 2 brute branch,
+ *                      P:549-577), s(s-1)/2 similarities per cluster.
+ *   c2_merge           Step 3: Alg. 3, per user merge of the t partial
+ *                      neighbourhoods keeping the k best, similarity values reused.
+ * c2_build runs all three.  The readings of the paper (numbered A#) are listed in DESIGN.md.
+ *
+ * CONVENTIONS (all entry points)
+ *  - Pointers marked "dev" are CUDA device memory on the ctx's device, OWNED BY THE CALLER;
+ *    "host" pointers are ordinary host memory.  The library never frees caller memory; its
+ *    scratch lives in the ctx (grown on demand, reused, freed by c2_ctx_destroy).
+ *  - Work is enqueued on the ctx stream in order.  Entry points return after the work is
+ *    enqueued, except where a host value is produced (n_clusters, stats), which costs one
+ *    stream synchronisation; the recursive split also synchronises once per level.
+ *  - CSR input: csr_offsets dev int32[n_users+1] (offsets[0] = 0), item_ids dev int32[nnz],
+ *    each row non-empty, strictly ascending, ids >= 0, |P_u| <= 32767 (A17, A18, A28).
+ *    Rows violating this make the call return C2_EDATA (first bad row in c2_last_error).
+ *  - Scalars: 1 <= t <= 64; 1 <= b <= 32768 (A26); N >= 2 (A27); 1 <= k <= 64;
+ *    1 <= n_users < 2^29; t * n_users < 2^31.  Otherwise C2_EINVAL, nothing enqueued.
+ *  - Errors: integer codes below; c2_last_error() describes the last failure of that ctx.
+ *    On a non-OK return the outputs are unspecified.  No exceptions cross the ABI.
+ *  - Determinism: outputs are a pure function of (CSR, t, b, N, k, seed, sim_mode), bit
+ *    exact with the CPU oracle (tests/), independent of launch configuration.
+ *  - One ctx per host thread; contexts are independent.
+ */
+#ifndef C2_H
+#define C2_H
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define C2_API __attribute__((visibility("default")))
+#else
+#define C2_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct c2_ctx c2_ctx;
+
+/* One neighbour candidate: id, |P_u ∩ P_v|, |P_u ∪ P_v|.  Padding = {-1, 0, 0}.  8 bytes. */
+typedef struct {
+  int32_t id;
+  uint16_t inter;
+  uint16_t uni;
+} c2_cand;
+
+enum {
+  C2_OK = 0,
+  C2_EINVAL = -1, /* bad scalar parameter or NULL pointer */
+  C2_EDATA = -2,  /* CSR rule violated */
+  C2_ENOMEM = -3, /* device allocation failed */
+  C2_ECUDA = -4   /* CUDA runtime error */
+};
+
+enum {
+  C2_SIM_EXACT = 0,  /* exact set Jaccard */
+  C2_SIM_GF1024 = 1  /* GoldFinger: 1024-bit fingerprint, bit = multiply-add-shift of the item
+                        with the GF seed; J = popc(A&B)/(pc(A)+pc(B)-popc(A&B)) (A19) */
+};
+
+/* Hash parameters (A1, A2): h_f(x) = floor(((a_f*x + c_f) mod 2^64) * b / 2^64), where
+ * (a_0,c_0,a_1,c_1,...) are consecutive outputs of SplitMix64 seeded with `seed`; the
+ * GoldFinger function uses the stream seeded with seed ^ C2_GF_SALT and b = 1024. */
+#define C2_GF_SALT 0x476f6c6446696e67ULL
+#define C2_ABSENT 0xFFFFu /* sketch padding: no further distinct value */
+
+/* ---------------------------------------------------------------- context */
+/* Create a context on CUDA device `device`, enqueueing on `cuda_stream` (a cudaStream_t;
+ * NULL -> the ctx creates and owns a non-blocking stream).  *out receives the ctx. */
+C2_API int c2_ctx_create(c2_ctx **out, int device, void *cuda_stream);
+C2_API void c2_ctx_destroy(c2_ctx *ctx);
+/* Message for the last non-OK return of this ctx (static storage owned by the ctx). */
+C2_API const char *c2_last_error(const c2_ctx *ctx);
+
+enum {
+  C2_OPT_SKETCH_DEPTH = 1, /* 1..8: sketch values kept per (function,user); deeper split
+                              levels recompute from the CSR (A29).  Default 8. */
+  C2_OPT_SYNC_CHECK = 2,   /* nonzero: synchronise + check errors after every launch */
+  C2_OPT_TIMING = 3        /* nonzero: record per-phase CUDA-event times into c2_stats */
+};
+C2_API int c2_ctx_set_option(c2_ctx *ctx, int key, int64_t value);
+
+/* ---------------------------------------------------------------- step 1 */
+/* Canonical cluster assignment (A25): for function f, clusters are ordered by their
+ * smallest member and members are ascending. */
+typedef struct {
+  int32_t *offsets;    /* dev [t][n_users+1]; cluster c of f = members[f][offsets[f][c] ..
+                          offsets[f][c+1]), c < n_clusters[f]; offsets[f][c] = n_users for
+                          c >= n_clusters[f] */
+  int32_t *members;    /* dev [t][n_users] */
+  int32_t *cluster_of; /* dev [t][n_users]: c such that u is in cluster c of f */
+  int32_t *n_clusters; /* HOST [t]; written before return (one stream synchronisation) */
+} c2_clusters;
+
+/* Step 1: FastRandomHash clustering with recursive splitting.  Every cluster
+ * ends with at most N users: a residual larger than N is cut into ceil(s/N) balanced chunks
+ * of its ascending members (A9). */
+C2_API int c2_fastrandomhash(c2_ctx *ctx, const int32_t *csr_offsets, const int32_t *item_ids, int32_t n_users,
+                      int32_t t, int32_t b, int32_t max_cluster_N, uint64_t seed, c2_clusters *out);
+
+/* As c2_fastrandomhash but h_f(x) = htab[f*m + x] (dev uint16 [t][m], values < b), for the
+ * paper's worked examples.  Item ids must be < m. */
+C2_API int c2_fastrandomhash_table(c2_ctx *ctx, const int32_t *csr_offsets, const int32_t *item_ids, int32_t n_users,
+                            int32_t t, int32_t b, int32_t max_cluster_N, const uint16_t *htab, int32_t m,
+                            c2_clusters *out);
+
+/* Stage hook: sketch[f][u][0..D) = the D smallest DISTINCT values of {h_f(x) : x in P_u},
+ * ascending, padded with C2_ABSENT (dev uint16 [t][n_users][D], 1 <= D <= 8).
+ * sketch[f][u][0] = H_f(u); sketch[f][u][d+1] = H\sketch[f][u][d](u). */
+C2_API int c2_sketch(c2_ctx *ctx, const int32_t *csr_offsets, const int32_t *item_ids, int32_t n_users, int32_t t,
+              int32_t b, uint64_t seed, int32_t D, uint16_t *sketch);
+
+/* ---------------------------------------------------------------- step 2 */
+/* Step 2: for every cluster C of every function and every u in C, the first min(k,|C|-1)
+ * users v in C \ {u} under the order "v1 before v2 iff i1*U2 > i2*U1, ties by lower id"
+ * (i = |P_u ∩ P_v|, U = |P_u ∪ P_v|; A13-A15), padded with {-1,0,0}.
+ * cand: dev [t][n_users][k], list of (f,u) at cand[(f*n_users + u)*k].  `clusters` must be
+ * a canonical assignment of the same CSR (e.g. from c2_fastrandomhash; n_clusters host).
+ * sim_mode C2_SIM_GF1024 uses the fingerprints derived from `seed` (A19). */
+C2_API int c2_local_knn(c2_ctx *ctx, const int32_t *csr_offsets, const int32_t *item_ids, int32_t n_users, int32_t t,
+                 const c2_clusters *clusters, int32_t k, int32_t sim_mode, uint64_t seed, c2_cand *cand);
+
+/* ---------------------------------------------------------------- step 3 */
+/* Step 3 (Alg. 3): per user the first k distinct ids of the union of its t lists under the
+ * same order; a repeated id always carries the same (inter, uni) (A16).  cand as produced
+ * by c2_local_knn (each list sorted best-first, pads last).  Outputs dev [n_users][k]:
+ * nbr (id or -1), inter, uni; sim (nullable) = (float)inter/(float)uni (IEEE div.rn), 0 for
+ * pads. */
+C2_API int c2_merge(c2_ctx *ctx, int32_t t, int32_t n_users, int32_t k, const c2_cand *cand, int32_t *nbr,
+             uint16_t *inter, uint16_t *uni, float *sim);
+
+/* ---------------------------------------------------------------- whole path */
+/* Steps 1-3 on device-resident inputs; outputs as c2_merge.  Cluster arrays and candidate
+ * lists live in ctx scratch. */
+C2_API int c2_build(c2_ctx *ctx, const int32_t *csr_offsets, const int32_t *item_ids, int32_t n_users, int32_t t,
+             int32_t b, int32_t max_cluster_N, int32_t k, int32_t sim_mode, uint64_t seed, int32_t *nbr,
+             uint16_t *inter, uint16_t *uni, float *sim);
+
+/* As c2_build with HOST inputs and outputs (nnz = csr_offsets[n_users]); the host<->device
+ * copies run on the ctx stream inside the call.  Host buffers may be pageable or pinned;
+ * sim may be NULL.  Returns after the outputs are in host memory. */
+C2_API int c2_build_host(c2_ctx *ctx, const int32_t *csr_offsets, const int32_t *item_ids, int32_t n_users, int32_t t,
+                  int32_t b, int32_t max_cluster_N, int32_t k, int32_t sim_mode, uint64_t seed, int32_t *nbr,
+                  uint16_t *inter, uint16_t *uni, float *sim);
+
+/* ---------------------------------------------------------------- stats */
+typedef struct {
+  int64_t pairs;             /* P = sum over functions and clusters of s(s-1)/2 (A21) */
+  int64_t clusters;          /* total clusters over all functions */
+  int64_t max_cluster_size;
+  int64_t split_nodes;       /* nodes split by H\eta */
+  int64_t max_depth;         /* deepest split level that created a cluster */
+  int64_t folded_singletons; /* users alone in their new cluster, kept in the parent (A7) */
+  int64_t chunked_residuals; /* residuals larger than N cut by the chunk guard (A9) */
+  int64_t launches;          /* kernels launched by the last entry point */
+  int64_t host_syncs;        /* stream synchronisations in the last entry point */
+  double ms_sketch, ms_cluster, ms_local, ms_merge, ms_total; /* with C2_OPT_TIMING */
+} c2_stats;
+/* Statistics of the last c2_fastrandomhash / c2_local_knn / c2_merge / c2_build call. */
+C2_API int c2_get_stats(const c2_ctx *ctx, c2_stats *out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

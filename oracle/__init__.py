@@ -58,6 +58,7 @@ def _load():
         "c2o_local_knn": (_I, [_I64, _P, _P, _I, _P, _P, _P, _I, _I, _P, _I64, _I, _P]),
         "c2o_merge": (_I, [_I64, _I, _I, _P, _I, _P, _P, _P, _P]),
         "c2o_knn_union": (_I, [_I64, _P, _P, _I, _P, _P, _P, _I, _I, _P, _I64, _I, _P, _P, _P]),
+        "c2o_knn_union_users": (_I, [_I64, _P, _P, _I, _P, _P, _P, _I, _I, _P, _I64, _I64, _P, _I, _P, _P, _P]),
         "c2o_exact_knn": (_I, [_I64, _P, _P, _I, _I, _P, _I64, _I64, _P, _I, _P, _P, _P]),
         "c2o_pair_counts": (_I, [_I64, _P, _P, _I64, _P, _P, _P, _P]),
     }
@@ -191,6 +192,22 @@ def knn_union(offs, items, cl: dict, k: int, sim_mode: int = 0, gtab=None, nthre
     _chk(_load().c2o_knn_union(n, _ptr(offs), _ptr(items), t, _ptr(cl["offsets"]), _ptr(cl["members"]),
                                _ptr(cl["cluster_of"]), k, sim_mode, _ptr(gtab), m, nthreads or NTHREADS, _ptr(nbr),
                                _ptr(inter), _ptr(uni)), "knn_union")
+    return nbr, inter, uni
+
+
+def knn_union_users(offs, items, cl: dict, k: int, users, sim_mode: int = 0, gtab=None,
+                    nthreads: int | None = None):
+    offs, items, n = _csr(offs, items)
+    t = cl["offsets"].shape[0]
+    m = 0 if gtab is None else len(gtab)
+    users = np.ascontiguousarray(users, np.int32)
+    q = len(users)
+    nbr = np.zeros((q, k), np.int32)
+    inter = np.zeros((q, k), np.uint16)
+    uni = np.zeros((q, k), np.uint16)
+    _chk(_load().c2o_knn_union_users(n, _ptr(offs), _ptr(items), t, _ptr(cl["offsets"]), _ptr(cl["members"]),
+                                     _ptr(cl["cluster_of"]), k, sim_mode, _ptr(gtab), m, q, _ptr(users),
+                                     nthreads or NTHREADS, _ptr(nbr), _ptr(inter), _ptr(uni)), "knn_union_users")
     return nbr, inter, uni
 
 

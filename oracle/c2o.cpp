@@ -413,12 +413,14 @@ int c2o_merge(int64_t n, int t, int k, const c2o_cand *cand, int nthreads, int32
   return 0;
 }
 
-int c2o_knn_union(int64_t n, const int32_t *offs, const int32_t *items, int t, const int32_t *offsets,
-                  const int32_t *members, const int32_t *cluster_of, int k, int sim_mode, const uint16_t *gtab,
-                  int64_t m, int nthreads, int32_t *nbr, uint16_t *inter, uint16_t *uni) {
+int c2o_knn_union_users(int64_t n, const int32_t *offs, const int32_t *items, int t, const int32_t *offsets,
+                        const int32_t *members, const int32_t *cluster_of, int k, int sim_mode,
+                        const uint16_t *gtab, int64_t m, int64_t n_sub, const int32_t *users, int nthreads,
+                        int32_t *nbr, uint16_t *inter, uint16_t *uni) {
   if (!row_ok(offs, items, n, m)) return -2;
   Profiles P(n, offs, items, sim_mode, gtab);
-  parallel_for(n, nthreads, [&](int64_t u) {
+  parallel_for(n_sub, nthreads, [&](int64_t q) {
+    int64_t u = users[q];
     std::vector<int32_t> V;  // V(u) = U_f cluster_f(u) \ {u}
     for (int f = 0; f < t; ++f) {
       int32_t c = cluster_of[f * n + u];
@@ -431,9 +433,18 @@ int c2o_knn_union(int64_t n, const int32_t *offs, const int32_t *items, int t, c
     for (int32_t v : V) cands.push_back(P.cand(u, v));
     std::vector<c2o_cand> out(k);
     write_topk(cands, k, out.data());
-    for (int j = 0; j < k; ++j) { nbr[u * k + j] = out[j].id; inter[u * k + j] = out[j].inter; uni[u * k + j] = out[j].uni; }
+    for (int j = 0; j < k; ++j) { nbr[q * k + j] = out[j].id; inter[q * k + j] = out[j].inter; uni[q * k + j] = out[j].uni; }
   });
   return 0;
+}
+
+int c2o_knn_union(int64_t n, const int32_t *offs, const int32_t *items, int t, const int32_t *offsets,
+                  const int32_t *members, const int32_t *cluster_of, int k, int sim_mode, const uint16_t *gtab,
+                  int64_t m, int nthreads, int32_t *nbr, uint16_t *inter, uint16_t *uni) {
+  std::vector<int32_t> all(n);
+  for (int64_t u = 0; u < n; ++u) all[u] = (int32_t)u;
+  return c2o_knn_union_users(n, offs, items, t, offsets, members, cluster_of, k, sim_mode, gtab, m, n, all.data(),
+                             nthreads, nbr, inter, uni);
 }
 
 int c2o_exact_knn(int64_t n, const int32_t *offs, const int32_t *items, int k, int sim_mode,

@@ -80,6 +80,12 @@ int c2o_knn_union(int64_t n, const int32_t *offs, const int32_t *items, int t, c
                   const int32_t *members, const int32_t *cluster_of, int k, int sim_mode, const uint16_t *gtab,
                   int64_t m, int nthreads, int32_t *nbr, uint16_t *inter, uint16_t *uni);
 
+/* Same for the users listed in `users` only (sampled parity at full size); outputs [n_sub][k]. */
+int c2o_knn_union_users(int64_t n, const int32_t *offs, const int32_t *items, int t, const int32_t *offsets,
+                        const int32_t *members, const int32_t *cluster_of, int k, int sim_mode,
+                        const uint16_t *gtab, int64_t m, int64_t n_sub, const int32_t *users, int nthreads,
+                        int32_t *nbr, uint16_t *inter, uint16_t *uni);
+
 /* Exact KNN (brute force over all users) for the users listed in `users`
  * (n_sub of them); outputs are [n_sub][k]. */
 int c2o_exact_knn(int64_t n, const int32_t *offs, const int32_t *items, int k, int sim_mode,

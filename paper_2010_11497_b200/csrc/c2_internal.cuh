@@ -1,0 +1,143 @@
+// c2_internal.cuh -- internals of libc2 (B200, sm_100a).  Not part of the ABI.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <cstdarg>
+#include <cstdio>
+#include <map>
+#include <string>
+
+#include "../../include/c2.h"
+
+#define C2_MAX_T 64
+#define C2_MAX_K 64
+#define C2_SKETCH_D 8
+#define C2_ABSENT16 ((uint16_t)0xFFFF)
+
+struct c2_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  int num_sms = 148;
+  size_t smem_optin = 0;
+  char err[512] = {0};
+  // options
+  int sketch_depth = C2_SKETCH_D;
+  bool sync_check = false;
+  bool timing = false;
+  c2_stats stats{};
+  // device workspace: name -> (ptr, bytes); grow-only
+  std::map<std::string, std::pair<void *, size_t>> ws;
+  // pinned host staging for small D2H reads
+  int64_t *h_small = nullptr;
+  int64_t *d_small = nullptr;
+  cudaEvent_t ev[8] = {nullptr};
+};
+
+namespace c2 {
+
+int set_err(c2_ctx *ctx, int code, const char *fmt, ...);
+
+// Device scratch owned by the ctx.  Contents are NOT preserved across growth.
+void *ws_get(c2_ctx *ctx, const char *name, size_t bytes, int *rc);
+
+// Launch bookkeeping: counts launches and, with C2_OPT_SYNC_CHECK, checks each one.
+int after_launch(c2_ctx *ctx, const char *what);
+// Synchronise the ctx stream (counted) and check errors.
+int stream_sync(c2_ctx *ctx, const char *what);
+
+// Hash parameters of the t generative functions + GoldFinger (product-side SplitMix64).
+struct HashParams {
+  uint64_t a[C2_MAX_T];
+  uint64_t c[C2_MAX_T];
+  uint64_t ga, gc;
+};
+void make_hash_params(uint64_t seed, int t, HashParams *hp);
+
+// ---------------------------------------------------------------- primitives (prims.cu)
+// out[i] = sum_{j<i} in[j] for i in [0, n]; out has n+1 entries (out[n] = total).
+int scan_exclusive(c2_ctx *ctx, const int32_t *in, int32_t *out, int64_t n);
+// Stable LSD radix sort of (key, val) pairs by the low `bits` bits of key.  Result in
+// keys_out / vals_out.  Scratch from ctx.
+int radix_sort_pairs(c2_ctx *ctx, const uint32_t *keys_in, const uint32_t *vals_in, uint32_t *keys_out,
+                     uint32_t *vals_out, int64_t n, int bits);
+
+// ---------------------------------------------------------------- stages
+struct Csr {
+  const int32_t *offs;  // dev [n+1]
+  const int32_t *items; // dev [nnz]
+  int32_t n;
+  int64_t nnz;
+  int32_t max_item;     // filled by validate()
+  int32_t max_len;
+  const int32_t *psize; // dev [n], |P_u|
+};
+// K0: CSR rules + |P_u| + max item / max row length (one host sync).
+int validate_csr(c2_ctx *ctx, Csr *csr);
+
+// Step 1 (k_sketch.cu + k_cluster.cu).  htab == nullptr -> hashed with params.
+struct Clusters {
+  int32_t *offsets, *members, *cluster_of; // dev, canonical
+  int32_t n_clusters[C2_MAX_T];            // host
+  int32_t max_size;
+};
+int sketch(c2_ctx *ctx, const Csr &csr, int t, int b, const HashParams *hp, const uint16_t *htab, int32_t m,
+           int D, uint16_t *out);
+int fastrandomhash(c2_ctx *ctx, const Csr &csr, int t, int b, int64_t N, const HashParams *hp,
+                   const uint16_t *htab, int32_t m, Clusters *out);
+
+// Step 2 (k_local.cu).
+int gf_encode(c2_ctx *ctx, const Csr &csr, const HashParams *hp, Csr *gf);
+int local_knn(c2_ctx *ctx, const Csr &csr, int t, const Clusters &cl, int k, c2_cand *cand);
+
+// Step 3 (k_merge.cu).
+int merge(c2_ctx *ctx, int t, int n, int k, const c2_cand *cand, int32_t *nbr, uint16_t *inter, uint16_t *uni,
+          float *sim);
+
+}  // namespace c2
+
+#define C2_CUDA(ctx, call)                                                                  \
+  do {                                                                                      \
+    cudaError_t e_ = (call);                                                                \
+    if (e_ != cudaSuccess)                                                                  \
+      return c2::set_err((ctx), C2_ECUDA, "%s: %s (%s:%d)", #call, cudaGetErrorString(e_), \
+                         __FILE__, __LINE__);                                               \
+  } while (0)
+
+#define C2_TRY(expr)          \
+  do {                        \
+    int rc_ = (expr);         \
+    if (rc_ != C2_OK) return rc_; \
+  } while (0)
+
+#define C2_LAUNCHED(ctx, name) C2_TRY(c2::after_launch((ctx), (name)))
+
+// ---------------------------------------------------------------- device helpers
+namespace c2d {
+
+__device__ __forceinline__ uint32_t item_hash(uint64_t a, uint64_t c, uint32_t x, uint32_t b) {
+  // h(x) = floor(((a*x + c) mod 2^64) * b / 2^64)  (A1): one IMAD.WIDE-style mul-add + UMULHI
+  uint64_t z = a * (uint64_t)x + c;
+  return (uint32_t)__umul64hi(z, (uint64_t)b);
+}
+
+// Candidate order (A13): (i1,U1,id1) before (i2,U2,id2) iff i1*U2 > i2*U1, ties by lower id.
+// inter <= 32767 and union <= 65534 (A28), so the products fit in 32 bits.
+__device__ __forceinline__ bool better(uint32_t i1, uint32_t U1, int32_t id1, uint32_t i2, uint32_t U2,
+                                       int32_t id2) {
+  uint32_t l = i1 * U2, r = i2 * U1;
+  return l > r || (l == r && id1 < id2);
+}
+
+__device__ __forceinline__ int warp_incl_scan(int v) {
+  int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    int y = __shfl_up_sync(0xffffffffu, v, o);
+    if (lane >= o) v += y;
+  }
+  return v;
+}
+
+}  // namespace c2d

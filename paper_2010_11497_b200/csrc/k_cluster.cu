@@ -1,0 +1,458 @@
+// k_cluster.cu -- Step 1 of C^2 on the GPU: Alg. 1 bucketing and the recursive
+// split of clusters larger than N, level-synchronously over all functions, then
+// the chunk guard (A9) and the canonical cluster arrays (A25).
+//
+// Representation.  key[f][u] is the id of the node user u currently belongs to under f
+// (level 0: f*b + H_f(u)); slot[f][u] >= 0 iff that node is larger than N and is being split
+// at the current level (slot = its index among the level's active nodes).  One level:
+//   count : for active users, nv = next distinct value (sketch[d+1], or recomputed from the
+//           CSR past the sketch depth) and hist[slot][nv]++
+//   assign: groups with >= 2 users become child nodes (new ids); groups of one user and
+//           users with no next value stay in the parent, which becomes a terminal residual
+//           (A6-A8); children larger than N are active at the next level
+//   apply : move users to their child node
+// The host reads two counters per level (children, next-level active nodes).
+#include <algorithm>
+
+#include "c2_internal.cuh"
+
+namespace c2 {
+
+struct HashArgs2 {
+  uint64_t a[C2_MAX_T];
+  uint64_t c[C2_MAX_T];
+};
+
+// ------------------------------------------------------------------ level 0
+__global__ void k_level0(const uint16_t *__restrict__ sk, int64_t TN, int32_t n, int32_t b,
+                         int32_t *__restrict__ key, uint16_t *__restrict__ curval, int32_t *__restrict__ size0) {
+  int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= TN) return;
+  int32_t f = (int32_t)(q / n);
+  uint16_t v = sk[q * C2_SKETCH_D];  // H_f(u)
+  int32_t k = f * b + v;
+  key[q] = k;
+  curval[q] = v;
+  atomicAdd(&size0[k], 1);
+}
+
+__global__ void k_flag_gt(const int32_t *__restrict__ cnt, int64_t E, int64_t N, int32_t *__restrict__ flag) {
+  int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e < E) flag[e] = cnt[e] > N ? 1 : 0;
+}
+
+__global__ void k_slot0(const int32_t *__restrict__ key, const int32_t *__restrict__ size0,
+                        const int32_t *__restrict__ ascan, int64_t TN, int64_t N, int32_t *__restrict__ slot) {
+  int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= TN) return;
+  int32_t k = key[q];
+  slot[q] = size0[k] > N ? ascan[k] : -1;
+}
+
+// ------------------------------------------------------------------ split level
+template <bool TABLE>
+__device__ __forceinline__ uint16_t next_above(const int32_t *__restrict__ offs, const int32_t *__restrict__ items,
+                                               int32_t u, int f, uint32_t eta, uint32_t b, const HashArgs2 &ha,
+                                               const uint16_t *__restrict__ htab, int32_t m) {
+  // H\eta(u) = min_{i in P_u, h(i) > eta} h(i), recomputed from the CSR
+  uint32_t best = C2_ABSENT16;
+  for (int32_t p = offs[u]; p < offs[u + 1]; ++p) {
+    uint32_t x = (uint32_t)items[p];
+    uint32_t v = TABLE ? (uint32_t)htab[(int64_t)f * m + x] : c2d::item_hash(ha.a[f], ha.c[f], x, b);
+    if (v > eta && v < best) best = v;
+  }
+  return (uint16_t)best;
+}
+
+template <bool TABLE>
+__global__ void k_split_count(const int32_t *__restrict__ slot, const uint16_t *__restrict__ sk,
+                              const uint16_t *__restrict__ curval, uint16_t *__restrict__ nextval, int64_t TN,
+                              int32_t n, int d, int Deff, int32_t a0, int32_t a1, int32_t b,
+                              int32_t *__restrict__ hist, const int32_t *__restrict__ offs,
+                              const int32_t *__restrict__ items, HashArgs2 ha, const uint16_t *__restrict__ htab,
+                              int32_t m) {
+  int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= TN) return;
+  int32_t s = slot[q];
+  if (s < a0 || s >= a1) return;
+  uint16_t nv;
+  if (d + 1 < Deff) nv = sk[q * C2_SKETCH_D + d + 1];
+  else nv = next_above<TABLE>(offs, items, (int32_t)(q % n), (int)(q / n), curval[q], (uint32_t)b, ha, htab, m);
+  nextval[q] = nv;
+  if (nv != C2_ABSENT16) atomicAdd(&hist[(int64_t)(s - a0) * b + nv], 1);
+}
+
+__global__ void k_child_flags(const int32_t *__restrict__ hist, int64_t E, int64_t N, int32_t *__restrict__ fc,
+                              int32_t *__restrict__ fa, unsigned long long *__restrict__ folded) {
+  int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  int one = 0;
+  if (e < E) {
+    int32_t c = hist[e];
+    fc[e] = c >= 2;
+    fa[e] = c > N;
+    one = c == 1;
+  }
+  unsigned bal = __ballot_sync(0xffffffffu, one);
+  if ((threadIdx.x & 31) == 0 && bal) atomicAdd(folded, (unsigned long long)__popc(bal));
+}
+
+__global__ void k_child_assign(const int32_t *__restrict__ hist, const int32_t *__restrict__ cscan,
+                               const int32_t *__restrict__ ascan, int64_t E, int64_t N, int32_t id_base,
+                               int32_t slot_base, int32_t *__restrict__ child_id, int32_t *__restrict__ child_slot) {
+  int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= E) return;
+  int32_t c = hist[e];
+  child_id[e] = c >= 2 ? id_base + cscan[e] : -1;
+  child_slot[e] = c > N ? slot_base + ascan[e] : -1;
+}
+
+__global__ void k_split_apply(int32_t *__restrict__ slot, int32_t *__restrict__ key, uint16_t *__restrict__ curval,
+                              const uint16_t *__restrict__ nextval, int64_t TN, int32_t a0, int32_t a1, int32_t b,
+                              const int32_t *__restrict__ child_id, const int32_t *__restrict__ child_slot,
+                              int32_t *__restrict__ slot_next) {
+  int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= TN) return;
+  int32_t s = slot[q];
+  if (s < a0 || s >= a1) return;
+  uint16_t nv = nextval[q];
+  int32_t ns = -1;
+  if (nv != C2_ABSENT16) {
+    int64_t e = (int64_t)(s - a0) * b + nv;
+    int32_t c = child_id[e];
+    if (c >= 0) {  // >= 2 users share nv: move to the child node
+      key[q] = c;
+      curval[q] = nv;
+      ns = child_slot[e];
+    }
+  }
+  slot_next[q] = ns;  // -1: stays in the parent's residual (terminal) or child <= N
+}
+
+// ------------------------------------------------------------------ canonical form
+__global__ void k_count_keys(const int32_t *__restrict__ key, int64_t TN, int32_t *__restrict__ size) {
+  int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (q < TN) atomicAdd(&size[key[q]], 1);
+}
+
+__global__ void k_max(const int32_t *__restrict__ x, int64_t E, int32_t *__restrict__ out) {
+  int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  int v = e < E ? x[e] : 0;
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v = max(v, __shfl_xor_sync(0xffffffffu, v, o));
+  if ((threadIdx.x & 31) == 0) atomicMax(out, v);
+}
+
+__global__ void k_rep(const int32_t *__restrict__ key, int64_t TN, int32_t n, int32_t *__restrict__ rep) {
+  int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (q < TN) atomicMin(&rep[key[q]], (int32_t)(q % n));
+}
+
+__global__ void k_heads(const int32_t *__restrict__ key, const int32_t *__restrict__ rep, int64_t TN, int32_t n,
+                        int32_t *__restrict__ head) {
+  int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (q < TN) head[q] = rep[key[q]] == (int32_t)(q % n);
+}
+
+__global__ void k_cluster_of(const int32_t *__restrict__ key, const int32_t *__restrict__ rep,
+                             const int32_t *__restrict__ hscan, const int32_t *__restrict__ size, int64_t TN,
+                             int32_t n, int32_t *__restrict__ cof, int32_t *__restrict__ csize,
+                             uint32_t *__restrict__ skey, uint32_t *__restrict__ sval) {
+  int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= TN) return;
+  int64_t f = q / n;
+  int32_t u = (int32_t)(q % n);
+  int32_t k = key[q];
+  int32_t r = rep[k];
+  int32_t c = hscan[f * n + r] - hscan[f * n];  // clusters of f ordered by smallest member
+  cof[q] = c;
+  if (r == u) csize[f * (n + 1) + c] = size[k];
+  skey[q] = (uint32_t)(f * n + c);
+  sval[q] = (uint32_t)u;
+}
+
+__global__ void k_fix_offsets(const int32_t *__restrict__ raw, int64_t E, int32_t n, int32_t *__restrict__ offsets) {
+  int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= E) return;
+  int64_t f = e / (n + 1);
+  offsets[e] = raw[e] - (int32_t)(f * n);
+}
+
+__global__ void k_pairs(const int32_t *__restrict__ csize, int64_t E, unsigned long long *__restrict__ acc) {
+  int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  unsigned long long s = e < E ? (unsigned long long)csize[e] : 0ull;
+  unsigned long long p = s * (s - (s > 0)) / 2;
+#pragma unroll
+  for (int o = 16; o; o >>= 1) p += __shfl_xor_sync(0xffffffffu, p, o);
+  if ((threadIdx.x & 31) == 0 && p) atomicAdd(acc, p);
+}
+
+// chunk guard: sorted (key, f*n+u) pairs; node_start = exclusive scan of sizes
+__global__ void k_chunk_count(const int32_t *__restrict__ size, int64_t E, int64_t N, int32_t *__restrict__ mc) {
+  int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e < E) mc[e] = size[e] > N ? (int32_t)((size[e] + N - 1) / N) : 0;
+}
+
+__global__ void k_chunk_assign(const uint32_t *__restrict__ skeys, const uint32_t *__restrict__ svals, int64_t TN,
+                               const int32_t *__restrict__ size, const int32_t *__restrict__ start,
+                               const int32_t *__restrict__ cbase, int64_t N, int32_t id_base,
+                               int32_t *__restrict__ key) {
+  int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= TN) return;
+  uint32_t k = skeys[p];
+  int64_t s = size[k];
+  if (s <= N) return;
+  int64_t r = p - start[k];               // rank among the node's members (ascending id)
+  int64_t mcount = (s + N - 1) / N;
+  int64_t j = ((r + 1) * mcount + s - 1) / s - 1;  // chunk j = [floor(j s/m), floor((j+1) s/m))
+  key[svals[p]] = id_base + cbase[k] + (int32_t)j;
+}
+
+static inline unsigned nblk(int64_t x, int bs = 256) { return (unsigned)((x + bs - 1) / bs); }
+static inline int bits_for(int64_t x) {
+  int b = 1;
+  while ((1LL << b) < x) ++b;
+  return b;
+}
+
+// ------------------------------------------------------------------ small helpers
+__global__ void k_fill_pairs(const int32_t *__restrict__ key, int64_t TN, uint32_t *__restrict__ k,
+                             uint32_t *__restrict__ v) {
+  int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (q < TN) {
+    k[q] = (uint32_t)key[q];
+    v[q] = (uint32_t)q;
+  }
+}
+int fill_key_pairs(c2_ctx *ctx, const int32_t *key, int64_t TN, uint32_t *k, uint32_t *v) {
+  k_fill_pairs<<<nblk(TN), 256, 0, ctx->stream>>>(key, TN, k, v);
+  C2_LAUNCHED(ctx, "k_fill_pairs");
+  return C2_OK;
+}
+
+__global__ void k_count_gt(const int32_t *__restrict__ x, int64_t E, int64_t N, int32_t *__restrict__ out) {
+  int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  unsigned bal = __ballot_sync(0xffffffffu, e < E && x[e] > N);
+  if ((threadIdx.x & 31) == 0 && bal) atomicAdd(out, __popc(bal));
+}
+int count_gt(c2_ctx *ctx, const int32_t *x, int64_t E, int64_t N, int32_t *out) {
+  k_count_gt<<<nblk(E), 256, 0, ctx->stream>>>(x, E, N, out);
+  C2_LAUNCHED(ctx, "k_count_gt");
+  return C2_OK;
+}
+
+int fastrandomhash(c2_ctx *ctx, const Csr &csr, int t, int b, int64_t N, const HashParams *hp,
+                   const uint16_t *htab, int32_t m, Clusters *out) {
+  int rc;
+  const int32_t n = csr.n;
+  const int64_t TN = (int64_t)t * n;
+  cudaStream_t st = ctx->stream;
+  HashArgs2 ha;
+  for (int f = 0; f < t; ++f) {
+    ha.a[f] = hp ? hp->a[f] : 0;
+    ha.c[f] = hp ? hp->c[f] : 0;
+  }
+  const int Deff = ctx->sketch_depth;
+
+  // ---- K1 sketch (all t functions, depth 8)
+  uint16_t *sk = (uint16_t *)ws_get(ctx, "sketch", (size_t)TN * C2_SKETCH_D * 2, &rc);
+  if (rc) return rc;
+  cudaEvent_t *ev = ctx->ev;
+  if (ctx->timing) cudaEventRecord(ev[0], st);
+  C2_TRY(sketch(ctx, csr, t, b, hp, htab, m, C2_SKETCH_D, sk));
+  if (ctx->timing) cudaEventRecord(ev[1], st);
+
+  int32_t *key = (int32_t *)ws_get(ctx, "key", (size_t)TN * 4, &rc);
+  if (rc) return rc;
+  int32_t *slot = (int32_t *)ws_get(ctx, "slot", (size_t)TN * 4, &rc);
+  if (rc) return rc;
+  int32_t *slot2 = (int32_t *)ws_get(ctx, "slot2", (size_t)TN * 4, &rc);
+  if (rc) return rc;
+  uint16_t *curval = (uint16_t *)ws_get(ctx, "curval", (size_t)TN * 2, &rc);
+  if (rc) return rc;
+  uint16_t *nextval = (uint16_t *)ws_get(ctx, "nextval", (size_t)TN * 2, &rc);
+  if (rc) return rc;
+  const int64_t TB = (int64_t)t * b;
+  int32_t *size0 = (int32_t *)ws_get(ctx, "size0", (size_t)TB * 4, &rc);
+  if (rc) return rc;
+  int32_t *ascan0 = (int32_t *)ws_get(ctx, "ascan0", (size_t)(TB + 1) * 4 * 2, &rc);
+  if (rc) return rc;
+  int32_t *aflag0 = ascan0 + TB + 1;
+  unsigned long long *acc = (unsigned long long *)ws_get(ctx, "acc", 64, &rc);
+  if (rc) return rc;
+  int32_t *hsmall = (int32_t *)ctx->h_small;
+
+  // ---- K2 level 0: Alg. 1, B_f[H_f(u)] <- B_f[H_f(u)] ∪ {u}
+  C2_CUDA(ctx, cudaMemsetAsync(size0, 0, (size_t)TB * 4, st));
+  C2_CUDA(ctx, cudaMemsetAsync(acc, 0, 64, st));
+  k_level0<<<nblk(TN), 256, 0, st>>>(sk, TN, n, b, key, curval, size0);
+  C2_LAUNCHED(ctx, "k_level0");
+  k_flag_gt<<<nblk(TB), 256, 0, st>>>(size0, TB, N, aflag0);
+  C2_LAUNCHED(ctx, "k_flag_gt");
+  C2_TRY(scan_exclusive(ctx, aflag0, ascan0, TB));
+  k_slot0<<<nblk(TN), 256, 0, st>>>(key, size0, ascan0, TN, N, slot);
+  C2_LAUNCHED(ctx, "k_slot0");
+  C2_CUDA(ctx, cudaMemcpyAsync(hsmall, ascan0 + TB, 4, cudaMemcpyDeviceToHost, st));
+  C2_TRY(stream_sync(ctx, "level0"));
+  int64_t n_active = hsmall[0];
+  int64_t next_id = TB;
+  int64_t split_nodes = 0, max_depth = 0;
+
+  // ---- K3 recursive split, one level per iteration (batched over active nodes)
+  const int64_t max_hist = (int64_t)1 << 26;
+  int64_t batch = std::max<int64_t>(1, max_hist / b);
+  for (int d = 0; n_active > 0; ++d) {
+    if (d > b + 1) return set_err(ctx, C2_ECUDA, "split did not terminate");
+    int64_t new_active = 0, children_lvl = 0;
+    C2_CUDA(ctx, cudaMemsetAsync(slot2, 0xFF, (size_t)TN * 4, st));
+    for (int64_t a0 = 0; a0 < n_active; a0 += batch) {
+      int64_t a1 = std::min(n_active, a0 + batch);
+      int64_t E = (a1 - a0) * b;
+      int32_t *hist = (int32_t *)ws_get(ctx, "hist", (size_t)E * 4, &rc);
+      if (rc) return rc;
+      int32_t *fbuf = (int32_t *)ws_get(ctx, "hflags", (size_t)(E + 1) * 4 * 4, &rc);
+      if (rc) return rc;
+      int32_t *fc = fbuf, *fa = fbuf + (E + 1), *cscan = fbuf + 2 * (E + 1), *ascan = fbuf + 3 * (E + 1);
+      int32_t *cid = (int32_t *)ws_get(ctx, "child_id", (size_t)E * 4 * 2, &rc);
+      if (rc) return rc;
+      int32_t *cslot = cid + E;
+      C2_CUDA(ctx, cudaMemsetAsync(hist, 0, (size_t)E * 4, st));
+      if (htab)
+        k_split_count<true><<<nblk(TN), 256, 0, st>>>(slot, sk, curval, nextval, TN, n, d, Deff, (int32_t)a0,
+                                                      (int32_t)a1, b, hist, csr.offs, csr.items, ha, htab, m);
+      else
+        k_split_count<false><<<nblk(TN), 256, 0, st>>>(slot, sk, curval, nextval, TN, n, d, Deff, (int32_t)a0,
+                                                       (int32_t)a1, b, hist, csr.offs, csr.items, ha, nullptr, 0);
+      C2_LAUNCHED(ctx, "k_split_count");
+      k_child_flags<<<nblk(E), 256, 0, st>>>(hist, E, N, fc, fa, acc + 1);
+      C2_LAUNCHED(ctx, "k_child_flags");
+      C2_TRY(scan_exclusive(ctx, fc, cscan, E));
+      C2_TRY(scan_exclusive(ctx, fa, ascan, E));
+      k_child_assign<<<nblk(E), 256, 0, st>>>(hist, cscan, ascan, E, N, (int32_t)next_id,
+                                              (int32_t)new_active, cid, cslot);
+      C2_LAUNCHED(ctx, "k_child_assign");
+      k_split_apply<<<nblk(TN), 256, 0, st>>>(slot, key, curval, nextval, TN, (int32_t)a0, (int32_t)a1, b, cid,
+                                              cslot, slot2);
+      C2_LAUNCHED(ctx, "k_split_apply");
+      C2_CUDA(ctx, cudaMemcpyAsync(hsmall, cscan + E, 4, cudaMemcpyDeviceToHost, st));
+      C2_CUDA(ctx, cudaMemcpyAsync(hsmall + 1, ascan + E, 4, cudaMemcpyDeviceToHost, st));
+      C2_TRY(stream_sync(ctx, "split level"));
+      next_id += hsmall[0];
+      children_lvl += hsmall[0];
+      new_active += hsmall[1];
+      if (next_id >= (int64_t)INT32_MAX / 2) return set_err(ctx, C2_EINVAL, "too many split nodes");
+    }
+    split_nodes += n_active;
+    if (children_lvl > 0) max_depth = d + 1;
+    std::swap(slot, slot2);  // slot2 was reset to -1 before the level; active users rewritten
+    n_active = new_active;
+  }
+  if (ctx->timing) cudaEventRecord(ev[2], st);
+
+  // ---- K4 chunk guard + canonical form
+  int32_t *size = (int32_t *)ws_get(ctx, "nsize", (size_t)(next_id + TN + 1) * 4, &rc);
+  if (rc) return rc;
+  C2_CUDA(ctx, cudaMemsetAsync(size, 0, (size_t)next_id * 4, st));
+  k_count_keys<<<nblk(TN), 256, 0, st>>>(key, TN, size);
+  C2_LAUNCHED(ctx, "k_count_keys");
+  int32_t *mx = (int32_t *)(acc + 2);
+  C2_CUDA(ctx, cudaMemsetAsync(mx, 0, 4, st));
+  k_max<<<nblk(next_id), 256, 0, st>>>(size, next_id, mx);
+  C2_LAUNCHED(ctx, "k_max");
+  C2_CUDA(ctx, cudaMemcpyAsync(hsmall, mx, 4, cudaMemcpyDeviceToHost, st));
+  C2_CUDA(ctx, cudaMemcpyAsync(ctx->h_small + 4, acc + 1, 8, cudaMemcpyDeviceToHost, st));
+  C2_TRY(stream_sync(ctx, "max size"));
+  int64_t chunked = 0;
+  int64_t folded = ctx->h_small[4];
+  uint32_t *skey = (uint32_t *)ws_get(ctx, "skey", (size_t)TN * 4, &rc);
+  if (rc) return rc;
+  uint32_t *sval = (uint32_t *)ws_get(ctx, "sval", (size_t)TN * 4, &rc);
+  if (rc) return rc;
+  uint32_t *skey2 = (uint32_t *)ws_get(ctx, "skey2", (size_t)TN * 4, &rc);
+  if (rc) return rc;
+  uint32_t *sval2 = (uint32_t *)ws_get(ctx, "sval2", (size_t)TN * 4, &rc);
+  if (rc) return rc;
+  if (hsmall[0] > N) {
+    // A9: residuals larger than N -> ceil(s/N) balanced chunks of their ascending members.
+    // Stable sort of (node, f*n+u) by node gives every node's members in ascending order.
+    int32_t *tmp = (int32_t *)ws_get(ctx, "chunk_tmp", (size_t)(next_id + 1) * 4 * 4, &rc);
+    if (rc) return rc;
+    int32_t *start = tmp, *mcnt = tmp + (next_id + 1), *cbase = tmp + 2 * (next_id + 1);
+    C2_TRY(scan_exclusive(ctx, size, start, next_id));
+    k_chunk_count<<<nblk(next_id), 256, 0, st>>>(size, next_id, N, mcnt);
+    C2_LAUNCHED(ctx, "k_chunk_count");
+    C2_TRY(scan_exclusive(ctx, mcnt, cbase, next_id));
+    // flat index -> (key) pairs
+    C2_TRY(fill_key_pairs(ctx, key, TN, skey2, sval2));
+    C2_TRY(radix_sort_pairs(ctx, skey2, sval2, skey, sval, TN, bits_for(next_id)));
+    k_chunk_assign<<<nblk(TN), 256, 0, st>>>(skey, sval, TN, size, start, cbase, N, (int32_t)next_id, key);
+    C2_LAUNCHED(ctx, "k_chunk_assign");
+    C2_CUDA(ctx, cudaMemcpyAsync(hsmall, cbase + next_id, 4, cudaMemcpyDeviceToHost, st));
+    int32_t *nbig = (int32_t *)(acc + 3);
+    C2_CUDA(ctx, cudaMemsetAsync(nbig, 0, 4, st));
+    C2_TRY(count_gt(ctx, size, next_id, N, nbig));
+    C2_CUDA(ctx, cudaMemcpyAsync(hsmall + 1, nbig, 4, cudaMemcpyDeviceToHost, st));
+    C2_TRY(stream_sync(ctx, "chunk guard"));
+    int64_t nchunks = hsmall[0];
+    chunked = hsmall[1];
+    next_id += nchunks;
+    size = (int32_t *)ws_get(ctx, "nsize", (size_t)(next_id + 1) * 4, &rc);
+    if (rc) return rc;
+    C2_CUDA(ctx, cudaMemsetAsync(size, 0, (size_t)next_id * 4, st));
+    k_count_keys<<<nblk(TN), 256, 0, st>>>(key, TN, size);
+    C2_LAUNCHED(ctx, "k_count_keys");
+  }
+  // rep[node] = smallest member; heads; canonical cluster index by scan over users
+  int32_t *rep = (int32_t *)ws_get(ctx, "rep", (size_t)next_id * 4, &rc);
+  if (rc) return rc;
+  C2_CUDA(ctx, cudaMemsetAsync(rep, 0x7F, (size_t)next_id * 4, st));
+  k_rep<<<nblk(TN), 256, 0, st>>>(key, TN, n, rep);
+  C2_LAUNCHED(ctx, "k_rep");
+  int32_t *head = (int32_t *)ws_get(ctx, "head", (size_t)(2 * TN + 2) * 4, &rc);
+  if (rc) return rc;
+  int32_t *hscan = head + TN + 1;
+  k_heads<<<nblk(TN), 256, 0, st>>>(key, rep, TN, n, head);
+  C2_LAUNCHED(ctx, "k_heads");
+  C2_TRY(scan_exclusive(ctx, head, hscan, TN));
+  const int64_t TN1 = (int64_t)t * (n + 1);
+  int32_t *csize = (int32_t *)ws_get(ctx, "csize", (size_t)(2 * TN1 + 2) * 4, &rc);
+  if (rc) return rc;
+  int32_t *craw = csize + TN1 + 1;
+  C2_CUDA(ctx, cudaMemsetAsync(csize, 0, (size_t)TN1 * 4, st));
+  k_cluster_of<<<nblk(TN), 256, 0, st>>>(key, rep, hscan, size, TN, n, out->cluster_of, csize, skey2, sval2);
+  C2_LAUNCHED(ctx, "k_cluster_of");
+  C2_TRY(scan_exclusive(ctx, csize, craw, TN1));
+  k_fix_offsets<<<nblk(TN1), 256, 0, st>>>(craw, TN1, n, out->offsets);
+  C2_LAUNCHED(ctx, "k_fix_offsets");
+  // members: stable sort of (f*n + cluster, u) by key -> ascending members per cluster
+  C2_TRY(radix_sort_pairs(ctx, skey2, sval2, skey, (uint32_t *)out->members, TN, bits_for(TN)));
+  C2_CUDA(ctx, cudaMemsetAsync(acc, 0, 8, st));
+  k_pairs<<<nblk(TN1), 256, 0, st>>>(csize, TN1, acc);
+  C2_LAUNCHED(ctx, "k_pairs");
+  C2_CUDA(ctx, cudaMemsetAsync(mx, 0, 4, st));
+  k_max<<<nblk(TN1), 256, 0, st>>>(csize, TN1, mx);
+  C2_LAUNCHED(ctx, "k_max");
+  // host values: n_clusters[f] = hscan[(f+1)n] - hscan[fn], P, max size
+  int32_t *hh = (int32_t *)ctx->h_small + 16;
+  for (int f = 0; f <= t; ++f)
+    C2_CUDA(ctx, cudaMemcpyAsync(hh + f, hscan + (int64_t)f * n, 4, cudaMemcpyDeviceToHost, st));
+  C2_CUDA(ctx, cudaMemcpyAsync(ctx->h_small, acc, 8, cudaMemcpyDeviceToHost, st));
+  C2_CUDA(ctx, cudaMemcpyAsync(ctx->h_small + 1, mx, 4, cudaMemcpyDeviceToHost, st));
+  C2_TRY(stream_sync(ctx, "canonical"));
+  int64_t total = 0;
+  for (int f = 0; f < t; ++f) {
+    out->n_clusters[f] = hh[f + 1] - hh[f];
+    total += out->n_clusters[f];
+  }
+  out->max_size = (int32_t)(ctx->h_small[1] & 0xffffffff);
+  ctx->stats.pairs = ctx->h_small[0];
+  ctx->stats.clusters = total;
+  ctx->stats.max_cluster_size = out->max_size;
+  ctx->stats.split_nodes = split_nodes;
+  ctx->stats.max_depth = max_depth;
+  ctx->stats.folded_singletons = folded;
+  ctx->stats.chunked_residuals = chunked;
+  if (ctx->timing) cudaEventRecord(ev[3], st);
+  return C2_OK;
+}
+
+}  // namespace c2

@@ -1,0 +1,92 @@
+// k_merge.cu -- Step 3 of C^2 on the GPU: Alg. 3.  Each user's t partial
+// neighbourhoods (sorted best-first by c2_local_knn) are merged keeping the k best; the
+// similarity values are reused, never recomputed.  Because the lists are sorted under
+// one strict total order and a repeated id carries identical (inter, uni) (A16), a head-
+// comparison t-way merge that skips an id equal to the last one emitted yields exactly the
+// first k distinct ids of the union.  One thread per user; heads held in registers.
+#include "c2_internal.cuh"
+
+namespace c2 {
+
+template <int TMAX>
+__global__ void __launch_bounds__(128) k_merge(const c2_cand *__restrict__ cand, int t, int32_t n, int k,
+                                               int32_t *__restrict__ nbr, uint16_t *__restrict__ inter,
+                                               uint16_t *__restrict__ uni, float *__restrict__ sim) {
+  int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (u >= n) return;
+  int pos[TMAX];
+  int32_t hid[TMAX];
+  uint32_t hi[TMAX], hU[TMAX];
+#pragma unroll
+  for (int f = 0; f < TMAX; ++f) {
+    pos[f] = 0;
+    hid[f] = -1;
+    hi[f] = 0;
+    hU[f] = 1;
+    if (f < t) {
+      c2_cand e = cand[((int64_t)f * n + u) * k];
+      hid[f] = e.id;
+      hi[f] = e.inter;
+      hU[f] = e.uni;
+    }
+  }
+  int cnt = 0;
+  int32_t last = -1;
+  int32_t *onb = nbr + u * k;
+  uint16_t *oi = inter + u * k, *ou = uni + u * k;
+  float *os = sim ? sim + u * k : nullptr;
+  while (cnt < k) {
+    int bf = -1;
+    int32_t bid = -1;
+    uint32_t bi = 0, bU = 1;
+#pragma unroll
+    for (int f = 0; f < TMAX; ++f) {
+      if (f < t && hid[f] >= 0 && (bf < 0 || c2d::better(hi[f], hU[f], hid[f], bi, bU, bid))) {
+        bf = f;
+        bid = hid[f];
+        bi = hi[f];
+        bU = hU[f];
+      }
+    }
+    if (bf < 0) break;  // all lists exhausted
+#pragma unroll
+    for (int f = 0; f < TMAX; ++f) {
+      if (f == bf) {
+        int p = ++pos[f];
+        if (p < k) {
+          c2_cand e = cand[((int64_t)f * n + u) * k + p];
+          hid[f] = e.id;
+          hi[f] = e.inter;
+          hU[f] = e.uni;
+        } else {
+          hid[f] = -1;
+        }
+      }
+    }
+    if (bid == last) continue;  // same id from another function: identical values (A16)
+    last = bid;
+    onb[cnt] = bid;
+    oi[cnt] = (uint16_t)bi;
+    ou[cnt] = (uint16_t)bU;
+    if (os) os[cnt] = __fdiv_rn((float)bi, (float)bU);
+    ++cnt;
+  }
+  for (; cnt < k; ++cnt) {
+    onb[cnt] = -1;
+    oi[cnt] = 0;
+    ou[cnt] = 0;
+    if (os) os[cnt] = 0.0f;
+  }
+}
+
+int merge(c2_ctx *ctx, int t, int n, int k, const c2_cand *cand, int32_t *nbr, uint16_t *inter, uint16_t *uni,
+          float *sim) {
+  unsigned blocks = (unsigned)((n + 127) / 128);
+  if (t <= 8) k_merge<8><<<blocks, 128, 0, ctx->stream>>>(cand, t, n, k, nbr, inter, uni, sim);
+  else if (t <= 16) k_merge<16><<<blocks, 128, 0, ctx->stream>>>(cand, t, n, k, nbr, inter, uni, sim);
+  else k_merge<64><<<blocks, 128, 0, ctx->stream>>>(cand, t, n, k, nbr, inter, uni, sim);
+  C2_LAUNCHED(ctx, "k_merge");
+  return C2_OK;
+}
+
+}  // namespace c2

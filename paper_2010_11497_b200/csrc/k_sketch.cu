@@ -1,0 +1,163 @@
+// k_sketch.cu -- K1 FastRandomHash sketch and K6 GoldFinger encode.
+//
+// K1: for every user u and function f, the D smallest DISTINCT values of {h_f(x) : x in P_u}
+// (ascending, C2_ABSENT padded).  Element 0 is H_f(u) = min_{i in P_u} h_f(i); element
+// d+1 is H\eta(u) with eta = element d (reading A5), so the recursive split never has to
+// revisit the CSR while its depth stays below D (A29).  One pass over the item list computes
+// all t functions (TF per pass), keeping a sorted distinct top-8 per function in registers.
+#include "c2_internal.cuh"
+
+namespace c2 {
+
+struct HashArgs {
+  uint64_t a[C2_MAX_T];
+  uint64_t c[C2_MAX_T];
+};
+
+template <int TF, bool TABLE>
+__global__ void __launch_bounds__(256) k_sketch(const int32_t *__restrict__ offs, const int32_t *__restrict__ items,
+                                                int32_t n, int t, int f0, uint32_t b, HashArgs ha,
+                                                const uint16_t *__restrict__ htab, int32_t m, int D,
+                                                uint16_t *__restrict__ out) {
+  int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (u >= n) return;
+  uint32_t s[TF][C2_SKETCH_D];
+#pragma unroll
+  for (int f = 0; f < TF; ++f)
+#pragma unroll
+    for (int j = 0; j < C2_SKETCH_D; ++j) s[f][j] = C2_ABSENT16;
+  int32_t p0 = offs[u], p1 = offs[u + 1];
+  for (int32_t p = p0; p < p1; ++p) {
+    uint32_t x = (uint32_t)__ldg(items + p);
+#pragma unroll
+    for (int f = 0; f < TF; ++f) {
+      if (f0 + f >= t) break;
+      uint32_t v = TABLE ? (uint32_t)__ldg(htab + (int64_t)(f0 + f) * m + x)
+                         : c2d::item_hash(ha.a[f0 + f], ha.c[f0 + f], x, b);
+      if (v < s[f][C2_SKETCH_D - 1]) {
+        bool dup = false;
+#pragma unroll
+        for (int j = 0; j < C2_SKETCH_D - 1; ++j) dup |= (s[f][j] == v);
+        if (!dup) {  // insert v into the sorted distinct list
+#pragma unroll
+          for (int j = C2_SKETCH_D - 1; j >= 1; --j)
+            s[f][j] = (v < s[f][j - 1]) ? s[f][j - 1] : ((v < s[f][j]) ? v : s[f][j]);
+          s[f][0] = min(s[f][0], v);
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int f = 0; f < TF; ++f) {
+    if (f0 + f >= t) break;
+    uint16_t *o = out + ((int64_t)(f0 + f) * n + u) * D;
+    if (D == C2_SKETCH_D) {
+      uint4 w;
+      w.x = s[f][0] | (s[f][1] << 16);
+      w.y = s[f][2] | (s[f][3] << 16);
+      w.z = s[f][4] | (s[f][5] << 16);
+      w.w = s[f][6] | (s[f][7] << 16);
+      *reinterpret_cast<uint4 *>(o) = w;
+    } else {
+#pragma unroll
+      for (int j = 0; j < C2_SKETCH_D; ++j)
+        if (j < D) o[j] = (uint16_t)s[f][j];
+    }
+  }
+}
+
+int sketch(c2_ctx *ctx, const Csr &csr, int t, int b, const HashParams *hp, const uint16_t *htab, int32_t m, int D,
+           uint16_t *out) {
+  HashArgs ha;
+  for (int f = 0; f < t; ++f) {
+    ha.a[f] = hp ? hp->a[f] : 0;
+    ha.c[f] = hp ? hp->c[f] : 0;
+  }
+  constexpr int TF = 8;
+  unsigned blocks = (unsigned)((csr.n + 255) / 256);
+  for (int f0 = 0; f0 < t; f0 += TF) {
+    if (htab)
+      k_sketch<TF, true><<<blocks, 256, 0, ctx->stream>>>(csr.offs, csr.items, csr.n, t, f0, (uint32_t)b, ha, htab,
+                                                          m, D, out);
+    else
+      k_sketch<TF, false><<<blocks, 256, 0, ctx->stream>>>(csr.offs, csr.items, csr.n, t, f0, (uint32_t)b, ha,
+                                                           nullptr, 0, D, out);
+    C2_LAUNCHED(ctx, "k_sketch");
+  }
+  return C2_OK;
+}
+
+// ---------------------------------------------------------------- K6 GoldFinger encode
+// F_u = OR over x in P_u of bit g(x), g(x) = floor(((a_g*x + c_g) mod 2^64) * 1024 / 2^64)
+// (reading A19).  The fingerprint is materialised as the ascending list of its set
+// bit positions, so the local kernel runs unchanged on it: |F_u AND F_v| is the size of the
+// intersection of the two lists, pc(F_u) the list length.  Warp per user; word w of the
+// 1024-bit vector is owned by lane w.
+__global__ void __launch_bounds__(256) k_gf_bits(const int32_t *__restrict__ offs, const int32_t *__restrict__ items,
+                                                 int32_t n, uint64_t ga, uint64_t gc, uint32_t *__restrict__ words,
+                                                 int32_t *__restrict__ pc) {
+  __shared__ uint32_t bm[8][32];
+  int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  int64_t u = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (u >= n) return;
+  bm[w][lane] = 0;
+  __syncwarp();
+  for (int32_t p = offs[u] + lane; p < offs[u + 1]; p += 32) {
+    uint32_t bit = c2d::item_hash(ga, gc, (uint32_t)items[p], 1024u);
+    atomicOr(&bm[w][bit >> 5], 1u << (bit & 31));
+  }
+  __syncwarp();
+  uint32_t word = bm[w][lane];
+  words[u * 32 + lane] = word;
+  int c = __popc(word);
+#pragma unroll
+  for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+  if (lane == 0) pc[u] = c;
+}
+
+__global__ void __launch_bounds__(256) k_gf_list(const uint32_t *__restrict__ words, const int32_t *__restrict__ goffs,
+                                                 int32_t n, int32_t *__restrict__ gitems) {
+  int lane = threadIdx.x & 31;
+  int64_t u = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (u >= n) return;
+  uint32_t word = words[u * 32 + lane];
+  int c = __popc(word);
+  int pos = c2d::warp_incl_scan(c) - c + goffs[u];
+  while (word) {
+    int bpos = __ffs(word) - 1;
+    word &= word - 1;
+    gitems[pos++] = lane * 32 + bpos;
+  }
+}
+
+int gf_encode(c2_ctx *ctx, const Csr &csr, const HashParams *hp, Csr *gf) {
+  int rc;
+  int n = csr.n;
+  uint32_t *words = (uint32_t *)ws_get(ctx, "gf_words", (size_t)n * 128, &rc);
+  if (rc) return rc;
+  int32_t *pc = (int32_t *)ws_get(ctx, "gf_pc", (size_t)n * 4, &rc);
+  if (rc) return rc;
+  int32_t *goffs = (int32_t *)ws_get(ctx, "gf_offs", (size_t)(n + 1) * 4, &rc);
+  if (rc) return rc;
+  unsigned blocks = (unsigned)(((int64_t)n * 32 + 255) / 256);
+  k_gf_bits<<<blocks, 256, 0, ctx->stream>>>(csr.offs, csr.items, n, hp->ga, hp->gc, words, pc);
+  C2_LAUNCHED(ctx, "k_gf_bits");
+  C2_TRY(scan_exclusive(ctx, pc, goffs, n));
+  int32_t total;
+  C2_CUDA(ctx, cudaMemcpyAsync(&total, goffs + n, 4, cudaMemcpyDeviceToHost, ctx->stream));
+  C2_TRY(stream_sync(ctx, "gf_encode"));
+  int32_t *gitems = (int32_t *)ws_get(ctx, "gf_items", (size_t)total * 4 + 16, &rc);
+  if (rc) return rc;
+  k_gf_list<<<blocks, 256, 0, ctx->stream>>>(words, goffs, n, gitems);
+  C2_LAUNCHED(ctx, "k_gf_list");
+  gf->offs = goffs;
+  gf->items = gitems;
+  gf->n = n;
+  gf->nnz = total;
+  gf->psize = pc;
+  gf->max_item = 1023;
+  gf->max_len = csr.max_len < 1024 ? csr.max_len : 1024;
+  return C2_OK;
+}
+
+}  // namespace c2
