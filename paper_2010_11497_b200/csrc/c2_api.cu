@@ -81,11 +81,13 @@ int build_device(c2_ctx *ctx, const int32_t *offs, const int32_t *items, int32_t
   Csr sims = csr;
   if (sim_mode == C2_SIM_GF1024) C2_TRY(gf_encode(ctx, csr, &hp, &sims));
   int rc;
-  c2_cand *cand = (c2_cand *)ws_get(ctx, "cand", (size_t)t * n * k * sizeof(c2_cand), &rc);
+  // Steps 2+3 fused: function by function, every local neighbourhood is merged into the
+  // running Alg. 3 result; the final lists equal merge(local lists) exactly.
+  c2_cand *run = (c2_cand *)ws_get(ctx, "runlist", (size_t)n * k * sizeof(c2_cand), &rc);
   if (rc) return rc;
-  C2_TRY(local_knn(ctx, sims, t, cl, k, cand));
+  C2_TRY(local_knn(ctx, sims, t, cl, k, run, true));
   if (ctx->timing) cudaEventRecord(ctx->ev[4], st);
-  C2_TRY(merge(ctx, t, n, k, cand, nbr, inter, uni, sim));
+  C2_TRY(merge(ctx, 1, n, k, run, nbr, inter, uni, sim));
   if (ctx->timing) cudaEventRecord(ctx->ev[5], st);
   return C2_OK;
 }
@@ -244,7 +246,7 @@ int c2_local_knn(c2_ctx *ctx, const int32_t *csr_offsets, const int32_t *item_id
   cl.max_size = hmx;
   Csr sims = csr;
   if (sim_mode == C2_SIM_GF1024) C2_TRY(gf_encode(ctx, csr, &hp, &sims));
-  return local_knn(ctx, sims, t, cl, k, cand);
+  return local_knn(ctx, sims, t, cl, k, cand, false);
 }
 
 int c2_merge(c2_ctx *ctx, int32_t t, int32_t n_users, int32_t k, const c2_cand *cand, int32_t *nbr,

@@ -89,7 +89,9 @@ int fastrandomhash(c2_ctx *ctx, const Csr &csr, int t, int b, int64_t N, const H
 
 // Step 2 (k_local.cu).
 int gf_encode(c2_ctx *ctx, const Csr &csr, const HashParams *hp, Csr *gf);
-int local_knn(c2_ctx *ctx, const Csr &csr, int t, const Clusters &cl, int k, c2_cand *cand);
+// fused=false: cand [t][n][k] per-function lists (c2_local_knn).  fused=true: out = the running
+// final lists [n][k] (Alg. 3 applied function by function, c2_build).
+int local_knn(c2_ctx *ctx, const Csr &csr, int t, const Clusters &cl, int k, c2_cand *out, bool fused);
 
 // Step 3 (k_merge.cu).
 int merge(c2_ctx *ctx, int t, int n, int k, const c2_cand *cand, int32_t *nbr, uint16_t *inter, uint16_t *uni,
@@ -138,6 +140,12 @@ __device__ __forceinline__ int warp_incl_scan(int v) {
     if (lane >= o) v += y;
   }
   return v;
+}
+
+// Warp-aggregated counter increment: lanes of `mask` with equal `key` add their count once.
+__device__ __forceinline__ void agg_inc(unsigned mask, int32_t *ctr, int32_t key) {
+  unsigned peers = __match_any_sync(mask, key);
+  if ((int)(threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(ctr, __popc(peers));
 }
 
 }  // namespace c2d

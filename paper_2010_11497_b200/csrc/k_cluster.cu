@@ -27,13 +27,15 @@ struct HashArgs2 {
 __global__ void k_level0(const uint16_t *__restrict__ sk, int64_t TN, int32_t n, int32_t b,
                          int32_t *__restrict__ key, uint16_t *__restrict__ curval, int32_t *__restrict__ size0) {
   int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (q >= TN) return;
+  const bool valid = q < TN;
+  const unsigned mask = __ballot_sync(0xffffffffu, valid);
+  if (!valid) return;
   int32_t f = (int32_t)(q / n);
   uint16_t v = sk[q * C2_SKETCH_D];  // H_f(u)
   int32_t k = f * b + v;
   key[q] = k;
   curval[q] = v;
-  atomicAdd(&size0[k], 1);
+  c2d::agg_inc(mask, &size0[k], k);
 }
 
 __global__ void k_flag_gt(const int32_t *__restrict__ cnt, int64_t E, int64_t N, int32_t *__restrict__ flag) {
@@ -79,7 +81,7 @@ __global__ void k_split_count(const int32_t *__restrict__ slot, const uint16_t *
   if (d + 1 < Deff) nv = sk[q * C2_SKETCH_D + d + 1];
   else nv = next_above<TABLE>(offs, items, (int32_t)(q % n), (int)(q / n), curval[q], (uint32_t)b, ha, htab, m);
   nextval[q] = nv;
-  if (nv != C2_ABSENT16) atomicAdd(&hist[(int64_t)(s - a0) * b + nv], 1);
+  if (nv != C2_ABSENT16) atomicAdd(&hist[(int64_t)(s - a0) * b + nv], 1);  // (spread over b bins)
 }
 
 __global__ void k_child_flags(const int32_t *__restrict__ hist, int64_t E, int64_t N, int32_t *__restrict__ fc,
@@ -131,7 +133,11 @@ __global__ void k_split_apply(int32_t *__restrict__ slot, int32_t *__restrict__ 
 // ------------------------------------------------------------------ canonical form
 __global__ void k_count_keys(const int32_t *__restrict__ key, int64_t TN, int32_t *__restrict__ size) {
   int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (q < TN) atomicAdd(&size[key[q]], 1);
+  const bool valid = q < TN;
+  const unsigned mask = __ballot_sync(0xffffffffu, valid);
+  if (!valid) return;
+  int32_t k = key[q];
+  c2d::agg_inc(mask, &size[k], k);
 }
 
 __global__ void k_max(const int32_t *__restrict__ x, int64_t E, int32_t *__restrict__ out) {

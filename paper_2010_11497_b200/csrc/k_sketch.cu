@@ -14,56 +14,62 @@ struct HashArgs {
   uint64_t c[C2_MAX_T];
 };
 
-template <int TF, bool TABLE>
+// G consecutive lanes share one user (its items are loaded once, broadcast to the group) and
+// lane g of the group handles function f0 + g, so a warp covers 32/G users.
+template <int G, bool TABLE>
 __global__ void __launch_bounds__(256) k_sketch(const int32_t *__restrict__ offs, const int32_t *__restrict__ items,
                                                 int32_t n, int t, int f0, uint32_t b, HashArgs ha,
                                                 const uint16_t *__restrict__ htab, int32_t m, int D,
                                                 uint16_t *__restrict__ out) {
-  int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  int64_t gt = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  int64_t u = gt / G;
+  int f = f0 + (int)(gt % G);
   if (u >= n) return;
-  uint32_t s[TF][C2_SKETCH_D];
+  const bool active = f < t;
+  const uint64_t ca = active ? ha.a[f] : 0, cc = active ? ha.c[f] : 0;
+  uint32_t s[C2_SKETCH_D];
 #pragma unroll
-  for (int f = 0; f < TF; ++f)
-#pragma unroll
-    for (int j = 0; j < C2_SKETCH_D; ++j) s[f][j] = C2_ABSENT16;
-  int32_t p0 = offs[u], p1 = offs[u + 1];
+  for (int j = 0; j < C2_SKETCH_D; ++j) s[j] = C2_ABSENT16;
+  const int32_t p0 = offs[u], p1 = offs[u + 1];
   for (int32_t p = p0; p < p1; ++p) {
     uint32_t x = (uint32_t)__ldg(items + p);
+    uint32_t v = TABLE ? (active ? (uint32_t)__ldg(htab + (int64_t)f * m + x) : C2_ABSENT16)
+                       : c2d::item_hash(ca, cc, x, b);
+    if (v < s[C2_SKETCH_D - 1]) {
+      bool dup = false;
 #pragma unroll
-    for (int f = 0; f < TF; ++f) {
-      if (f0 + f >= t) break;
-      uint32_t v = TABLE ? (uint32_t)__ldg(htab + (int64_t)(f0 + f) * m + x)
-                         : c2d::item_hash(ha.a[f0 + f], ha.c[f0 + f], x, b);
-      if (v < s[f][C2_SKETCH_D - 1]) {
-        bool dup = false;
+      for (int j = 0; j < C2_SKETCH_D - 1; ++j) dup |= (s[j] == v);
+      if (!dup) {  // insert v into the sorted distinct list
 #pragma unroll
-        for (int j = 0; j < C2_SKETCH_D - 1; ++j) dup |= (s[f][j] == v);
-        if (!dup) {  // insert v into the sorted distinct list
-#pragma unroll
-          for (int j = C2_SKETCH_D - 1; j >= 1; --j)
-            s[f][j] = (v < s[f][j - 1]) ? s[f][j - 1] : ((v < s[f][j]) ? v : s[f][j]);
-          s[f][0] = min(s[f][0], v);
-        }
+        for (int j = C2_SKETCH_D - 1; j >= 1; --j) s[j] = (v < s[j - 1]) ? s[j - 1] : ((v < s[j]) ? v : s[j]);
+        s[0] = min(s[0], v);
       }
     }
   }
+  if (!active) return;
+  uint16_t *o = out + ((int64_t)f * n + u) * D;
+  if (D == C2_SKETCH_D) {
+    *reinterpret_cast<uint4 *>(o) = make_uint4(s[0] | (s[1] << 16), s[2] | (s[3] << 16), s[4] | (s[5] << 16),
+                                               s[6] | (s[7] << 16));
+  } else {
 #pragma unroll
-  for (int f = 0; f < TF; ++f) {
-    if (f0 + f >= t) break;
-    uint16_t *o = out + ((int64_t)(f0 + f) * n + u) * D;
-    if (D == C2_SKETCH_D) {
-      uint4 w;
-      w.x = s[f][0] | (s[f][1] << 16);
-      w.y = s[f][2] | (s[f][3] << 16);
-      w.z = s[f][4] | (s[f][5] << 16);
-      w.w = s[f][6] | (s[f][7] << 16);
-      *reinterpret_cast<uint4 *>(o) = w;
-    } else {
-#pragma unroll
-      for (int j = 0; j < C2_SKETCH_D; ++j)
-        if (j < D) o[j] = (uint16_t)s[f][j];
-    }
+    for (int j = 0; j < C2_SKETCH_D; ++j)
+      if (j < D) o[j] = (uint16_t)s[j];
   }
+}
+
+template <int G>
+static int launch_sketch(c2_ctx *ctx, const Csr &csr, int t, int f0, int b, const HashArgs &ha,
+                         const uint16_t *htab, int32_t m, int D, uint16_t *out) {
+  unsigned blocks = (unsigned)(((int64_t)csr.n * G + 255) / 256);
+  if (htab)
+    k_sketch<G, true><<<blocks, 256, 0, ctx->stream>>>(csr.offs, csr.items, csr.n, t, f0, (uint32_t)b, ha, htab, m,
+                                                       D, out);
+  else
+    k_sketch<G, false><<<blocks, 256, 0, ctx->stream>>>(csr.offs, csr.items, csr.n, t, f0, (uint32_t)b, ha, nullptr,
+                                                        0, D, out);
+  C2_LAUNCHED(ctx, "k_sketch");
+  return C2_OK;
 }
 
 int sketch(c2_ctx *ctx, const Csr &csr, int t, int b, const HashParams *hp, const uint16_t *htab, int32_t m, int D,
@@ -73,16 +79,11 @@ int sketch(c2_ctx *ctx, const Csr &csr, int t, int b, const HashParams *hp, cons
     ha.a[f] = hp ? hp->a[f] : 0;
     ha.c[f] = hp ? hp->c[f] : 0;
   }
-  constexpr int TF = 8;
-  unsigned blocks = (unsigned)((csr.n + 255) / 256);
-  for (int f0 = 0; f0 < t; f0 += TF) {
-    if (htab)
-      k_sketch<TF, true><<<blocks, 256, 0, ctx->stream>>>(csr.offs, csr.items, csr.n, t, f0, (uint32_t)b, ha, htab,
-                                                          m, D, out);
-    else
-      k_sketch<TF, false><<<blocks, 256, 0, ctx->stream>>>(csr.offs, csr.items, csr.n, t, f0, (uint32_t)b, ha,
-                                                           nullptr, 0, D, out);
-    C2_LAUNCHED(ctx, "k_sketch");
+  for (int f0 = 0; f0 < t; f0 += 8) {
+    int rem = t - f0;
+    if (rem <= 2) C2_TRY(launch_sketch<2>(ctx, csr, t, f0, b, ha, htab, m, D, out));
+    else if (rem <= 4) C2_TRY(launch_sketch<4>(ctx, csr, t, f0, b, ha, htab, m, D, out));
+    else C2_TRY(launch_sketch<8>(ctx, csr, t, f0, b, ha, htab, m, D, out));
   }
   return C2_OK;
 }
