@@ -166,6 +166,10 @@ typedef struct {
   int64_t launches;          /* kernels launched by the last entry point */
   int64_t host_syncs;        /* stream synchronisations in the last entry point */
   double ms_sketch, ms_cluster, ms_local, ms_merge, ms_total; /* with C2_OPT_TIMING */
+  int64_t work_steps;    /* sum over unordered local pairs of |P_u|+|P_v|: the element comparisons of
+                            a two-pointer intersection (algorithmic work unit of Step 2) */
+  int64_t tile_launches; /* launches of the local tile kernel (K7) in the last call */
+  double ms_tile;        /* with C2_OPT_TIMING: summed CUDA-event duration of those launches */
 } c2_stats;
 /* Statistics of the last c2_fastrandomhash / c2_local_knn / c2_merge / c2_build call. */
 C2_API int c2_get_stats(const c2_ctx *ctx, c2_stats *out);

@@ -46,7 +46,8 @@ class _Clusters(ctypes.Structure):
 class Stats(ctypes.Structure):
     _fields_ = [(k, ctypes.c_int64) for k in ("pairs", "clusters", "max_cluster_size", "split_nodes", "max_depth",
                                               "folded_singletons", "chunked_residuals", "launches", "host_syncs")] + \
-               [(k, ctypes.c_double) for k in ("ms_sketch", "ms_cluster", "ms_local", "ms_merge", "ms_total")]
+               [(k, ctypes.c_double) for k in ("ms_sketch", "ms_cluster", "ms_local", "ms_merge", "ms_total")] + \
+               [("work_steps", ctypes.c_int64), ("tile_launches", ctypes.c_int64), ("ms_tile", ctypes.c_double)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}

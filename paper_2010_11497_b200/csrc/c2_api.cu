@@ -32,6 +32,9 @@ int check_k(c2_ctx *ctx, int32_t k, int32_t sim_mode) {
 void begin(c2_ctx *ctx) {
   ctx->stats.launches = 0;
   ctx->stats.host_syncs = 0;
+  ctx->stats.tile_launches = 0;
+  ctx->stats.ms_tile = 0;
+  ctx->tile_ev_used = 0;
   ctx->err[0] = 0;
   cudaSetDevice(ctx->device);
 }
@@ -83,11 +86,12 @@ int build_device(c2_ctx *ctx, const int32_t *offs, const int32_t *items, int32_t
   int rc;
   // Steps 2+3 fused: function by function, every local neighbourhood is merged into the
   // running Alg. 3 result; the final lists equal merge(local lists) exactly.
-  c2_cand *run = (c2_cand *)ws_get(ctx, "runlist", (size_t)n * k * sizeof(c2_cand), &rc);
+  c2_cand *run = (c2_cand *)ws_get(ctx, "runlist", (size_t)2 * n * k * sizeof(c2_cand), &rc);
   if (rc) return rc;
-  C2_TRY(local_knn(ctx, sims, t, cl, k, run, true));
+  c2_cand *fin = nullptr;
+  C2_TRY(local_knn(ctx, sims, t, cl, k, run, true, &fin));
   if (ctx->timing) cudaEventRecord(ctx->ev[4], st);
-  C2_TRY(merge(ctx, 1, n, k, run, nbr, inter, uni, sim));
+  C2_TRY(merge(ctx, 1, n, k, fin, nbr, inter, uni, sim));
   if (ctx->timing) cudaEventRecord(ctx->ev[5], st);
   return C2_OK;
 }
@@ -100,6 +104,9 @@ void collect_timing(c2_ctx *ctx) {
   ctx->stats.ms_local = ev_ms(ctx->ev[3], ctx->ev[4]);
   ctx->stats.ms_merge = ev_ms(ctx->ev[4], ctx->ev[5]);
   ctx->stats.ms_total = ev_ms(ctx->ev[6], ctx->ev[5]);
+  double mt = 0;
+  for (int i = 0; i < ctx->tile_ev_used; ++i) mt += ev_ms(ctx->tile_ev[2 * i], ctx->tile_ev[2 * i + 1]);
+  ctx->stats.ms_tile = mt;
 }
 
 }  // namespace
@@ -146,6 +153,7 @@ void c2_ctx_destroy(c2_ctx *ctx) {
   for (auto &kv : ctx->ws) cudaFree(kv.second.first);
   for (auto &e : ctx->ev)
     if (e) cudaEventDestroy(e);
+  for (auto &e : ctx->tile_ev) cudaEventDestroy(e);
   if (ctx->h_small) cudaFreeHost(ctx->h_small);
   if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
   delete ctx;
@@ -246,7 +254,7 @@ int c2_local_knn(c2_ctx *ctx, const int32_t *csr_offsets, const int32_t *item_id
   cl.max_size = hmx;
   Csr sims = csr;
   if (sim_mode == C2_SIM_GF1024) C2_TRY(gf_encode(ctx, csr, &hp, &sims));
-  return local_knn(ctx, sims, t, cl, k, cand, false);
+  return local_knn(ctx, sims, t, cl, k, cand, false, nullptr);
 }
 
 int c2_merge(c2_ctx *ctx, int32_t t, int32_t n_users, int32_t k, const c2_cand *cand, int32_t *nbr,

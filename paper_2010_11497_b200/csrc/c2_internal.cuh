@@ -6,6 +6,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <map>
+#include <vector>
 #include <string>
 
 #include "../../include/c2.h"
@@ -33,6 +34,8 @@ struct c2_ctx {
   int64_t *h_small = nullptr;
   int64_t *d_small = nullptr;
   cudaEvent_t ev[8] = {nullptr};
+  std::vector<cudaEvent_t> tile_ev;  // pairs of events around K7 launches (C2_OPT_TIMING)
+  int tile_ev_used = 0;
 };
 
 namespace c2 {
@@ -90,8 +93,9 @@ int fastrandomhash(c2_ctx *ctx, const Csr &csr, int t, int b, int64_t N, const H
 // Step 2 (k_local.cu).
 int gf_encode(c2_ctx *ctx, const Csr &csr, const HashParams *hp, Csr *gf);
 // fused=false: cand [t][n][k] per-function lists (c2_local_knn).  fused=true: out = the running
-// final lists [n][k] (Alg. 3 applied function by function, c2_build).
-int local_knn(c2_ctx *ctx, const Csr &csr, int t, const Clusters &cl, int k, c2_cand *out, bool fused);
+// final lists (2*n*k entries, ping-pong; Alg. 3 applied function by function, c2_build).
+int local_knn(c2_ctx *ctx, const Csr &csr, int t, const Clusters &cl, int k, c2_cand *out, bool fused,
+              c2_cand **result);
 
 // Step 3 (k_merge.cu).
 int merge(c2_ctx *ctx, int t, int n, int k, const c2_cand *cand, int32_t *nbr, uint16_t *inter, uint16_t *uni,

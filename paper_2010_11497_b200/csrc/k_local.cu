@@ -16,11 +16,11 @@
 //    x in P_r} (bit r).  Each thread owns VPT slices' lanes (one v each) and accumulates the
 //    32 counts |P_r ∩ P_v| bit-sliced with Harley-Seal carry-save adders over 16 masks, so
 //    one LDS + ~3 LOP3 serve 32 pairs.  A 32x32 bit transpose turns the planes into counts.
-// K8 (in K7): per row, a warp keeps the k best candidates under the exact order
-//    (i1*U2 > i2*U1, ties by lower id) as a warp-distributed sorted list.  In fused mode
-//    (c2_build) the list is seeded with the running Alg. 3 result of the earlier functions,
-//    so only candidates that can still enter the final k-NN are inserted (exact: the k-th
-//    best never decreases), and the result is written back in place of a per-function list.
+// K8 (in K7): per row, one warp selects the k best candidates under the exact order
+//    (i1*U2 > i2*U1, ties by lower id) with a threshold from per-lane top lists (row_topk).
+//    In fused mode (c2_build) it starts from the running Alg. 3 result of the earlier
+//    functions (the k-th best never decreases, so pruning below it is exact) and writes the
+//    merged list, instead of a per-function list.
 #include <algorithm>
 #include <vector>
 
@@ -235,45 +235,270 @@ __global__ void k_sl_fill(const Tile *__restrict__ tiles, int64_t nslices, const
   }
 }
 
-// ------------------------------------------------------------------ K7 small clusters
-constexpr int SMALL_WARPS = 8;
 
-__device__ __forceinline__ void fused_insert(c2_cand *__restrict__ R, int k, int32_t xid, uint32_t xi, uint32_t xU) {
-  // insert x into the sorted list R[0..k) (pads last) unless present or not better than R[k-1]
-  c2_cand last = R[k - 1];
-  if (last.id >= 0 && !c2d::better(xi, xU, xid, last.inter, last.uni, last.id)) return;
-  int pos = k;
-  for (int q = 0; q < k; ++q) {
-    c2_cand e = R[q];
-    if (e.id == xid) return;
-    if (e.id < 0 || c2d::better(xi, xU, xid, e.inter, e.uni, e.id)) {
-      pos = q;
-      break;
+// ------------------------------------------------------------------ candidate lists
+// A candidate (v, i, U) is held as {iu = i | U << 16, id}.  The order (A13): a before b iff
+// a.i * b.U > b.i * a.U, ties by lower id.  SENT is worse than every real candidate.
+struct Cand {
+  uint32_t iu;
+  int32_t id;
+};
+__device__ __forceinline__ Cand sent() { return Cand{1u << 16, INT32_MAX}; }
+__device__ __forceinline__ bool is_real(Cand a) { return a.id != INT32_MAX; }
+__device__ __forceinline__ bool better_c(Cand a, Cand b) {
+  uint32_t l = (a.iu & 0xFFFFu) * (b.iu >> 16), r = (b.iu & 0xFFFFu) * (a.iu >> 16);
+  return l > r || (l == r && a.id < b.id);
+}
+__device__ __forceinline__ Cand shfl_c(Cand a, int src) {
+  return Cand{__shfl_sync(0xffffffffu, a.iu, src), __shfl_sync(0xffffffffu, a.id, src)};
+}
+__device__ __forceinline__ Cand shfl_xor_c(Cand a, int m) {
+  return Cand{__shfl_xor_sync(0xffffffffu, a.iu, m), __shfl_xor_sync(0xffffffffu, a.id, m)};
+}
+__device__ __forceinline__ Cand shfl_up_c(Cand a) {
+  return Cand{__shfl_up_sync(0xffffffffu, a.iu, 1), __shfl_up_sync(0xffffffffu, a.id, 1)};
+}
+__device__ __forceinline__ c2_cand to_out(Cand a) {
+  return is_real(a) ? c2_cand{a.id, (uint16_t)(a.iu & 0xFFFFu), (uint16_t)(a.iu >> 16)} : c2_cand{-1, 0, 0};
+}
+__device__ __forceinline__ Cand from_out(c2_cand e) {
+  return e.id >= 0 ? Cand{(uint32_t)e.inter | ((uint32_t)e.uni << 16), e.id} : sent();
+}
+
+// Bitonic sort of the 32R warp-held elements a[j] (position 32j + lane), best first.
+template <int R>
+__device__ __forceinline__ void warp_sort(Cand (&a)[R]) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int size = 2; size <= 32 * R; size <<= 1) {
+#pragma unroll
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      if (stride >= 32) {
+        const int js = stride >> 5;
+#pragma unroll
+        for (int j = 0; j < R; ++j) {
+          if ((j & js) == 0) {
+            const int p = 32 * j + lane;
+            const bool desc = (p & size) == 0;  // lower position takes the better element
+            Cand x = a[j], y = a[j + js];
+            if (desc ? better_c(y, x) : better_c(x, y)) {
+              a[j] = y;
+              a[j + js] = x;
+            }
+          }
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < R; ++j) {
+          const int p = 32 * j + lane;
+          Cand o = shfl_xor_c(a[j], stride);
+          const bool lower = (lane & stride) == 0;
+          const bool desc = (p & size) == 0;
+          const bool ob = better_c(o, a[j]);
+          // lower position of a descending block keeps the better one
+          if ((lower == desc) ? ob : better_c(a[j], o)) a[j] = o;
+        }
+      }
     }
   }
-  if (pos >= k) return;
-  for (int q = k - 1; q > pos; --q) R[q] = R[q - 1];
-  R[pos] = c2_cand{xid, (uint16_t)xi, (uint16_t)xU};
 }
+
+// Bitonic merge of a bitonic sequence of 32R warp-held elements into best-first order.
+template <int R>
+__device__ __forceinline__ void warp_bitonic_merge(Cand (&a)[R]) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int stride = 16 * R; stride > 0; stride >>= 1) {
+    if (stride >= 32) {
+      const int js = stride >> 5;
+#pragma unroll
+      for (int j = 0; j < R; ++j)
+        if ((j & js) == 0 && better_c(a[j + js], a[j])) {
+          Cand x = a[j];
+          a[j] = a[j + js];
+          a[j + js] = x;
+        }
+    } else {
+#pragma unroll
+      for (int j = 0; j < R; ++j) {
+        Cand o = shfl_xor_c(a[j], stride);
+        const bool lower = (lane & stride) == 0;
+        if (lower ? better_c(o, a[j]) : better_c(a[j], o)) a[j] = o;
+      }
+    }
+  }
+}
+
+// Insert x into the sorted warp list a (32R positions, best first); the worst drops out.
+template <int R>
+__device__ __forceinline__ void warp_insert(Cand (&a)[R], Cand x) {
+  const int lane = threadIdx.x & 31;
+  int pos = 0;
+#pragma unroll
+  for (int j = 0; j < R; ++j) pos += __popc(__ballot_sync(0xffffffffu, better_c(a[j], x)));
+  Cand up[R];
+#pragma unroll
+  for (int j = 0; j < R; ++j) up[j] = shfl_up_c(a[j]);
+#pragma unroll
+  for (int j = 1; j < R; ++j) {
+    Cand last = shfl_c(a[j - 1], 31);
+    if (lane == 0) up[j] = last;
+  }
+#pragma unroll
+  for (int j = 0; j < R; ++j) {
+    const int p = 32 * j + lane;
+    if (p == pos) a[j] = x;
+    else if (p > pos) a[j] = up[j];
+  }
+}
+
+template <int R>
+__device__ __forceinline__ Cand warp_get(const Cand (&a)[R], int p) {
+  Cand r = a[0];
+#pragma unroll
+  for (int j = 1; j < R; ++j)
+    if ((p >> 5) == j) r = a[j];
+  return shfl_c(r, p & 31);
+}
+
+// Exact top-k of one row's candidates (k <= 16R), optionally merged with a seed list S (the
+// running Alg. 3 result, sorted, pads = sentinels), written best-first to dst[0..k).
+//   1. every lane keeps its best R candidates that beat tau = S[k-1] (local top-R), so the
+//      warp holds 32R "tops";
+//   2. sorting the tops gives T = their k-th best: k distinct real candidates are >= T, so T
+//      is <= the row's true k-th best (a valid pruning threshold);
+//   3. candidates >= T that are not among their lane's tops (rare) are inserted;
+//   4. the first k of the tops are top-k(C above tau); merged with S (bitonic merge + removal
+//      of adjacent equal ids: a repeated id carries identical values, A16) -> first k.
+template <int R, class GetC>
+__device__ __forceinline__ void row_topk(int s, int k, GetC get, const c2_cand *seed, c2_cand *dst) {
+  const int lane = threadIdx.x & 31;
+  Cand S[R];
+  Cand tau = sent();
+#pragma unroll
+  for (int j = 0; j < R; ++j) S[j] = sent();
+  if (seed) {
+#pragma unroll
+    for (int j = 0; j < R; ++j)
+      if (32 * j + lane < k) S[j] = from_out(seed[32 * j + lane]);
+    tau = warp_get<R>(S, k - 1);
+  }
+  // 1. local tops (best first per lane)
+  Cand t[R];
+#pragma unroll
+  for (int j = 0; j < R; ++j) t[j] = sent();
+  for (int vb = 0; vb < s; vb += 32) {
+    Cand c = get(vb + lane);  // sentinel for invalid / self
+    if (better_c(c, tau) && better_c(c, t[R - 1])) {
+#pragma unroll
+      for (int j = R - 1; j > 0; --j) {
+        if (better_c(c, t[j - 1])) t[j] = t[j - 1];
+        else if (better_c(c, t[j])) t[j] = c;
+      }
+      if (better_c(c, t[0])) t[0] = c;
+    }
+  }
+  const Cand lastTop = t[R - 1];  // lane's worst kept top: later candidates beyond it are extras
+  // 2. sort the tops, threshold T = k-th best (sentinel if fewer than k real tops)
+  warp_sort<R>(t);
+  const Cand T = warp_get<R>(t, k - 1);
+  // 3. extras: candidates >= T (and above tau) that were not kept as tops
+  if (is_real(T)) {
+    for (int vb = 0; vb < s; vb += 32) {
+      Cand c = get(vb + lane);
+      bool ex = is_real(c) && better_c(c, tau) && !better_c(T, c) && better_c(lastTop, c);
+      unsigned mask = __ballot_sync(0xffffffffu, ex);
+      while (mask) {
+        int l = __ffs(mask) - 1;
+        mask &= mask - 1;
+        warp_insert<R>(t, shfl_c(c, l));
+      }
+    }
+  } else {
+    // fewer than k real tops: every candidate above tau is a top unless its lane had > R
+    for (int vb = 0; vb < s; vb += 32) {
+      Cand c = get(vb + lane);
+      bool ex = is_real(c) && better_c(c, tau) && better_c(lastTop, c);
+      unsigned mask = __ballot_sync(0xffffffffu, ex);
+      while (mask) {
+        int l = __ffs(mask) - 1;
+        mask &= mask - 1;
+        warp_insert<R>(t, shfl_c(c, l));
+      }
+    }
+  }
+  // t[0..k) = top-k of the row's candidates above tau (sentinels when fewer)
+  if (!seed) {
+#pragma unroll
+    for (int j = 0; j < R; ++j)
+      if (32 * j + lane < k) dst[32 * j + lane] = to_out(t[j]);
+    return;
+  }
+  // 4. merge with S: positions >= k of t are dropped; bitonic = t (best first) ++ reverse(S)
+  Cand m[2 * R];
+#pragma unroll
+  for (int j = 0; j < R; ++j) m[j] = (32 * j + lane < k) ? t[j] : sent();
+#pragma unroll
+  for (int j = 0; j < R; ++j) {
+    // reverse(S) over 32R positions: position p takes S[32R-1-p]
+    Cand r = shfl_c(S[R - 1 - j], 31 - lane);
+    m[R + j] = r;
+  }
+  warp_bitonic_merge<2 * R>(m);
+  // remove adjacent duplicates (same id), keep the first k
+  int base = 0;
+#pragma unroll
+  for (int j = 0; j < 2 * R; ++j) {
+    int32_t prev = __shfl_up_sync(0xffffffffu, m[j].id, 1);
+    int32_t prevj = j > 0 ? __shfl_sync(0xffffffffu, m[j - 1].id, 31) : -2;
+    if (lane == 0) prev = prevj;
+    bool keep = is_real(m[j]) && m[j].id != prev;
+    unsigned bal = __ballot_sync(0xffffffffu, keep);
+    int rank = base + __popc(bal & ((1u << lane) - 1));
+    if (keep && rank < k) dst[rank] = to_out(m[j]);
+    base += __popc(bal);
+  }
+  for (int p = base + lane; p < k; p += 32) dst[p] = c2_cand{-1, 0, 0};
+}
+
+// ------------------------------------------------------------------ K7 small clusters
+constexpr int SMALL_WARPS = 8;
+constexpr int SMALL_STAGE = 2048;  // ints of staged item lists per warp
 
 __global__ void __launch_bounds__(SMALL_WARPS * 32) k_local_small(
     const SmallItem *__restrict__ work, int64_t lo, int64_t hi, const int32_t *__restrict__ members, int32_t n,
     const int32_t *__restrict__ offs, const int32_t *__restrict__ itm, const int32_t *__restrict__ psize, int k,
-    int fused, c2_cand *__restrict__ out) {
+    const c2_cand *__restrict__ seed, c2_cand *__restrict__ out) {
   __shared__ uint32_t cnt[SMALL_WARPS][32][33];
-  __shared__ int32_t sid[SMALL_WARPS][32], sps[SMALL_WARPS][32], sbeg[SMALL_WARPS][32];
+  __shared__ int32_t sid[SMALL_WARPS][32], sps[SMALL_WARPS][32], sbeg[SMALL_WARPS][33];
+  extern __shared__ __align__(16) int32_t small_dyn[];  // [SMALL_WARPS][SMALL_STAGE]
+  int32_t(*stage)[SMALL_STAGE] = reinterpret_cast<int32_t(*)[SMALL_STAGE]>(small_dyn);
   int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   for (int64_t it = lo + warp; it < hi; it += nwarps) {
     SmallItem I = work[it];
     const int32_t *mem = members + (int64_t)I.f * n + I.start;
-    int s = I.s;
+    const int s = I.s;
     int32_t u = lane < s ? mem[lane] : -1;
+    int32_t len = u >= 0 ? psize[u] : 0;
     sid[w][lane] = u;
-    sps[w][lane] = u >= 0 ? psize[u] : 0;
-    sbeg[w][lane] = u >= 0 ? offs[u] : 0;
+    sps[w][lane] = len;
+    // stage the s rows contiguously in shared memory when they fit
+    int incl = c2d::warp_incl_scan(len);
+    int total = __shfl_sync(0xffffffffu, incl, 31);
+    const bool staged = total <= SMALL_STAGE;
+    sbeg[w][lane] = staged ? incl - len : (u >= 0 ? offs[u] : 0);
     __syncwarp();
+    if (staged) {
+      for (int r = 0; r < s; ++r) {
+        const int32_t *src = itm + offs[sid[w][r]];
+        int32_t *d = &stage[w][sbeg[w][r]];
+        for (int q = lane; q < sps[w][r]; q += 32) d[q] = src[q];
+      }
+    }
+    __syncwarp();
+    const int32_t *base = staged ? &stage[w][0] : itm;
     // all unordered pairs (a > b), each by a two-pointer merge of the two sorted rows
     int np = s * (s - 1) / 2;
     for (int p = lane; p < np; p += 32) {
@@ -281,8 +506,8 @@ __global__ void __launch_bounds__(SMALL_WARPS * 32) k_local_small(
       while (a * (a - 1) / 2 > p) --a;
       while ((a + 1) * a / 2 <= p) ++a;
       int bb = p - a * (a - 1) / 2;
-      const int32_t *A = itm + sbeg[w][a];
-      const int32_t *B = itm + sbeg[w][bb];
+      const int32_t *A = base + sbeg[w][a];
+      const int32_t *B = base + sbeg[w][bb];
       int na = sps[w][a], nb = sps[w][bb];
       int i = 0, j = 0, c = 0;
       while (i < na && j < nb) {
@@ -295,33 +520,54 @@ __global__ void __launch_bounds__(SMALL_WARPS * 32) k_local_small(
       cnt[w][bb][a] = c;
     }
     __syncwarp();
+    // exact rank of every candidate of row `lane` among the row's s-1 candidates
+    c2_cand *loc = reinterpret_cast<c2_cand *>(&stage[w][0]) + lane * 32;  // 32 slots / lane
+    const int nl = min(s - 1, k);
     if (u >= 0) {
-      const uint32_t len = (uint32_t)sps[w][lane];
-      if (!fused) {
-        // exact rank of every candidate among the row's s-1 candidates
-        c2_cand *o = out + ((int64_t)I.f * n + u) * k;
-        for (int j = 0; j < s; ++j) {
-          if (j == lane) continue;
-          int32_t vj = sid[w][j];
-          uint32_t ij = cnt[w][lane][j], Uj = len + sps[w][j] - ij;
-          int rank = 0;
-          for (int j2 = 0; j2 < s; ++j2) {
-            if (j2 == lane || j2 == j) continue;
-            uint32_t i2 = cnt[w][lane][j2], U2 = len + sps[w][j2] - i2;
-            rank += c2d::better(i2, U2, sid[w][j2], ij, Uj, vj);
-          }
-          if (rank < k) o[rank] = c2_cand{vj, (uint16_t)ij, (uint16_t)Uj};
+      c2_cand *o = seed ? loc : out + ((int64_t)I.f * n + u) * k;
+      for (int j = 0; j < s; ++j) {
+        if (j == lane) continue;
+        int32_t vj = sid[w][j];
+        uint32_t ij = cnt[w][lane][j], Uj = len + sps[w][j] - ij;
+        int rank = 0;
+        for (int j2 = 0; j2 < s; ++j2) {
+          if (j2 == lane || j2 == j) continue;
+          uint32_t i2 = cnt[w][lane][j2], U2 = len + sps[w][j2] - i2;
+          rank += c2d::better(i2, U2, sid[w][j2], ij, Uj, vj);
         }
-        for (int q = s - 1; q < k; ++q) o[q] = c2_cand{-1, 0, 0};
-      } else {
-        // fused: insert each candidate into the running final list of u (Alg. 3)
-        c2_cand *R = out + (int64_t)u * k;
-        for (int j = 0; j < s; ++j) {
-          if (j == lane) continue;
-          uint32_t ij = cnt[w][lane][j];
-          fused_insert(R, k, sid[w][j], ij, len + sps[w][j] - ij);
-        }
+        if (rank < k) o[rank] = c2_cand{vj, (uint16_t)ij, (uint16_t)Uj};
       }
+      if (!seed)
+        for (int q = s - 1; q < k; ++q) o[q] = c2_cand{-1, 0, 0};
+    }
+    __syncwarp();
+    if (seed && u >= 0) {
+      // Alg. 3: merge the running list of u with the local list (both best first), dedup
+      const c2_cand *Rin = seed + (int64_t)u * k;
+      c2_cand *Rout = out + (int64_t)u * k;
+      int i = 0, j = 0, o = 0;
+      c2_cand a = Rin[0];
+      while (o < k) {
+        bool ha = i < k && a.id >= 0, hb = j < nl;
+        if (!ha && !hb) break;
+        c2_cand b = hb ? loc[j] : c2_cand{-1, 0, 0};
+        c2_cand e;
+        if (ha && hb && a.id == b.id) {
+          e = a;
+          ++i;
+          ++j;
+          a = i < k ? Rin[i] : c2_cand{-1, 0, 0};
+        } else if (ha && (!hb || c2d::better(a.inter, a.uni, a.id, b.inter, b.uni, b.id))) {
+          e = a;
+          ++i;
+          a = i < k ? Rin[i] : c2_cand{-1, 0, 0};
+        } else {
+          e = b;
+          ++j;
+        }
+        Rout[o++] = e;
+      }
+      for (; o < k; ++o) Rout[o] = c2_cand{-1, 0, 0};
     }
     __syncwarp();
   }
@@ -351,6 +597,8 @@ __device__ __forceinline__ void transpose32(uint32_t (&A)[32]) {
   }
 }
 
+constexpr int STAGE_V = 2048;  // cluster members whose (id, |P|) are staged in shared memory
+
 struct TileArgs {
   const Tile *tiles;
   int64_t lo, hi;
@@ -364,9 +612,9 @@ struct TileArgs {
   int32_t n;
   int32_t W, nwin;
   int k;
-  int fused;
-  c2_cand *out;       // local: cand [t][n][k]; fused: running final lists [n][k]
-  uint16_t *scratch;  // [grid][32][smax]
+  const c2_cand *seed;  // fused: running lists before this function [n][k]; else nullptr
+  c2_cand *out;         // local: cand [t][n][k]; fused: running lists after this function
+  uint16_t *scratch;    // [grid][32][smax]
   int32_t smax;
 };
 
@@ -391,7 +639,7 @@ struct Counter {
 #pragma unroll
     for (int i = 0; i < NHI; ++i) H[i] = 0;
   }
-  // add 8 masks; returns the carry of weight 8 (to be combined by add16)
+  // add 8 masks; returns the carry of weight 8 (combined in pairs by add16)
   __device__ __forceinline__ uint32_t add8(const uint32_t (&m)[8]) {
     uint32_t tA, tB, fA, fB, e8;
     csa(tA, ones, ones, m[0], m[1]);
@@ -417,7 +665,10 @@ struct Counter {
 
 template <int NHI, int VPT, int KS>
 __global__ void __launch_bounds__(TILE_T, 1) k_local_tile(TileArgs a) {
-  extern __shared__ uint32_t M[];  // W + 1 words; M[W] stays 0 (padding id)
+  extern __shared__ __align__(16) uint32_t dyn[];
+  uint32_t *M = dyn;                                                // W + 1 words; M[W] == 0
+  int32_t *s_vid = reinterpret_cast<int32_t *>(dyn + ((a.W + 4) & ~3));  // STAGE_V
+  uint32_t *s_vps = reinterpret_cast<uint32_t *>(s_vid + STAGE_V);       // STAGE_V
   __shared__ int s_item;
   __shared__ int32_t s_ru[32];
   __shared__ uint32_t s_rp[32];
@@ -438,6 +689,13 @@ __global__ void __launch_bounds__(TILE_T, 1) k_local_tile(TileArgs a) {
     const int r0 = T.j * 32;
     const int nr = min(32, B.s - r0);
     const int32_t *vp = a.vperm + B.vp_off;
+    const bool vstaged = B.s <= STAGE_V;
+    if (vstaged)
+      for (int i = tid; i < B.s; i += TILE_T) {
+        int32_t v = vp[i];
+        s_vid[i] = v;
+        s_vps[i] = (uint32_t)a.psize[v];
+      }
     if (tid < 32) {
       int32_t u = tid < nr ? vp[r0 + tid] : -1;
       s_ru[tid] = u;
@@ -536,70 +794,29 @@ __global__ void __launch_bounds__(TILE_T, 1) k_local_tile(TileArgs a) {
     __syncthreads();
     // ---- K8: per-row top-k, warp per row
     const int kk = a.k;
-    const int tl = (kk - 1) & 31, ts = (kk - 1) >> 5;
     for (int r = warp; r < nr; r += TILE_WARPS) {
       const int32_t ur = s_ru[r];
       const uint32_t pr = s_rp[r];
-      int32_t id0 = INT32_MAX, id1 = INT32_MAX;
-      uint32_t i0 = 0, U0 = 1, i1 = 0, U1 = 1;
-      c2_cand *dst = a.fused ? a.out + (int64_t)ur * kk : a.out + ((int64_t)B.f * a.n + ur) * kk;
-      if (a.fused) {
-        if (lane < kk) {
-          c2_cand e = dst[lane];
-          if (e.id >= 0) { id0 = e.id; i0 = e.inter; U0 = e.uni; }
-        }
-        if (KS == 2 && 32 + lane < kk) {
-          c2_cand e = dst[32 + lane];
-          if (e.id >= 0) { id1 = e.id; i1 = e.inter; U1 = e.uni; }
-        }
-      }
-      int32_t tid_ = __shfl_sync(0xffffffffu, ts ? id1 : id0, tl);
-      uint32_t ti = __shfl_sync(0xffffffffu, ts ? i1 : i0, tl);
-      uint32_t tU = __shfl_sync(0xffffffffu, ts ? U1 : U0, tl);
       const uint16_t *crow = cnt + (int64_t)r * a.smax;
-      for (int vb = 0; vb < B.s; vb += 32) {
-        const int vi = vb + lane;
-        int32_t v = vi < B.s ? vp[vi] : -1;
-        bool valid = v >= 0 && v != ur;
-        uint32_t ci = valid ? crow[vi] : 0u;
-        uint32_t cU = valid ? pr + (uint32_t)a.psize[v] - ci : 1u;
-        bool bt = valid && c2d::better(ci, cU, v, ti, tU, tid_);
-        unsigned mask = __ballot_sync(0xffffffffu, bt);
-        while (mask) {
-          int l = __ffs(mask) - 1;
-          mask &= mask - 1;
-          uint32_t xi = __shfl_sync(0xffffffffu, ci, l);
-          uint32_t xU = __shfl_sync(0xffffffffu, cU, l);
-          int32_t xid = __shfl_sync(0xffffffffu, v, l);
-          if (!c2d::better(xi, xU, xid, ti, tU, tid_)) continue;
-          if (a.fused) {
-            bool dup = (id0 == xid) || (KS == 2 && id1 == xid);
-            if (__any_sync(0xffffffffu, dup)) continue;  // same id from an earlier function (A16)
-          }
-          int pos = __popc(__ballot_sync(0xffffffffu, c2d::better(i0, U0, id0, xi, xU, xid)));
-          int32_t pid0 = __shfl_up_sync(0xffffffffu, id0, 1);
-          uint32_t pi0 = __shfl_up_sync(0xffffffffu, i0, 1), pU0 = __shfl_up_sync(0xffffffffu, U0, 1);
-          if (KS == 2) {
-            pos += __popc(__ballot_sync(0xffffffffu, c2d::better(i1, U1, id1, xi, xU, xid)));
-            int32_t pid1 = __shfl_up_sync(0xffffffffu, id1, 1);
-            uint32_t pi1 = __shfl_up_sync(0xffffffffu, i1, 1), pU1 = __shfl_up_sync(0xffffffffu, U1, 1);
-            int32_t lid0 = __shfl_sync(0xffffffffu, id0, 31);
-            uint32_t li0 = __shfl_sync(0xffffffffu, i0, 31), lU0 = __shfl_sync(0xffffffffu, U0, 31);
-            if (lane == 0) { pid1 = lid0; pi1 = li0; pU1 = lU0; }
-            const int j1 = 32 + lane;
-            if (j1 == pos) { id1 = xid; i1 = xi; U1 = xU; }
-            else if (j1 > pos) { id1 = pid1; i1 = pi1; U1 = pU1; }
-          }
-          if (lane == pos) { id0 = xid; i0 = xi; U0 = xU; }
-          else if (lane > pos) { id0 = pid0; i0 = pi0; U0 = pU0; }
-          tid_ = __shfl_sync(0xffffffffu, ts ? id1 : id0, tl);
-          ti = __shfl_sync(0xffffffffu, ts ? i1 : i0, tl);
-          tU = __shfl_sync(0xffffffffu, ts ? U1 : U0, tl);
+      const int s = B.s;
+      auto get = [&](int vi) -> Cand {
+        if (vi >= s) return sent();
+        int32_t v;
+        uint32_t ps;
+        if (vstaged) {
+          v = s_vid[vi];
+          ps = s_vps[vi];
+        } else {
+          v = vp[vi];
+          ps = (uint32_t)a.psize[v];
         }
-      }
-      if (lane < kk) dst[lane] = id0 == INT32_MAX ? c2_cand{-1, 0, 0} : c2_cand{id0, (uint16_t)i0, (uint16_t)U0};
-      if (KS == 2 && 32 + lane < kk)
-        dst[32 + lane] = id1 == INT32_MAX ? c2_cand{-1, 0, 0} : c2_cand{id1, (uint16_t)i1, (uint16_t)U1};
+        if (v == ur) return sent();
+        uint32_t ci = crow[vi];
+        return Cand{ci | ((pr + ps - ci) << 16), v};
+      };
+      const c2_cand *seed = a.seed ? a.seed + (int64_t)ur * kk : nullptr;
+      c2_cand *dst = a.seed ? a.out + (int64_t)ur * kk : a.out + ((int64_t)B.f * a.n + ur) * kk;
+      row_topk<2 * KS>(s, kk, get, seed, dst);
     }
   }
 }
@@ -623,13 +840,33 @@ __global__ void k_init_pads(c2_cand *__restrict__ R, int64_t E) {
   if (e < E) R[e] = c2_cand{-1, 0, 0};
 }
 
+// sum over unordered pairs of (|P_u| + |P_v|) = sum over (f,u) of (s_c - 1) * |P_u|
+__global__ void k_work_steps(const int32_t *__restrict__ offsets, const int32_t *__restrict__ cof,
+                             const int32_t *__restrict__ psize, int64_t TN, int32_t n,
+                             unsigned long long *__restrict__ acc) {
+  int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  unsigned long long w = 0;
+  if (q < TN) {
+    int64_t f = q / n;
+    int32_t u = (int32_t)(q % n);
+    int32_t c = cof[q];
+    const int32_t *off = offsets + f * (n + 1);
+    w = (unsigned long long)(off[c + 1] - off[c] - 1) * (unsigned long long)psize[u];
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) w += __shfl_xor_sync(0xffffffffu, w, o);
+  if ((threadIdx.x & 31) == 0 && w) atomicAdd(acc, w);
+}
+
 __global__ void k_count_small_f(const SmallItem *__restrict__ w, int64_t ns, int32_t *__restrict__ per_f) {
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < ns) atomicAdd(&per_f[w[i].f], 1);
 }
 
-// fused: out = running final lists [n][k] (initialised here); local: out = cand [t][n][k]
-int local_knn(c2_ctx *ctx, const Csr &csr, int t, const Clusters &cl, int k, c2_cand *out, bool fused) {
+// fused: `out` holds 2*n*k entries (ping-pong running lists); *result = the final one.
+// local: out = cand [t][n][k].
+int local_knn(c2_ctx *ctx, const Csr &csr, int t, const Clusters &cl, int k, c2_cand *out, bool fused,
+              c2_cand **result) {
   int rc;
   cudaStream_t st = ctx->stream;
   const int32_t n = csr.n;
@@ -666,8 +903,14 @@ int local_knn(c2_ctx *ctx, const Csr &csr, int t, const Clusters &cl, int k, c2_
     k_count_small_f<<<nblk(nsmall), 256, 0, st>>>(wsmall, nsmall, per_f + t);
     C2_LAUNCHED(ctx, "k_count_small_f");
   }
+  unsigned long long *wacc = (unsigned long long *)ws_get(ctx, "work_acc", 16, &rc);
+  if (rc) return rc;
+  C2_CUDA(ctx, cudaMemsetAsync(wacc, 0, 8, st));
+  k_work_steps<<<nblk((int64_t)t * n), 256, 0, st>>>(cl.offsets, cl.cluster_of, csr.psize, (int64_t)t * n, n, wacc);
+  C2_LAUNCHED(ctx, "k_work_steps");
+  c2_cand *R[2] = {out, out + (int64_t)n * k};
   if (fused) {
-    k_init_pads<<<nblk((int64_t)n * k), 256, 0, st>>>(out, (int64_t)n * k);
+    k_init_pads<<<nblk((int64_t)n * k), 256, 0, st>>>(R[0], (int64_t)n * k);
     C2_LAUNCHED(ctx, "k_init_pads");
   }
 
@@ -722,13 +965,16 @@ int local_knn(c2_ctx *ctx, const Csr &csr, int t, const Clusters &cl, int k, c2_
     C2_LAUNCHED(ctx, "k_sl_fill");
   }
   int32_t hper[2 * C2_MAX_T];
+  unsigned long long hwork = 0;
   C2_CUDA(ctx, cudaMemcpyAsync(hper, per_f, 4 * 2 * C2_MAX_T, cudaMemcpyDeviceToHost, st));
+  C2_CUDA(ctx, cudaMemcpyAsync(&hwork, wacc, 8, cudaMemcpyDeviceToHost, st));
   C2_TRY(stream_sync(ctx, "per-function counts"));
+  ctx->stats.work_steps = (int64_t)hwork;
 
   // ---- tile kernel configuration
   TileKernel tk = nullptr;
   int grid = 0;
-  size_t smem = (size_t)(W + 1) * 4;
+  const size_t smem = (size_t)((W + 4) & ~3) * 4 + (size_t)STAGE_V * 8;
   uint16_t *scratch = nullptr;
   int *counters = nullptr;
   int32_t smax = (int32_t)((maxs + 31) / 32 * 32);
@@ -749,36 +995,57 @@ int local_knn(c2_ctx *ctx, const Csr &csr, int t, const Clusters &cl, int k, c2_
     if (rc) return rc;
     C2_CUDA(ctx, cudaMemsetAsync(counters, 0, 4 * (C2_MAX_T + 1), st));
   }
-  auto launch_small = [&](int64_t lo, int64_t hi) -> int {
+  auto launch_small = [&](int64_t lo, int64_t hi, const c2_cand *seed, c2_cand *dst) -> int {
     if (hi <= lo) return C2_OK;
     int64_t blocks = std::min<int64_t>((hi - lo + SMALL_WARPS - 1) / SMALL_WARPS, (int64_t)ctx->num_sms * 16);
-    k_local_small<<<(unsigned)blocks, SMALL_WARPS * 32, 0, st>>>(wsmall, lo, hi, cl.members, n, csr.offs, csr.items,
-                                                                 csr.psize, k, fused ? 1 : 0, out);
+    const size_t ssm = (size_t)SMALL_WARPS * SMALL_STAGE * 4;
+    C2_CUDA(ctx, cudaFuncSetAttribute(k_local_small, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ssm));
+    k_local_small<<<(unsigned)blocks, SMALL_WARPS * 32, ssm, st>>>(wsmall, lo, hi, cl.members, n, csr.offs,
+                                                                   csr.items, csr.psize, k, seed, dst);
     C2_LAUNCHED(ctx, "k_local_small");
     return C2_OK;
   };
-  auto launch_tiles = [&](int64_t lo, int64_t hi, int ci) -> int {
+  auto launch_tiles = [&](int64_t lo, int64_t hi, int ci, const c2_cand *seed, c2_cand *dst) -> int {
     if (hi <= lo) return C2_OK;
     TileArgs ta{tiles, lo, hi, counters + ci, bcs, vperm, blk_len8, blk_off8, packed, csr.psize, n, W, nwin, k,
-                fused ? 1 : 0, out, scratch, smax};
+                seed, dst, scratch, smax};
     int g = (int)std::min<int64_t>(grid, hi - lo);
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (ctx->timing) {
+      while ((int)ctx->tile_ev.size() < 2 * (ctx->tile_ev_used + 1)) {
+        cudaEvent_t e;
+        C2_CUDA(ctx, cudaEventCreate(&e));
+        ctx->tile_ev.push_back(e);
+      }
+      e0 = ctx->tile_ev[2 * ctx->tile_ev_used];
+      e1 = ctx->tile_ev[2 * ctx->tile_ev_used + 1];
+      ctx->tile_ev_used++;
+      C2_CUDA(ctx, cudaEventRecord(e0, st));
+    }
     tk<<<g, TILE_T, smem, st>>>(ta);
     C2_LAUNCHED(ctx, "k_local_tile");
+    if (ctx->timing) C2_CUDA(ctx, cudaEventRecord(e1, st));
+    ctx->stats.tile_launches++;
     return C2_OK;
   };
   if (!fused) {
-    C2_TRY(launch_small(0, nsmall));
-    C2_TRY(launch_tiles(0, nslices, 0));
+    C2_TRY(launch_small(0, nsmall, nullptr, out));
+    C2_TRY(launch_tiles(0, nslices, 0, nullptr, out));
+    if (result) *result = out;
   } else {
-    // Alg. 3 order: function by function, each row merged into its running final list
+    // Alg. 3 order: function by function, every user's running list (R[cur]) is merged with
+    // its neighbourhood in that function's cluster into R[cur ^ 1]
     int64_t slo = 0, tlo = 0;
+    int cur = 0;
     for (int f = 0; f < t; ++f) {
       int64_t shi = slo + hper[t + f], thi = tlo + hper[f];
-      C2_TRY(launch_tiles(tlo, thi, f));
-      C2_TRY(launch_small(slo, shi));
+      C2_TRY(launch_tiles(tlo, thi, f, R[cur], R[cur ^ 1]));
+      C2_TRY(launch_small(slo, shi, R[cur], R[cur ^ 1]));
       slo = shi;
       tlo = thi;
+      cur ^= 1;
     }
+    if (result) *result = R[cur];
   }
   return C2_OK;
 }
