@@ -1,10 +1,11 @@
 // k_local.cu -- Step 2 of C^2 on the GPU: brute-force Jaccard top-k inside every cluster
 // (Alg. 2, brute-force branch; s(s-1)/2 similarities per cluster).
 //
-// K5 worklist.  Clusters of <= 32 users go to k_local_small (one warp per cluster, all
-//    unordered pairs by two-pointer merge, exact rank selection).  Larger ("big") clusters
-//    are ordered by function, then by size (largest first: the paper's decreasing priority
-//    queue), cut into 32-user slices, and repacked once per call:
+// K5 worklist.  Clusters of more than 32 users ("big") are ordered by function, then by size
+//    (largest first: the paper's decreasing priority queue) and cut into 32-user
+//    slices; clusters of 2..32 users are packed 32/slot per "mixed" slice, each in an aligned
+//    group of slot = 2^ceil(log2 s) positions (pairs across groups are ignored).  Then, once
+//    per call:
 //      vperm   members of the cluster sorted by |P_v| (descending), so the 32 lists of a
 //              slice have similar lengths;
 //      packed  for every (slice, item window) a block of u16 window-local item ids laid out
@@ -16,11 +17,13 @@
 //    x in P_r} (bit r).  Each thread owns VPT slices' lanes (one v each) and accumulates the
 //    32 counts |P_r ∩ P_v| bit-sliced with Harley-Seal carry-save adders over 16 masks, so
 //    one LDS + ~3 LOP3 serve 32 pairs.  A 32x32 bit transpose turns the planes into counts.
-// K8 (in K7): per row, one warp selects the k best candidates under the exact order
-//    (i1*U2 > i2*U1, ties by lower id) with a threshold from per-lane top lists (row_topk).
-//    In fused mode (c2_build) it starts from the running Alg. 3 result of the earlier
-//    functions (the k-th best never decreases, so pruning below it is exact) and writes the
-//    merged list, instead of a per-function list.
+// K8 (in K7): exact top-k per row under the order i1*U2 > i2*U1, ties by lower id.  Lane =
+//    row, the 16 warps scan interleaved candidate segments: round 1 keeps each thread's best
+//    2 (4 if k > 32) -> 32 (64) "tops" per row, whose k-th best T_r is a valid lower bound of
+//    the row's k-th best; round 2 queues the few candidates >= T_r; one warp sorts the queue.
+//    In fused mode (c2_build) candidates must also beat tau = the running Alg. 3 result's
+//    k-th best (it never decreases, so the pruning is exact); the queue is merged with that
+//    running list (duplicate ids dropped) instead of being written as a per-function list.
 #include <algorithm>
 #include <vector>
 
@@ -28,11 +31,11 @@
 
 namespace c2 {
 
-struct SmallItem {
-  int32_t f, start, s;
-};
+// A cluster processed by the tile kernel: either one big cluster (slot == 0; members in
+// vperm[vp_off .. vp_off + s)) or one "mixed" 32-row slice packing 32/slot small clusters of
+// 2..32 users, each in its own aligned group of `slot` positions (empty positions are -1).
 struct BigC {
-  int32_t f, start, s, vp_off, sl_off;
+  int32_t f, s, vp_off, sl_off, slot;
 };
 struct Tile {
   int32_t bc, j;
@@ -56,31 +59,39 @@ __device__ __forceinline__ int find_f(const int32_t *ccum, int t, int64_t g) {
   return f;
 }
 
+// category of every cluster: big (> 32 users), small (2..32), single.  One 32-bit sort key
+// orders them [big: by function, then size descending][small: by function, slot class]
+// [single: by function]; counts per (category, f, class) go to cnt_fc.
+__device__ __forceinline__ int slot_class(int32_t s) {  // slot = 2^class >= s, s in [2, 32]
+  int c = 1;
+  while ((1 << c) < s) ++c;
+  return c;
+}
+
 __global__ void k_wl_classify(const int32_t *__restrict__ offsets, const int32_t *__restrict__ ccum, int t,
-                              int32_t n, int64_t C, int32_t *__restrict__ fsmall, uint32_t *__restrict__ key,
-                              uint32_t *__restrict__ val, uint32_t maxs, int sized) {
+                              int32_t n, int64_t C, uint32_t *__restrict__ key, uint32_t *__restrict__ val,
+                              uint32_t maxs, int sized, int32_t *__restrict__ cnt_fc) {
   int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (g >= C) return;
   int f = find_f(ccum, t, g);
   int64_t c = g - ccum[f];
   const int32_t *off = offsets + (int64_t)f * (n + 1);
   uint32_t s = (uint32_t)(off[c + 1] - off[c]);
-  bool big = s > 32;
-  fsmall[g] = !big;
-  // big clusters first, by function, then size descending; small ones after all of them
-  key[g] = big ? (uint32_t)f * (sized ? (maxs + 1) : 1u) + (sized ? (maxs - s) : 0u) : 0xFFFFFFFFu;
+  uint32_t k;
+  if (s > 32) {
+    k = ((uint32_t)f << 24) | (sized ? min(maxs - s, 0xFFFFFFu) : 0u);
+    atomicAdd(&cnt_fc[f * 8 + 0], (int32_t)((s + 31) / 32));  // big tiles of f
+    atomicAdd(&cnt_fc[f * 8 + 7], 1);                          // big clusters of f
+  } else if (s >= 2) {
+    int cl = slot_class((int32_t)s);
+    k = (1u << 30) | ((uint32_t)f << 24) | (uint32_t)cl;
+    atomicAdd(&cnt_fc[f * 8 + cl], 1);  // small clusters of (f, class), class 1..5
+  } else {
+    k = (2u << 30) | ((uint32_t)f << 24);
+    atomicAdd(&cnt_fc[f * 8 + 6], 1);  // singletons of f
+  }
+  key[g] = k;
   val[g] = (uint32_t)g;
-}
-
-__global__ void k_wl_small(const int32_t *__restrict__ offsets, const int32_t *__restrict__ ccum, int t, int32_t n,
-                           int64_t C, const int32_t *__restrict__ fsmall, const int32_t *__restrict__ sscan,
-                           SmallItem *__restrict__ out) {
-  int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (g >= C || !fsmall[g]) return;
-  int f = find_f(ccum, t, g);
-  int64_t c = g - ccum[f];
-  const int32_t *off = offsets + (int64_t)f * (n + 1);
-  out[sscan[g]] = SmallItem{f, off[c], off[c + 1] - off[c]};
 }
 
 __global__ void k_bc_sizes(const uint32_t *__restrict__ sval, int64_t nbig, const int32_t *__restrict__ offsets,
@@ -100,7 +111,7 @@ __global__ void k_bc_sizes(const uint32_t *__restrict__ sval, int64_t nbig, cons
 __global__ void k_bc_fill(const uint32_t *__restrict__ sval, int64_t nbig, const int32_t *__restrict__ offsets,
                           const int32_t *__restrict__ ccum, int t, int32_t n, const int32_t *__restrict__ vp_scan,
                           const int32_t *__restrict__ sl_scan, BigC *__restrict__ bcs, Tile *__restrict__ tiles,
-                          int32_t *__restrict__ per_f) {
+                          int32_t *__restrict__ bstart) {
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= nbig) return;
   int64_t g = sval[i];
@@ -108,22 +119,75 @@ __global__ void k_bc_fill(const uint32_t *__restrict__ sval, int64_t nbig, const
   int64_t c = g - ccum[f];
   const int32_t *off = offsets + (int64_t)f * (n + 1);
   int32_t s = off[c + 1] - off[c];
-  BigC b{f, off[c], s, vp_scan[i], sl_scan[i]};
+  BigC b{f, s, vp_scan[i], sl_scan[i], 0};
   bcs[i] = b;
+  bstart[i] = off[c];
   int ns = (s + 31) / 32;
   for (int j = 0; j < ns; ++j) tiles[b.sl_off + j] = Tile{(int32_t)i, j};
-  atomicAdd(&per_f[f], ns);
+}
+
+// small clusters (sorted by (f, class)): place members into their mixed slice
+struct MixGroup {
+  int32_t f, cls, first_entry, count, first_slice;  // entries = positions in the sorted small list
+};
+__global__ void k_mix_fill(const uint32_t *__restrict__ sval_small, int64_t nsmall, const int32_t *__restrict__ offsets,
+                           const int32_t *__restrict__ ccum, int t, int32_t n, const int32_t *__restrict__ members,
+                           const MixGroup *__restrict__ groups, int ngroups, int32_t vp_base,
+                           int32_t *__restrict__ vperm) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nsmall) return;
+  int gi = 0;
+  while (gi + 1 < ngroups && groups[gi + 1].first_entry <= i) ++gi;
+  const MixGroup G = groups[gi];
+  int64_t g = sval_small[i];
+  int f = find_f(ccum, t, g);
+  int64_t c = g - ccum[f];
+  const int32_t *off = offsets + (int64_t)f * (n + 1);
+  int32_t st = off[c], s = off[c + 1] - st;
+  int q = (int)(i - G.first_entry);
+  int per = 32 >> G.cls;
+  int64_t slice = G.first_slice + q / per;
+  int pos = (q % per) << G.cls;
+  int32_t *dst = vperm + vp_base + slice * 32 + pos;
+  for (int j = 0; j < s; ++j) dst[j] = members[(int64_t)f * n + st + j];
+}
+
+__global__ void k_mix_bc(const MixGroup *__restrict__ groups, int ngroups, int64_t nmix, int64_t nbig, int32_t vp_base,
+                         int64_t sl_base, BigC *__restrict__ bcs, Tile *__restrict__ tiles) {
+  int64_t m = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (m >= nmix) return;
+  int gi = 0;
+  while (gi + 1 < ngroups && groups[gi + 1].first_slice <= m) ++gi;
+  bcs[nbig + m] = BigC{groups[gi].f, 32, (int32_t)(vp_base + m * 32), (int32_t)(sl_base + m), 1 << groups[gi].cls};
+  tiles[sl_base + m] = Tile{(int32_t)(nbig + m), 0};
+}
+
+// singletons: no candidates.  local: pad rows; fused: running list carried over unchanged.
+__global__ void k_singles(const uint32_t *__restrict__ sval_single, int64_t nsingle, const int32_t *__restrict__ offsets,
+                          const int32_t *__restrict__ ccum, int t, int32_t n, const int32_t *__restrict__ members,
+                          int k, int64_t lo, int64_t hi, const c2_cand *__restrict__ seed,
+                          c2_cand *__restrict__ out) {
+  int64_t e = lo * k + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= hi * k) return;
+  int64_t i = e / k;
+  int j = (int)(e % k);
+  int64_t g = sval_single[i];
+  int f = find_f(ccum, t, g);
+  int64_t c = g - ccum[f];
+  int32_t u = members[(int64_t)f * n + offsets[(int64_t)f * (n + 1) + c]];
+  if (seed) out[(int64_t)u * k + j] = seed[(int64_t)u * k + j];
+  else out[((int64_t)f * n + u) * k + j] = c2_cand{-1, 0, 0};
 }
 
 // vperm: members of each big cluster sorted by |P_v| descending (ties by position).  One CTA
 // per cluster, bitonic sort in shared memory for s <= 2048 (larger clusters keep the
 // canonical order: performance only, results do not depend on it).
-__global__ void __launch_bounds__(1024) k_sl_sort(const BigC *__restrict__ bcs, const int32_t *__restrict__ members,
-                                                  int32_t n, const int32_t *__restrict__ psize,
-                                                  int32_t *__restrict__ vperm) {
+__global__ void __launch_bounds__(1024) k_sl_sort(const BigC *__restrict__ bcs, const int32_t *__restrict__ bstart,
+                                                  const int32_t *__restrict__ members, int32_t n,
+                                                  const int32_t *__restrict__ psize, int32_t *__restrict__ vperm) {
   __shared__ uint32_t key[2048];
   const BigC b = bcs[blockIdx.x];
-  const int32_t *mem = members + (int64_t)b.f * n + b.start;
+  const int32_t *mem = members + (int64_t)b.f * n + bstart[blockIdx.x];
   int32_t *out = vperm + b.vp_off;
   if (b.s > 2048) {
     for (int i = threadIdx.x; i < b.s; i += blockDim.x) out[i] = mem[i];
@@ -167,8 +231,8 @@ __global__ void k_sl_len(const Tile *__restrict__ tiles, int64_t nslices, const 
   int cnt[MAX_WIN];
 #pragma unroll
   for (int w = 0; w < MAX_WIN; ++w) cnt[w] = 0;
-  if (vi < b.s) {
-    int32_t v = vperm[b.vp_off + vi];
+  int32_t v = vi < b.s ? vperm[b.vp_off + vi] : -1;
+  if (v >= 0) {
     int32_t p = offs[v], e = offs[v + 1];
     int32_t bound = W;
     int w = 0, run = 0;
@@ -210,8 +274,8 @@ __global__ void k_sl_fill(const Tile *__restrict__ tiles, int64_t nslices, const
   BigC b = bcs[T.bc];
   int vi = T.j * 32 + lane;
   int32_t p = 0, e = 0;
-  if (vi < b.s) {
-    int32_t v = vperm[b.vp_off + vi];
+  int32_t v = vi < b.s ? vperm[b.vp_off + vi] : -1;
+  if (v >= 0) {
     p = offs[v];
     e = offs[v + 1];
   }
@@ -361,218 +425,6 @@ __device__ __forceinline__ Cand warp_get(const Cand (&a)[R], int p) {
   return shfl_c(r, p & 31);
 }
 
-// Exact top-k of one row's candidates (k <= 16R), optionally merged with a seed list S (the
-// running Alg. 3 result, sorted, pads = sentinels), written best-first to dst[0..k).
-//   1. every lane keeps its best R candidates that beat tau = S[k-1] (local top-R), so the
-//      warp holds 32R "tops";
-//   2. sorting the tops gives T = their k-th best: k distinct real candidates are >= T, so T
-//      is <= the row's true k-th best (a valid pruning threshold);
-//   3. candidates >= T that are not among their lane's tops (rare) are inserted;
-//   4. the first k of the tops are top-k(C above tau); merged with S (bitonic merge + removal
-//      of adjacent equal ids: a repeated id carries identical values, A16) -> first k.
-template <int R, class GetC>
-__device__ __forceinline__ void row_topk(int s, int k, GetC get, const c2_cand *seed, c2_cand *dst) {
-  const int lane = threadIdx.x & 31;
-  Cand S[R];
-  Cand tau = sent();
-#pragma unroll
-  for (int j = 0; j < R; ++j) S[j] = sent();
-  if (seed) {
-#pragma unroll
-    for (int j = 0; j < R; ++j)
-      if (32 * j + lane < k) S[j] = from_out(seed[32 * j + lane]);
-    tau = warp_get<R>(S, k - 1);
-  }
-  // 1. local tops (best first per lane)
-  Cand t[R];
-#pragma unroll
-  for (int j = 0; j < R; ++j) t[j] = sent();
-  for (int vb = 0; vb < s; vb += 32) {
-    Cand c = get(vb + lane);  // sentinel for invalid / self
-    if (better_c(c, tau) && better_c(c, t[R - 1])) {
-#pragma unroll
-      for (int j = R - 1; j > 0; --j) {
-        if (better_c(c, t[j - 1])) t[j] = t[j - 1];
-        else if (better_c(c, t[j])) t[j] = c;
-      }
-      if (better_c(c, t[0])) t[0] = c;
-    }
-  }
-  const Cand lastTop = t[R - 1];  // lane's worst kept top: later candidates beyond it are extras
-  // 2. sort the tops, threshold T = k-th best (sentinel if fewer than k real tops)
-  warp_sort<R>(t);
-  const Cand T = warp_get<R>(t, k - 1);
-  // 3. extras: candidates >= T (and above tau) that were not kept as tops
-  if (is_real(T)) {
-    for (int vb = 0; vb < s; vb += 32) {
-      Cand c = get(vb + lane);
-      bool ex = is_real(c) && better_c(c, tau) && !better_c(T, c) && better_c(lastTop, c);
-      unsigned mask = __ballot_sync(0xffffffffu, ex);
-      while (mask) {
-        int l = __ffs(mask) - 1;
-        mask &= mask - 1;
-        warp_insert<R>(t, shfl_c(c, l));
-      }
-    }
-  } else {
-    // fewer than k real tops: every candidate above tau is a top unless its lane had > R
-    for (int vb = 0; vb < s; vb += 32) {
-      Cand c = get(vb + lane);
-      bool ex = is_real(c) && better_c(c, tau) && better_c(lastTop, c);
-      unsigned mask = __ballot_sync(0xffffffffu, ex);
-      while (mask) {
-        int l = __ffs(mask) - 1;
-        mask &= mask - 1;
-        warp_insert<R>(t, shfl_c(c, l));
-      }
-    }
-  }
-  // t[0..k) = top-k of the row's candidates above tau (sentinels when fewer)
-  if (!seed) {
-#pragma unroll
-    for (int j = 0; j < R; ++j)
-      if (32 * j + lane < k) dst[32 * j + lane] = to_out(t[j]);
-    return;
-  }
-  // 4. merge with S: positions >= k of t are dropped; bitonic = t (best first) ++ reverse(S)
-  Cand m[2 * R];
-#pragma unroll
-  for (int j = 0; j < R; ++j) m[j] = (32 * j + lane < k) ? t[j] : sent();
-#pragma unroll
-  for (int j = 0; j < R; ++j) {
-    // reverse(S) over 32R positions: position p takes S[32R-1-p]
-    Cand r = shfl_c(S[R - 1 - j], 31 - lane);
-    m[R + j] = r;
-  }
-  warp_bitonic_merge<2 * R>(m);
-  // remove adjacent duplicates (same id), keep the first k
-  int base = 0;
-#pragma unroll
-  for (int j = 0; j < 2 * R; ++j) {
-    int32_t prev = __shfl_up_sync(0xffffffffu, m[j].id, 1);
-    int32_t prevj = j > 0 ? __shfl_sync(0xffffffffu, m[j - 1].id, 31) : -2;
-    if (lane == 0) prev = prevj;
-    bool keep = is_real(m[j]) && m[j].id != prev;
-    unsigned bal = __ballot_sync(0xffffffffu, keep);
-    int rank = base + __popc(bal & ((1u << lane) - 1));
-    if (keep && rank < k) dst[rank] = to_out(m[j]);
-    base += __popc(bal);
-  }
-  for (int p = base + lane; p < k; p += 32) dst[p] = c2_cand{-1, 0, 0};
-}
-
-// ------------------------------------------------------------------ K7 small clusters
-constexpr int SMALL_WARPS = 8;
-constexpr int SMALL_STAGE = 2048;  // ints of staged item lists per warp
-
-__global__ void __launch_bounds__(SMALL_WARPS * 32) k_local_small(
-    const SmallItem *__restrict__ work, int64_t lo, int64_t hi, const int32_t *__restrict__ members, int32_t n,
-    const int32_t *__restrict__ offs, const int32_t *__restrict__ itm, const int32_t *__restrict__ psize, int k,
-    const c2_cand *__restrict__ seed, c2_cand *__restrict__ out) {
-  __shared__ uint32_t cnt[SMALL_WARPS][32][33];
-  __shared__ int32_t sid[SMALL_WARPS][32], sps[SMALL_WARPS][32], sbeg[SMALL_WARPS][33];
-  extern __shared__ __align__(16) int32_t small_dyn[];  // [SMALL_WARPS][SMALL_STAGE]
-  int32_t(*stage)[SMALL_STAGE] = reinterpret_cast<int32_t(*)[SMALL_STAGE]>(small_dyn);
-  int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t it = lo + warp; it < hi; it += nwarps) {
-    SmallItem I = work[it];
-    const int32_t *mem = members + (int64_t)I.f * n + I.start;
-    const int s = I.s;
-    int32_t u = lane < s ? mem[lane] : -1;
-    int32_t len = u >= 0 ? psize[u] : 0;
-    sid[w][lane] = u;
-    sps[w][lane] = len;
-    // stage the s rows contiguously in shared memory when they fit
-    int incl = c2d::warp_incl_scan(len);
-    int total = __shfl_sync(0xffffffffu, incl, 31);
-    const bool staged = total <= SMALL_STAGE;
-    sbeg[w][lane] = staged ? incl - len : (u >= 0 ? offs[u] : 0);
-    __syncwarp();
-    if (staged) {
-      for (int r = 0; r < s; ++r) {
-        const int32_t *src = itm + offs[sid[w][r]];
-        int32_t *d = &stage[w][sbeg[w][r]];
-        for (int q = lane; q < sps[w][r]; q += 32) d[q] = src[q];
-      }
-    }
-    __syncwarp();
-    const int32_t *base = staged ? &stage[w][0] : itm;
-    // all unordered pairs (a > b), each by a two-pointer merge of the two sorted rows
-    int np = s * (s - 1) / 2;
-    for (int p = lane; p < np; p += 32) {
-      int a = (int)((1.0f + sqrtf(1.0f + 8.0f * (float)p)) * 0.5f);
-      while (a * (a - 1) / 2 > p) --a;
-      while ((a + 1) * a / 2 <= p) ++a;
-      int bb = p - a * (a - 1) / 2;
-      const int32_t *A = base + sbeg[w][a];
-      const int32_t *B = base + sbeg[w][bb];
-      int na = sps[w][a], nb = sps[w][bb];
-      int i = 0, j = 0, c = 0;
-      while (i < na && j < nb) {
-        int32_t x = A[i], y = B[j];
-        c += x == y;
-        i += x <= y;
-        j += y <= x;
-      }
-      cnt[w][a][bb] = c;
-      cnt[w][bb][a] = c;
-    }
-    __syncwarp();
-    // exact rank of every candidate of row `lane` among the row's s-1 candidates
-    c2_cand *loc = reinterpret_cast<c2_cand *>(&stage[w][0]) + lane * 32;  // 32 slots / lane
-    const int nl = min(s - 1, k);
-    if (u >= 0) {
-      c2_cand *o = seed ? loc : out + ((int64_t)I.f * n + u) * k;
-      for (int j = 0; j < s; ++j) {
-        if (j == lane) continue;
-        int32_t vj = sid[w][j];
-        uint32_t ij = cnt[w][lane][j], Uj = len + sps[w][j] - ij;
-        int rank = 0;
-        for (int j2 = 0; j2 < s; ++j2) {
-          if (j2 == lane || j2 == j) continue;
-          uint32_t i2 = cnt[w][lane][j2], U2 = len + sps[w][j2] - i2;
-          rank += c2d::better(i2, U2, sid[w][j2], ij, Uj, vj);
-        }
-        if (rank < k) o[rank] = c2_cand{vj, (uint16_t)ij, (uint16_t)Uj};
-      }
-      if (!seed)
-        for (int q = s - 1; q < k; ++q) o[q] = c2_cand{-1, 0, 0};
-    }
-    __syncwarp();
-    if (seed && u >= 0) {
-      // Alg. 3: merge the running list of u with the local list (both best first), dedup
-      const c2_cand *Rin = seed + (int64_t)u * k;
-      c2_cand *Rout = out + (int64_t)u * k;
-      int i = 0, j = 0, o = 0;
-      c2_cand a = Rin[0];
-      while (o < k) {
-        bool ha = i < k && a.id >= 0, hb = j < nl;
-        if (!ha && !hb) break;
-        c2_cand b = hb ? loc[j] : c2_cand{-1, 0, 0};
-        c2_cand e;
-        if (ha && hb && a.id == b.id) {
-          e = a;
-          ++i;
-          ++j;
-          a = i < k ? Rin[i] : c2_cand{-1, 0, 0};
-        } else if (ha && (!hb || c2d::better(a.inter, a.uni, a.id, b.inter, b.uni, b.id))) {
-          e = a;
-          ++i;
-          a = i < k ? Rin[i] : c2_cand{-1, 0, 0};
-        } else {
-          e = b;
-          ++j;
-        }
-        Rout[o++] = e;
-      }
-      for (; o < k; ++o) Rout[o] = c2_cand{-1, 0, 0};
-    }
-    __syncwarp();
-  }
-}
-
 // ------------------------------------------------------------------ K7 tile kernel
 __device__ __forceinline__ void csa(uint32_t &h, uint32_t &l, uint32_t a, uint32_t b, uint32_t c) {
   uint32_t u = a ^ b;
@@ -663,20 +515,40 @@ struct Counter {
   }
 };
 
+// Shared-memory words the K8 phase needs (aliased onto the M region, which is all zero
+// between tiles): staged (id, |P|) of the cluster, per-row tops, per-row survivor queues.
+template <int KS>
+struct K8Smem {
+  static constexpr int QCAP = 64 * KS;                 // survivors kept per row
+  static constexpr int TOPS = 32 * KS;                 // tops per row (16 segments x 2KS)
+  static constexpr int VID = 0;                        // STAGE_V ints
+  static constexpr int VPS = STAGE_V;                  // STAGE_V uints
+  static constexpr int TOP = 2 * STAGE_V;              // 32 x TOPS Cand
+  static constexpr int QUE = TOP + 32 * TOPS * 2;      // 32 x QCAP Cand
+  static constexpr int WORDS = QUE + 32 * QCAP * 2;
+};
+
 template <int NHI, int VPT, int KS>
 __global__ void __launch_bounds__(TILE_T, 1) k_local_tile(TileArgs a) {
+  using SM = K8Smem<KS>;
   extern __shared__ __align__(16) uint32_t dyn[];
-  uint32_t *M = dyn;                                                // W + 1 words; M[W] == 0
-  int32_t *s_vid = reinterpret_cast<int32_t *>(dyn + ((a.W + 4) & ~3));  // STAGE_V
-  uint32_t *s_vps = reinterpret_cast<uint32_t *>(s_vid + STAGE_V);       // STAGE_V
+  uint32_t *M = dyn;  // phase A: W + 1 words, M[W] == 0.  K8: aliased by the SM regions.
+  int32_t *s_vid = reinterpret_cast<int32_t *>(dyn + SM::VID);
+  uint32_t *s_vps = dyn + SM::VPS;
+  Cand *s_tops = reinterpret_cast<Cand *>(dyn + SM::TOP);
+  Cand *s_q = reinterpret_cast<Cand *>(dyn + SM::QUE);
   __shared__ int s_item;
   __shared__ int32_t s_ru[32];
   __shared__ uint32_t s_rp[32];
+  __shared__ int s_qn[32];
+  __shared__ Cand s_tau[32], s_T[32];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  for (int i = tid; i <= a.W; i += TILE_T) M[i] = 0;
-  uint16_t *cnt = a.scratch + (int64_t)blockIdx.x * 32 * a.smax;
+  const int zero_words = max(a.W + 1, SM::WORDS);
+  for (int i = tid; i < zero_words; i += TILE_T) M[i] = 0;
+  uint16_t *cnt = a.scratch + (int64_t)blockIdx.x * 32 * a.smax;  // [v][32 rows]
   const int nwin = a.nwin;
   const uint32_t W = (uint32_t)a.W;
+  const int kk = a.k;
   for (;;) {
     __syncthreads();
     if (tid == 0) s_item = atomicAdd(a.counter, 1);
@@ -685,22 +557,19 @@ __global__ void __launch_bounds__(TILE_T, 1) k_local_tile(TileArgs a) {
     if (it >= a.hi) break;
     const Tile T = a.tiles[it];
     const BigC B = a.bcs[T.bc];
-    const int nsl = (B.s + 31) >> 5;
+    const int s = B.s;
+    const int nsl = (s + 31) >> 5;
     const int r0 = T.j * 32;
-    const int nr = min(32, B.s - r0);
+    const int nr = min(32, s - r0);
     const int32_t *vp = a.vperm + B.vp_off;
-    const bool vstaged = B.s <= STAGE_V;
-    if (vstaged)
-      for (int i = tid; i < B.s; i += TILE_T) {
-        int32_t v = vp[i];
-        s_vid[i] = v;
-        s_vps[i] = (uint32_t)a.psize[v];
-      }
     if (tid < 32) {
       int32_t u = tid < nr ? vp[r0 + tid] : -1;
       s_ru[tid] = u;
       s_rp[tid] = u >= 0 ? (uint32_t)a.psize[u] : 0u;
+      s_qn[tid] = 0;
+      s_tau[tid] = (u >= 0 && a.seed) ? from_out(a.seed[(int64_t)u * kk + kk - 1]) : sent();
     }
+    // ================= phase A: counts |P_r ∩ P_v| for the 32 rows x all v of the cluster
     for (int g0 = 0; g0 < nsl; g0 += VPT * TILE_WARPS) {
       Counter<NHI> C[VPT];
 #pragma unroll
@@ -767,7 +636,7 @@ __global__ void __launch_bounds__(TILE_T, 1) k_local_tile(TileArgs a) {
         }
         __syncthreads();
       }
-      // ---- counts: planes -> 32 counts per v (transpose), to scratch [row][v]
+      // ---- planes -> 32 counts per v (transpose); scratch row of v = 32 u16 (64 B)
 #pragma unroll
       for (int q = 0; q < VPT; ++q) {
         const int jj = g0 + q * TILE_WARPS + warp;
@@ -783,41 +652,169 @@ __global__ void __launch_bounds__(TILE_T, 1) k_local_tile(TileArgs a) {
 #pragma unroll
           for (int i = 4 + NHI; i < 32; ++i) A[i] = 0;
           transpose32(A);
-          if (vi < B.s) {
+          if (vi < s) {
+            uint4 *dst = reinterpret_cast<uint4 *>(cnt + (int64_t)vi * 32);
 #pragma unroll
-            for (int r = 0; r < 32; ++r)
-              if (r < nr) cnt[(int64_t)r * a.smax + vi] = (uint16_t)A[r];
+            for (int j = 0; j < 4; ++j)
+              dst[j] = make_uint4(A[8 * j] | (A[8 * j + 1] << 16), A[8 * j + 2] | (A[8 * j + 3] << 16),
+                                  A[8 * j + 4] | (A[8 * j + 5] << 16), A[8 * j + 6] | (A[8 * j + 7] << 16));
           }
         }
       }
     }
     __syncthreads();
-    // ---- K8: per-row top-k, warp per row
-    const int kk = a.k;
-    for (int r = warp; r < nr; r += TILE_WARPS) {
-      const int32_t ur = s_ru[r];
-      const uint32_t pr = s_rp[r];
-      const uint16_t *crow = cnt + (int64_t)r * a.smax;
-      const int s = B.s;
-      auto get = [&](int vi) -> Cand {
-        if (vi >= s) return sent();
-        int32_t v;
-        uint32_t ps;
-        if (vstaged) {
-          v = s_vid[vi];
-          ps = s_vps[vi];
-        } else {
-          v = vp[vi];
-          ps = (uint32_t)a.psize[v];
+    // ================= K8: exact top-k per row (lane = row, warps split the candidates)
+    const bool vstaged = s <= STAGE_V;
+    if (vstaged)
+      for (int i = tid; i < s; i += TILE_T) {
+        int32_t v = vp[i];
+        s_vid[i] = v;
+        s_vps[i] = v >= 0 ? (uint32_t)a.psize[v] : 0u;
+      }
+    __syncthreads();
+    const int32_t ur = s_ru[lane];
+    const uint32_t pr = s_rp[lane];
+    const Cand tau = s_tau[lane];
+    const bool rowok = lane < nr && ur >= 0;
+    const int slot = B.slot;  // mixed slice: candidates only inside the row's own slot group
+    auto cand_of = [&](int vi, bool &ok) -> Cand {
+      int32_t v;
+      uint32_t ps;
+      if (vstaged) {
+        v = s_vid[vi];
+        ps = s_vps[vi];
+      } else {
+        v = vp[vi];
+        ps = v >= 0 ? (uint32_t)a.psize[v] : 0u;
+      }
+      uint32_t ci = cnt[(int64_t)vi * 32 + lane];
+      ok = rowok && v >= 0 && v != ur && (slot == 0 || (vi ^ lane) < slot);
+      return Cand{ci | ((pr + ps - ci) << 16), v};
+    };
+    // round 1: each thread's best 2KS candidates above tau in its segment
+    {
+      constexpr int R = 2 * KS;
+      Cand t[R];
+#pragma unroll
+      for (int j = 0; j < R; ++j) t[j] = sent();
+      for (int vi = warp; vi < s; vi += TILE_WARPS) {
+        bool ok;
+        Cand c = cand_of(vi, ok);
+        if (ok && better_c(c, tau) && better_c(c, t[R - 1])) {
+#pragma unroll
+          for (int j = R - 1; j > 0; --j) {
+            if (better_c(c, t[j - 1])) t[j] = t[j - 1];
+            else if (better_c(c, t[j])) t[j] = c;
+          }
+          if (better_c(c, t[0])) t[0] = c;
         }
-        if (v == ur) return sent();
-        uint32_t ci = crow[vi];
-        return Cand{ci | ((pr + ps - ci) << 16), v};
-      };
-      const c2_cand *seed = a.seed ? a.seed + (int64_t)ur * kk : nullptr;
-      c2_cand *dst = a.seed ? a.out + (int64_t)ur * kk : a.out + ((int64_t)B.f * a.n + ur) * kk;
-      row_topk<2 * KS>(s, kk, get, seed, dst);
+      }
+#pragma unroll
+      for (int j = 0; j < R; ++j) s_tops[lane * SM::TOPS + warp * R + j] = t[j];
     }
+    __syncthreads();
+    // threshold T_r = k-th best of the row's tops (k distinct real candidates are >= T_r)
+    for (int r = warp; r < nr; r += TILE_WARPS) {
+      Cand e[KS];
+#pragma unroll
+      for (int j = 0; j < KS; ++j) e[j] = s_tops[r * SM::TOPS + 32 * j + lane];
+      warp_sort<KS>(e);
+      Cand Tr = warp_get<KS>(e, kk - 1);
+      if (lane == 0) s_T[r] = Tr;
+    }
+    __syncthreads();
+    // round 2: survivors (above tau and not below T_r) to the row's queue
+    {
+      const Cand Tr = s_T[lane];
+      for (int vi = warp; vi < s; vi += TILE_WARPS) {
+        bool ok;
+        Cand c = cand_of(vi, ok);
+        if (ok && better_c(c, tau) && !better_c(Tr, c)) {
+          int p = atomicAdd(&s_qn[lane], 1);
+          if (p < SM::QCAP) s_q[lane * SM::QCAP + p] = c;
+        }
+      }
+    }
+    __syncthreads();
+    // final: per row (warp per row) sort the survivors, merge with the seed, write k
+    for (int r = warp; r < nr; r += TILE_WARPS) {
+      const int32_t u = s_ru[r];
+      if (u < 0) continue;
+      const int nq = s_qn[r];
+      const c2_cand *seed = a.seed ? a.seed + (int64_t)u * kk : nullptr;
+      c2_cand *dst = a.seed ? a.out + (int64_t)u * kk : a.out + ((int64_t)B.f * a.n + u) * kk;
+      Cand L[KS];  // top-k of this function's candidates above tau (sentinel padded)
+      if (nq <= SM::QCAP) {
+        Cand q[2 * KS];
+#pragma unroll
+        for (int j = 0; j < 2 * KS; ++j) q[j] = (32 * j + lane < nq) ? s_q[r * SM::QCAP + 32 * j + lane] : sent();
+        warp_sort<2 * KS>(q);
+#pragma unroll
+        for (int j = 0; j < KS; ++j) L[j] = q[j];
+      } else {
+        // rare overflow: exact insertion over all the row's candidates
+#pragma unroll
+        for (int j = 0; j < KS; ++j) L[j] = sent();
+        const Cand tr = s_tau[r];
+        const uint32_t prr = s_rp[r];
+        Cand thr = sent();
+        for (int vb = 0; vb < s; vb += 32) {
+          const int vi = vb + lane;
+          Cand c = sent();
+          if (vi < s) {
+            int32_t v = vstaged ? s_vid[vi] : vp[vi];
+            if (v >= 0 && v != u && (slot == 0 || (vi ^ r) < slot)) {
+              uint32_t ps = vstaged ? s_vps[vi] : (uint32_t)a.psize[v];
+              uint32_t ci = cnt[(int64_t)vi * 32 + r];
+              c = Cand{ci | ((prr + ps - ci) << 16), v};
+            }
+          }
+          bool bt = is_real(c) && better_c(c, tr) && better_c(c, thr);
+          unsigned mask = __ballot_sync(0xffffffffu, bt);
+          while (mask) {
+            int l = __ffs(mask) - 1;
+            mask &= mask - 1;
+            Cand x = shfl_c(c, l);
+            if (!better_c(x, thr)) continue;
+            warp_insert<KS>(L, x);
+            thr = warp_get<KS>(L, kk - 1);
+          }
+        }
+      }
+      if (!seed) {
+#pragma unroll
+        for (int j = 0; j < KS; ++j)
+          if (32 * j + lane < kk) dst[32 * j + lane] = to_out(L[j]);
+        continue;
+      }
+      // merge with the seed S (best first): bitonic sequence L(first k) ++ reverse(S)
+      Cand S[KS];
+#pragma unroll
+      for (int j = 0; j < KS; ++j) S[j] = (32 * j + lane < kk) ? from_out(seed[32 * j + lane]) : sent();
+      Cand m[2 * KS];
+#pragma unroll
+      for (int j = 0; j < KS; ++j) m[j] = (32 * j + lane < kk) ? L[j] : sent();
+#pragma unroll
+      for (int j = 0; j < KS; ++j) m[KS + j] = shfl_c(S[KS - 1 - j], 31 - lane);
+      warp_bitonic_merge<2 * KS>(m);
+      // drop adjacent duplicates (a repeated id carries identical values, A16); keep k
+      int base = 0;
+#pragma unroll
+      for (int j = 0; j < 2 * KS; ++j) {
+        int32_t prev = __shfl_up_sync(0xffffffffu, m[j].id, 1);
+        int32_t prevj = j > 0 ? __shfl_sync(0xffffffffu, m[j - 1].id, 31) : -2;
+        if (lane == 0) prev = prevj;
+        bool keep = is_real(m[j]) && m[j].id != prev;
+        unsigned bal = __ballot_sync(0xffffffffu, keep);
+        int rank = base + __popc(bal & ((1u << lane) - 1));
+        if (keep && rank < kk) dst[rank] = to_out(m[j]);
+        base += __popc(bal);
+      }
+      for (int p = base + lane; p < kk; p += 32) dst[p] = c2_cand{-1, 0, 0};
+    }
+    __syncthreads();
+    // restore the all-zero M region
+    for (int i = tid; i < SM::WORDS; i += TILE_T) dyn[i] = 0;
   }
 }
 
@@ -858,13 +855,6 @@ __global__ void k_work_steps(const int32_t *__restrict__ offsets, const int32_t 
   if ((threadIdx.x & 31) == 0 && w) atomicAdd(acc, w);
 }
 
-__global__ void k_count_small_f(const SmallItem *__restrict__ w, int64_t ns, int32_t *__restrict__ per_f) {
-  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < ns) atomicAdd(&per_f[w[i].f], 1);
-}
-
-// fused: `out` holds 2*n*k entries (ping-pong running lists); *result = the final one.
-// local: out = cand [t][n][k].
 int local_knn(c2_ctx *ctx, const Csr &csr, int t, const Clusters &cl, int k, c2_cand *out, bool fused,
               c2_cand **result) {
   int rc;
@@ -874,48 +864,63 @@ int local_knn(c2_ctx *ctx, const Csr &csr, int t, const Clusters &cl, int k, c2_
   hcum[0] = 0;
   for (int f = 0; f < t; ++f) hcum[f + 1] = hcum[f] + cl.n_clusters[f];
   const int64_t C = hcum[t];
-  int32_t *ccum = (int32_t *)ws_get(ctx, "wl_ccum", (C2_MAX_T + 1) * 4 + 4 * (2 * C2_MAX_T + 2), &rc);
+  int32_t *ccum = (int32_t *)ws_get(ctx, "wl_ccum", (C2_MAX_T + 1) * 4 + 4 * 8 * C2_MAX_T, &rc);
   if (rc) return rc;
-  int32_t *per_f = ccum + C2_MAX_T + 1;  // [0..t) tiles per f, [t..2t) small per f
+  int32_t *cnt_fc = ccum + C2_MAX_T + 1;  // [f][8]: 0 big tiles, 1..5 small per class, 6 single, 7 big
   C2_CUDA(ctx, cudaMemcpyAsync(ccum, hcum, (t + 1) * 4, cudaMemcpyHostToDevice, st));
-  C2_CUDA(ctx, cudaMemsetAsync(per_f, 0, 4 * 2 * C2_MAX_T, st));
-  int32_t *fl = (int32_t *)ws_get(ctx, "wl_flags", (size_t)(C + 1) * 4 * 2, &rc);
-  if (rc) return rc;
-  int32_t *fsmall = fl, *sscan = fl + (C + 1);
+  C2_CUDA(ctx, cudaMemsetAsync(cnt_fc, 0, 4 * 8 * C2_MAX_T, st));
   uint32_t *kv = (uint32_t *)ws_get(ctx, "wl_kv", (size_t)C * 4 * 4 + 16, &rc);
   if (rc) return rc;
   uint32_t *key = kv, *val = kv + C, *skey = kv + 2 * C, *sval = kv + 3 * C;
   const uint32_t maxs = (uint32_t)std::max(cl.max_size, 1);
-  const int sized = maxs < (1u << 25) ? 1 : 0;
-  k_wl_classify<<<nblk(C), 256, 0, st>>>(cl.offsets, ccum, t, n, C, fsmall, key, val, maxs, sized);
+  const int sized = maxs < (1u << 24) ? 1 : 0;
+  k_wl_classify<<<nblk(C), 256, 0, st>>>(cl.offsets, ccum, t, n, C, key, val, maxs, sized, cnt_fc);
   C2_LAUNCHED(ctx, "k_wl_classify");
-  C2_TRY(scan_exclusive(ctx, fsmall, sscan, C));
   C2_TRY(radix_sort_pairs(ctx, key, val, skey, sval, C, 32));
-  int32_t hs;
-  C2_CUDA(ctx, cudaMemcpyAsync(&hs, sscan + C, 4, cudaMemcpyDeviceToHost, st));
-  C2_TRY(stream_sync(ctx, "worklist counts"));
-  const int64_t nsmall = hs, nbig = C - hs;
-  SmallItem *wsmall = (SmallItem *)ws_get(ctx, "wl_small", (size_t)(nsmall + 1) * sizeof(SmallItem), &rc);
-  if (rc) return rc;
-  k_wl_small<<<nblk(C), 256, 0, st>>>(cl.offsets, ccum, t, n, C, fsmall, sscan, wsmall);
-  C2_LAUNCHED(ctx, "k_wl_small");
-  if (nsmall > 0) {
-    k_count_small_f<<<nblk(nsmall), 256, 0, st>>>(wsmall, nsmall, per_f + t);
-    C2_LAUNCHED(ctx, "k_count_small_f");
-  }
   unsigned long long *wacc = (unsigned long long *)ws_get(ctx, "work_acc", 16, &rc);
   if (rc) return rc;
   C2_CUDA(ctx, cudaMemsetAsync(wacc, 0, 8, st));
   k_work_steps<<<nblk((int64_t)t * n), 256, 0, st>>>(cl.offsets, cl.cluster_of, csr.psize, (int64_t)t * n, n, wacc);
   C2_LAUNCHED(ctx, "k_work_steps");
+  int32_t hfc[8 * C2_MAX_T];
+  unsigned long long hwork = 0;
+  C2_CUDA(ctx, cudaMemcpyAsync(hfc, cnt_fc, 4 * 8 * t, cudaMemcpyDeviceToHost, st));
+  C2_CUDA(ctx, cudaMemcpyAsync(&hwork, wacc, 8, cudaMemcpyDeviceToHost, st));
+  C2_TRY(stream_sync(ctx, "worklist counts"));
+  ctx->stats.work_steps = (int64_t)hwork;
+  int64_t nbig = 0, nsmall = 0, nsingle = 0, nbigtiles = 0;
+  for (int f = 0; f < t; ++f) {
+    nbig += hfc[f * 8 + 7];
+    nbigtiles += hfc[f * 8 + 0];
+    for (int c = 1; c <= 5; ++c) nsmall += hfc[f * 8 + c];
+    nsingle += hfc[f * 8 + 6];
+  }
+  // mixed slices: groups (f, class) in sorted order
+  std::vector<MixGroup> groups;
+  int64_t nmix = 0, entry = 0;
+  std::vector<int64_t> mix_lo(t + 1, 0);
+  for (int f = 0; f < t; ++f) {
+    mix_lo[f] = nmix;
+    for (int c = 1; c <= 5; ++c) {
+      int32_t cntc = hfc[f * 8 + c];
+      if (!cntc) continue;
+      int per = 32 >> c;
+      groups.push_back(MixGroup{f, c, (int32_t)entry, cntc, (int32_t)nmix});
+      entry += cntc;
+      nmix += (cntc + per - 1) / per;
+    }
+  }
+  mix_lo[t] = nmix;
+
   c2_cand *R[2] = {out, out + (int64_t)n * k};
   if (fused) {
     k_init_pads<<<nblk((int64_t)n * k), 256, 0, st>>>(R[0], (int64_t)n * k);
     C2_LAUNCHED(ctx, "k_init_pads");
   }
 
-  // ---- big clusters: descriptors, tiles, length-sorted member order, packed lists
-  int64_t nslices = 0;
+  // ---- tile descriptors: big clusters (length-sorted members) + mixed slices
+  const int64_t ncl = nbig + nmix;
+  const int64_t nslices = nbigtiles + nmix;
   BigC *bcs = nullptr;
   Tile *tiles = nullptr;
   int32_t *vperm = nullptr, *blk_len8 = nullptr, *blk_off8 = nullptr;
@@ -924,30 +929,47 @@ int local_knn(c2_ctx *ctx, const Csr &csr, int t, const Clusters &cl, int k, c2_
   int32_t nwin = (int32_t)((m + 50000 - 1) / 50000);
   int32_t W = (int32_t)((m + nwin - 1) / nwin);
   if (nwin > MAX_WIN) return set_err(ctx, C2_EINVAL, "item ids up to %d need %d windows (max %d)", m, nwin, MAX_WIN);
-  if (nbig > 0) {
-    int32_t *bsz = (int32_t *)ws_get(ctx, "bc_sz", (size_t)(nbig + 1) * 4 * 4, &rc);
-    if (rc) return rc;
-    int32_t *bns = bsz + (nbig + 1), *vp_scan = bsz + 2 * (nbig + 1), *sl_scan = bsz + 3 * (nbig + 1);
-    k_bc_sizes<<<nblk(nbig), 256, 0, st>>>(sval, nbig, cl.offsets, ccum, t, n, bsz, bns);
-    C2_LAUNCHED(ctx, "k_bc_sizes");
-    C2_TRY(scan_exclusive(ctx, bsz, vp_scan, nbig));
-    C2_TRY(scan_exclusive(ctx, bns, sl_scan, nbig));
-    int32_t h2[2];
-    C2_CUDA(ctx, cudaMemcpyAsync(h2, vp_scan + nbig, 4, cudaMemcpyDeviceToHost, st));
-    C2_CUDA(ctx, cudaMemcpyAsync(h2 + 1, sl_scan + nbig, 4, cudaMemcpyDeviceToHost, st));
-    C2_TRY(stream_sync(ctx, "big cluster sizes"));
-    const int64_t nv = h2[0];
-    nslices = h2[1];
-    bcs = (BigC *)ws_get(ctx, "bc", (size_t)nbig * sizeof(BigC), &rc);
+  if (nslices > 0) {
+    bcs = (BigC *)ws_get(ctx, "bc", (size_t)ncl * sizeof(BigC), &rc);
     if (rc) return rc;
     tiles = (Tile *)ws_get(ctx, "tiles", (size_t)nslices * sizeof(Tile), &rc);
     if (rc) return rc;
-    vperm = (int32_t *)ws_get(ctx, "vperm", (size_t)nv * 4, &rc);
+    int64_t nv_big = 0;
+    int32_t *bsz = (int32_t *)ws_get(ctx, "bc_sz", (size_t)(nbig + 1) * 4 * 5, &rc);
     if (rc) return rc;
-    k_bc_fill<<<nblk(nbig), 256, 0, st>>>(sval, nbig, cl.offsets, ccum, t, n, vp_scan, sl_scan, bcs, tiles, per_f);
-    C2_LAUNCHED(ctx, "k_bc_fill");
-    k_sl_sort<<<(unsigned)nbig, 1024, 0, st>>>(bcs, cl.members, n, csr.psize, vperm);
-    C2_LAUNCHED(ctx, "k_sl_sort");
+    int32_t *bns = bsz + (nbig + 1), *vp_scan = bsz + 2 * (nbig + 1), *sl_scan = bsz + 3 * (nbig + 1);
+    int32_t *bstart = bsz + 4 * (nbig + 1);
+    if (nbig > 0) {
+      k_bc_sizes<<<nblk(nbig), 256, 0, st>>>(sval, nbig, cl.offsets, ccum, t, n, bsz, bns);
+      C2_LAUNCHED(ctx, "k_bc_sizes");
+      C2_TRY(scan_exclusive(ctx, bsz, vp_scan, nbig));
+      C2_TRY(scan_exclusive(ctx, bns, sl_scan, nbig));
+      int32_t h1;
+      C2_CUDA(ctx, cudaMemcpyAsync(&h1, vp_scan + nbig, 4, cudaMemcpyDeviceToHost, st));
+      C2_TRY(stream_sync(ctx, "big cluster sizes"));
+      nv_big = h1;
+    }
+    vperm = (int32_t *)ws_get(ctx, "vperm", (size_t)(nv_big + nmix * 32 + 1) * 4, &rc);
+    if (rc) return rc;
+    if (nbig > 0) {
+      k_bc_fill<<<nblk(nbig), 256, 0, st>>>(sval, nbig, cl.offsets, ccum, t, n, vp_scan, sl_scan, bcs, tiles, bstart);
+      C2_LAUNCHED(ctx, "k_bc_fill");
+      k_sl_sort<<<(unsigned)nbig, 1024, 0, st>>>(bcs, bstart, cl.members, n, csr.psize, vperm);
+      C2_LAUNCHED(ctx, "k_sl_sort");
+    }
+    if (nmix > 0) {
+      MixGroup *dgroups = (MixGroup *)ws_get(ctx, "mix_groups", groups.size() * sizeof(MixGroup), &rc);
+      if (rc) return rc;
+      C2_CUDA(ctx, cudaMemcpyAsync(dgroups, groups.data(), groups.size() * sizeof(MixGroup), cudaMemcpyHostToDevice,
+                                   st));
+      C2_CUDA(ctx, cudaMemsetAsync(vperm + nv_big, 0xFF, (size_t)nmix * 32 * 4, st));
+      k_mix_fill<<<nblk(nsmall), 256, 0, st>>>(sval + nbig, nsmall, cl.offsets, ccum, t, n, cl.members, dgroups,
+                                               (int)groups.size(), (int32_t)nv_big, vperm);
+      C2_LAUNCHED(ctx, "k_mix_fill");
+      k_mix_bc<<<nblk(nmix), 256, 0, st>>>(dgroups, (int)groups.size(), nmix, nbig, (int32_t)nv_big, nbigtiles, bcs,
+                                           tiles);
+      C2_LAUNCHED(ctx, "k_mix_bc");
+    }
     const int64_t nb = nslices * nwin;
     blk_len8 = (int32_t *)ws_get(ctx, "blk_len8", (size_t)(2 * nb + 2) * 4, &rc);
     if (rc) return rc;
@@ -964,20 +986,14 @@ int local_knn(c2_ctx *ctx, const Csr &csr, int t, const Clusters &cl, int k, c2_
                                                   blk_off8, packed);
     C2_LAUNCHED(ctx, "k_sl_fill");
   }
-  int32_t hper[2 * C2_MAX_T];
-  unsigned long long hwork = 0;
-  C2_CUDA(ctx, cudaMemcpyAsync(hper, per_f, 4 * 2 * C2_MAX_T, cudaMemcpyDeviceToHost, st));
-  C2_CUDA(ctx, cudaMemcpyAsync(&hwork, wacc, 8, cudaMemcpyDeviceToHost, st));
-  C2_TRY(stream_sync(ctx, "per-function counts"));
-  ctx->stats.work_steps = (int64_t)hwork;
 
   // ---- tile kernel configuration
   TileKernel tk = nullptr;
   int grid = 0;
-  const size_t smem = (size_t)((W + 4) & ~3) * 4 + (size_t)STAGE_V * 8;
+  const size_t smem = (size_t)std::max<int64_t>((W + 4) & ~3, k <= 32 ? K8Smem<1>::WORDS : K8Smem<2>::WORDS) * 4;
   uint16_t *scratch = nullptr;
   int *counters = nullptr;
-  int32_t smax = (int32_t)((maxs + 31) / 32 * 32);
+  const int32_t smax = (int32_t)((std::max<uint32_t>(maxs, 32) + 31) / 32 * 32);
   if (nslices > 0) {
     int nbits = bits_for((int64_t)csr.max_len + 1);
     int nhi = std::max(nbits - 4, 1);
@@ -991,20 +1007,10 @@ int local_knn(c2_ctx *ctx, const Csr &csr, int t, const Clusters &cl, int k, c2_
     grid = (int)std::min<int64_t>((int64_t)ctx->num_sms * occ, nslices);
     scratch = (uint16_t *)ws_get(ctx, "tile_scratch", (size_t)grid * 32 * smax * 2, &rc);
     if (rc) return rc;
-    counters = (int *)ws_get(ctx, "tile_counter", 4 * (C2_MAX_T + 1), &rc);
+    counters = (int *)ws_get(ctx, "tile_counter", 4 * (2 * C2_MAX_T + 2), &rc);
     if (rc) return rc;
-    C2_CUDA(ctx, cudaMemsetAsync(counters, 0, 4 * (C2_MAX_T + 1), st));
+    C2_CUDA(ctx, cudaMemsetAsync(counters, 0, 4 * (2 * C2_MAX_T + 2), st));
   }
-  auto launch_small = [&](int64_t lo, int64_t hi, const c2_cand *seed, c2_cand *dst) -> int {
-    if (hi <= lo) return C2_OK;
-    int64_t blocks = std::min<int64_t>((hi - lo + SMALL_WARPS - 1) / SMALL_WARPS, (int64_t)ctx->num_sms * 16);
-    const size_t ssm = (size_t)SMALL_WARPS * SMALL_STAGE * 4;
-    C2_CUDA(ctx, cudaFuncSetAttribute(k_local_small, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ssm));
-    k_local_small<<<(unsigned)blocks, SMALL_WARPS * 32, ssm, st>>>(wsmall, lo, hi, cl.members, n, csr.offs,
-                                                                   csr.items, csr.psize, k, seed, dst);
-    C2_LAUNCHED(ctx, "k_local_small");
-    return C2_OK;
-  };
   auto launch_tiles = [&](int64_t lo, int64_t hi, int ci, const c2_cand *seed, c2_cand *dst) -> int {
     if (hi <= lo) return C2_OK;
     TileArgs ta{tiles, lo, hi, counters + ci, bcs, vperm, blk_len8, blk_off8, packed, csr.psize, n, W, nwin, k,
@@ -1028,21 +1034,29 @@ int local_knn(c2_ctx *ctx, const Csr &csr, int t, const Clusters &cl, int k, c2_
     ctx->stats.tile_launches++;
     return C2_OK;
   };
+  auto launch_singles = [&](int64_t lo, int64_t hi, const c2_cand *seed, c2_cand *dst) -> int {
+    if (hi <= lo) return C2_OK;
+    k_singles<<<nblk((hi - lo) * k), 256, 0, st>>>(sval + nbig + nsmall, nsingle, cl.offsets, ccum, t, n, cl.members,
+                                                   k, lo, hi, seed, dst);
+    C2_LAUNCHED(ctx, "k_singles");
+    return C2_OK;
+  };
   if (!fused) {
-    C2_TRY(launch_small(0, nsmall, nullptr, out));
     C2_TRY(launch_tiles(0, nslices, 0, nullptr, out));
+    C2_TRY(launch_singles(0, nsingle, nullptr, out));
     if (result) *result = out;
   } else {
     // Alg. 3 order: function by function, every user's running list (R[cur]) is merged with
     // its neighbourhood in that function's cluster into R[cur ^ 1]
-    int64_t slo = 0, tlo = 0;
+    int64_t blo = 0, slo = 0;
     int cur = 0;
     for (int f = 0; f < t; ++f) {
-      int64_t shi = slo + hper[t + f], thi = tlo + hper[f];
-      C2_TRY(launch_tiles(tlo, thi, f, R[cur], R[cur ^ 1]));
-      C2_TRY(launch_small(slo, shi, R[cur], R[cur ^ 1]));
+      int64_t bhi = blo + hfc[f * 8 + 0], shi = slo + hfc[f * 8 + 6];
+      C2_TRY(launch_tiles(blo, bhi, 2 * f, R[cur], R[cur ^ 1]));
+      C2_TRY(launch_tiles(nbigtiles + mix_lo[f], nbigtiles + mix_lo[f + 1], 2 * f + 1, R[cur], R[cur ^ 1]));
+      C2_TRY(launch_singles(slo, shi, R[cur], R[cur ^ 1]));
+      blo = bhi;
       slo = shi;
-      tlo = thi;
       cur ^= 1;
     }
     if (result) *result = R[cur];
