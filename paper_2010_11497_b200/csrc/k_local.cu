@@ -449,7 +449,30 @@ __device__ __forceinline__ void transpose32(uint32_t (&A)[32]) {
   }
 }
 
-constexpr int STAGE_V = 2048;  // cluster members whose (id, |P|) are staged in shared memory
+// Shared-memory layout of the K8 phase (32-bit words), aliased onto the M region once phase A
+// is done (M is dead then).  Depends on the tile's cluster size s:
+//   cnt  [32 rows][RS] u16   |P_r ∩ P_v| by (row, member position); RS = 64*ceil(s/64)+4, so a
+//                            warp reading 4 consecutive counts per row (LDS.64, lane = row) is
+//                            bank-conflict free
+//   vid  [s4] int32          member ids (positions >= s: INT32_MAX)
+//   vps  [s4] uint32         member |P_v| (positions >= s: 0)
+//   top  [32][32*KS] Cand    round-1 survivors per row (each thread's best 2*KS)
+//   que  [32][64*KS] Cand    round-2 survivors per row
+template <int KS>
+struct K8Lay {
+  static constexpr int QCAP = 64 * KS;
+  static constexpr int TOPS = 32 * KS;
+  int RS, vid, vps, top, que, words;
+  __host__ __device__ __forceinline__ explicit K8Lay(int s) {
+    RS = ((s + 63) / 64) * 64 + 4;
+    const int s4 = (s + 3) & ~3;
+    vid = 16 * RS;
+    vps = vid + s4;
+    top = vps + s4;
+    que = top + 32 * TOPS * 2;
+    words = que + 32 * QCAP * 2;
+  }
+};
 
 struct TileArgs {
   const Tile *tiles;
@@ -466,7 +489,7 @@ struct TileArgs {
   int k;
   const c2_cand *seed;  // fused: running lists before this function [n][k]; else nullptr
   c2_cand *out;         // local: cand [t][n][k]; fused: running lists after this function
-  uint16_t *scratch;    // [grid][32][smax]
+  uint32_t *gscratch;   // !SMEM_CNT only: per CTA K8Lay<KS>(smax).words words
   int32_t smax;
 };
 
@@ -515,37 +538,38 @@ struct Counter {
   }
 };
 
-// Shared-memory words the K8 phase needs (aliased onto the M region, which is all zero
-// between tiles): staged (id, |P|) of the cluster, per-row tops, per-row survivor queues.
-template <int KS>
-struct K8Smem {
-  static constexpr int QCAP = 64 * KS;                 // survivors kept per row
-  static constexpr int TOPS = 32 * KS;                 // tops per row (16 segments x 2KS)
-  static constexpr int VID = 0;                        // STAGE_V ints
-  static constexpr int VPS = STAGE_V;                  // STAGE_V uints
-  static constexpr int TOP = 2 * STAGE_V;              // 32 x TOPS Cand
-  static constexpr int QUE = TOP + 32 * TOPS * 2;      // 32 x QCAP Cand
-  static constexpr int WORDS = QUE + 32 * QCAP * 2;
+// A fixed reference candidate of row r (|P_r| = pr) in the form that makes the order test of a
+// candidate (i, |P_v|, id) two multiply-adds: with U = pr + |P_v| - i and the reference (iT, UT),
+//   i*UT > iT*U  <=>  i*(UT + iT) > iT*|P_v| + iT*pr.
+// Both sides fit in 32 bits (i <= 32767, U <= 65534, A28).  Ties are decided by id < idlim
+// (idlim = idT: strictly better; idT + 1: better or the reference itself).  Unsigned id compare:
+// an id of -1 (empty position of a mixed slice) never passes a tie.
+struct Ref {
+  uint32_t A, B, iT, idlim;
 };
+__device__ __forceinline__ Ref make_ref(Cand t, uint32_t pr, bool or_equal) {
+  const uint32_t i = t.iu & 0xFFFFu, U = t.iu >> 16;
+  return Ref{U + i, i * pr, i, (uint32_t)t.id + (or_equal ? 1u : 0u)};
+}
+__device__ __forceinline__ bool passes(uint32_t i, uint32_t ps, int32_t id, const Ref &R) {
+  const uint32_t l = i * R.A, r = R.iT * ps + R.B;
+  return l > r || (l == r && (uint32_t)id < R.idlim);
+}
 
-template <int NHI, int VPT, int KS>
+template <int NHI, int VPT, int KS, bool SMEM_CNT>
 __global__ void __launch_bounds__(TILE_T, 1) k_local_tile(TileArgs a) {
-  using SM = K8Smem<KS>;
+  using L = K8Lay<KS>;
+  constexpr int QCAP = L::QCAP, TOPS = L::TOPS, R1 = 2 * KS;
   extern __shared__ __align__(16) uint32_t dyn[];
-  uint32_t *M = dyn;  // phase A: W + 1 words, M[W] == 0.  K8: aliased by the SM regions.
-  int32_t *s_vid = reinterpret_cast<int32_t *>(dyn + SM::VID);
-  uint32_t *s_vps = dyn + SM::VPS;
-  Cand *s_tops = reinterpret_cast<Cand *>(dyn + SM::TOP);
-  Cand *s_q = reinterpret_cast<Cand *>(dyn + SM::QUE);
+  uint32_t *M = dyn;  // phase A: W + 1 words, M[W] == 0
   __shared__ int s_item;
   __shared__ int32_t s_ru[32];
   __shared__ uint32_t s_rp[32];
   __shared__ int s_qn[32];
   __shared__ Cand s_tau[32], s_T[32];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int zero_words = max(a.W + 1, SM::WORDS);
-  for (int i = tid; i < zero_words; i += TILE_T) M[i] = 0;
-  uint16_t *cnt = a.scratch + (int64_t)blockIdx.x * 32 * a.smax;  // [v][32 rows]
+  for (int i = tid; i < a.W + 1; i += TILE_T) M[i] = 0;
+  uint32_t *kb = SMEM_CNT ? dyn : a.gscratch + (int64_t)blockIdx.x * L(a.smax).words;  // K8 region
   const int nwin = a.nwin;
   const uint32_t W = (uint32_t)a.W;
   const int kk = a.k;
@@ -562,6 +586,12 @@ __global__ void __launch_bounds__(TILE_T, 1) k_local_tile(TileArgs a) {
     const int r0 = T.j * 32;
     const int nr = min(32, s - r0);
     const int32_t *vp = a.vperm + B.vp_off;
+    const L lay(s);
+    uint16_t *cnt = reinterpret_cast<uint16_t *>(kb);
+    int32_t *s_vid = reinterpret_cast<int32_t *>(kb + lay.vid);
+    uint32_t *s_vps = kb + lay.vps;
+    Cand *s_tops = reinterpret_cast<Cand *>(kb + lay.top);
+    Cand *s_q = reinterpret_cast<Cand *>(kb + lay.que);
     if (tid < 32) {
       int32_t u = tid < nr ? vp[r0 + tid] : -1;
       s_ru[tid] = u;
@@ -636,7 +666,8 @@ __global__ void __launch_bounds__(TILE_T, 1) k_local_tile(TileArgs a) {
         }
         __syncthreads();
       }
-      // ---- planes -> 32 counts per v (transpose); scratch row of v = 32 u16 (64 B)
+      // ---- planes -> 32 counts per v (transpose) -> cnt[r][v] (M is dead from here on when
+      //      SMEM_CNT: the host guarantees a single g0 group then)
 #pragma unroll
       for (int q = 0; q < VPT; ++q) {
         const int jj = g0 + q * TILE_WARPS + warp;
@@ -652,86 +683,102 @@ __global__ void __launch_bounds__(TILE_T, 1) k_local_tile(TileArgs a) {
 #pragma unroll
           for (int i = 4 + NHI; i < 32; ++i) A[i] = 0;
           transpose32(A);
-          if (vi < s) {
-            uint4 *dst = reinterpret_cast<uint4 *>(cnt + (int64_t)vi * 32);
 #pragma unroll
-            for (int j = 0; j < 4; ++j)
-              dst[j] = make_uint4(A[8 * j] | (A[8 * j + 1] << 16), A[8 * j + 2] | (A[8 * j + 3] << 16),
-                                  A[8 * j + 4] | (A[8 * j + 5] << 16), A[8 * j + 6] | (A[8 * j + 7] << 16));
-          }
+          for (int r = 0; r < 32; ++r)
+            if (r < nr) cnt[r * lay.RS + vi] = (uint16_t)A[r];
         }
+      }
+    }
+    // member ids and sizes (positions s .. s4-1: never-passing pads)
+    {
+      const int s4 = (s + 3) & ~3;
+      for (int i = tid; i < s4; i += TILE_T) {
+        int32_t v = i < s ? vp[i] : INT32_MAX;
+        s_vid[i] = v;
+        s_vps[i] = (v >= 0 && v != INT32_MAX) ? (uint32_t)a.psize[v] : 0u;
       }
     }
     __syncthreads();
     // ================= K8: exact top-k per row (lane = row, warps split the candidates)
-    const bool vstaged = s <= STAGE_V;
-    if (vstaged)
-      for (int i = tid; i < s; i += TILE_T) {
-        int32_t v = vp[i];
-        s_vid[i] = v;
-        s_vps[i] = v >= 0 ? (uint32_t)a.psize[v] : 0u;
-      }
-    __syncthreads();
     const int32_t ur = s_ru[lane];
     const uint32_t pr = s_rp[lane];
-    const Cand tau = s_tau[lane];
     const bool rowok = lane < nr && ur >= 0;
+    const int self = B.slot ? lane : r0 + lane;  // position of the row's own user
     const int slot = B.slot;  // mixed slice: candidates only inside the row's own slot group
-    auto cand_of = [&](int vi, bool &ok) -> Cand {
-      int32_t v;
-      uint32_t ps;
-      if (vstaged) {
-        v = s_vid[vi];
-        ps = s_vps[vi];
-      } else {
-        v = vp[vi];
-        ps = v >= 0 ? (uint32_t)a.psize[v] : 0u;
-      }
-      uint32_t ci = cnt[(int64_t)vi * 32 + lane];
-      ok = rowok && v >= 0 && v != ur && (slot == 0 || (vi ^ lane) < slot);
-      return Cand{ci | ((pr + ps - ci) << 16), v};
-    };
-    // round 1: each thread's best 2KS candidates above tau in its segment
-    {
-      constexpr int R = 2 * KS;
-      Cand t[R];
+    const uint16_t *crow = cnt + lane * lay.RS;
+    // round 1 only when the survivors of tau alone could overflow the queue
+    const bool round1 = s - 1 > QCAP - 4;
+    if (round1) {
+      // each thread's best R1 candidates of its interleaved share (any R1 distinct candidates
+      // of the row give a valid lower bound of the row's k-th best; the better, the tighter)
+      Cand t[R1];
 #pragma unroll
-      for (int j = 0; j < R; ++j) t[j] = sent();
-      for (int vi = warp; vi < s; vi += TILE_WARPS) {
-        bool ok;
-        Cand c = cand_of(vi, ok);
-        if (ok && better_c(c, tau) && better_c(c, t[R - 1])) {
+      for (int j = 0; j < R1; ++j) t[j] = sent();
+      Ref wr = make_ref(sent(), pr, false);
+      if (rowok) {
+        for (int v4 = warp * 4; v4 < s; v4 += TILE_WARPS * 4) {
+          const uint2 c = *reinterpret_cast<const uint2 *>(crow + v4);
+          const uint4 ps = *reinterpret_cast<const uint4 *>(s_vps + v4);
+          const int4 id = *reinterpret_cast<const int4 *>(s_vid + v4);
+          const uint32_t iv[4] = {c.x & 0xFFFFu, c.x >> 16, c.y & 0xFFFFu, c.y >> 16};
+          const uint32_t pv[4] = {ps.x, ps.y, ps.z, ps.w};
+          const int32_t dv[4] = {id.x, id.y, id.z, id.w};
 #pragma unroll
-          for (int j = R - 1; j > 0; --j) {
-            if (better_c(c, t[j - 1])) t[j] = t[j - 1];
-            else if (better_c(c, t[j])) t[j] = c;
+          for (int e = 0; e < 4; ++e) {
+            if (v4 + e != self && passes(iv[e], pv[e], dv[e], wr)) {
+              Cand x{iv[e] | ((pr + pv[e] - iv[e]) << 16), dv[e]};
+#pragma unroll
+              for (int j = R1 - 1; j > 0; --j) {
+                if (better_c(x, t[j - 1])) t[j] = t[j - 1];
+                else if (better_c(x, t[j])) t[j] = x;
+              }
+              if (better_c(x, t[0])) t[0] = x;
+              wr = make_ref(t[R1 - 1], pr, false);
+            }
           }
-          if (better_c(c, t[0])) t[0] = c;
         }
       }
 #pragma unroll
-      for (int j = 0; j < R; ++j) s_tops[lane * SM::TOPS + warp * R + j] = t[j];
-    }
-    __syncthreads();
-    // threshold T_r = k-th best of the row's tops (k distinct real candidates are >= T_r)
-    for (int r = warp; r < nr; r += TILE_WARPS) {
-      Cand e[KS];
+      for (int j = 0; j < R1; ++j) s_tops[lane * TOPS + warp * R1 + j] = t[j];
+      __syncthreads();
+      // T_r = the k-th best of the row's tops (>= k distinct real candidates are >= T_r), or
+      // tau when that is better (survivors must beat the running k-th best anyway)
+      for (int r = warp; r < nr; r += TILE_WARPS) {
+        Cand e[KS];
 #pragma unroll
-      for (int j = 0; j < KS; ++j) e[j] = s_tops[r * SM::TOPS + 32 * j + lane];
-      warp_sort<KS>(e);
-      Cand Tr = warp_get<KS>(e, kk - 1);
-      if (lane == 0) s_T[r] = Tr;
+        for (int j = 0; j < KS; ++j) e[j] = s_tops[r * TOPS + 32 * j + lane];
+        warp_sort<KS>(e);
+        Cand Tr = warp_get<KS>(e, kk - 1);
+        if (lane == 0) s_T[r] = Tr;
+      }
+      __syncthreads();
     }
-    __syncthreads();
-    // round 2: survivors (above tau and not below T_r) to the row's queue
+    // round 2: survivors (better than tau and not worse than T_r) to the row's queue
     {
-      const Cand Tr = s_T[lane];
-      for (int vi = warp; vi < s; vi += TILE_WARPS) {
-        bool ok;
-        Cand c = cand_of(vi, ok);
-        if (ok && better_c(c, tau) && !better_c(Tr, c)) {
-          int p = atomicAdd(&s_qn[lane], 1);
-          if (p < SM::QCAP) s_q[lane * SM::QCAP + p] = c;
+      const Cand tau = s_tau[lane];
+      Ref ref = make_ref(tau, pr, false);
+      if (round1) {
+        const Cand Tr = s_T[lane];
+        if (is_real(Tr) && better_c(Tr, tau)) ref = make_ref(Tr, pr, true);
+      }
+      if (rowok) {
+        for (int v4 = warp * 4; v4 < s; v4 += TILE_WARPS * 4) {
+          const uint2 c = *reinterpret_cast<const uint2 *>(crow + v4);
+          const uint4 ps = *reinterpret_cast<const uint4 *>(s_vps + v4);
+          const int4 id = *reinterpret_cast<const int4 *>(s_vid + v4);
+          const uint32_t iv[4] = {c.x & 0xFFFFu, c.x >> 16, c.y & 0xFFFFu, c.y >> 16};
+          const uint32_t pv[4] = {ps.x, ps.y, ps.z, ps.w};
+          const int32_t dv[4] = {id.x, id.y, id.z, id.w};
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const int vi = v4 + e;
+            bool ok = vi != self && passes(iv[e], pv[e], dv[e], ref);
+            if (slot) ok = ok && (vi ^ lane) < slot;
+            if (ok) {
+              int p = atomicAdd(&s_qn[lane], 1);
+              if (p < QCAP) s_q[lane * QCAP + p] = Cand{iv[e] | ((pr + pv[e] - iv[e]) << 16), dv[e]};
+            }
+          }
         }
       }
     }
@@ -744,29 +791,39 @@ __global__ void __launch_bounds__(TILE_T, 1) k_local_tile(TileArgs a) {
       const c2_cand *seed = a.seed ? a.seed + (int64_t)u * kk : nullptr;
       c2_cand *dst = a.seed ? a.out + (int64_t)u * kk : a.out + ((int64_t)B.f * a.n + u) * kk;
       Cand L[KS];  // top-k of this function's candidates above tau (sentinel padded)
-      if (nq <= SM::QCAP) {
-        Cand q[2 * KS];
+      if (nq <= QCAP) {
+        if (nq <= 32 * KS) {
+          Cand q[KS];
 #pragma unroll
-        for (int j = 0; j < 2 * KS; ++j) q[j] = (32 * j + lane < nq) ? s_q[r * SM::QCAP + 32 * j + lane] : sent();
-        warp_sort<2 * KS>(q);
+          for (int j = 0; j < KS; ++j) q[j] = (32 * j + lane < nq) ? s_q[r * QCAP + 32 * j + lane] : sent();
+          warp_sort<KS>(q);
 #pragma unroll
-        for (int j = 0; j < KS; ++j) L[j] = q[j];
+          for (int j = 0; j < KS; ++j) L[j] = q[j];
+        } else {
+          Cand q[2 * KS];
+#pragma unroll
+          for (int j = 0; j < 2 * KS; ++j) q[j] = (32 * j + lane < nq) ? s_q[r * QCAP + 32 * j + lane] : sent();
+          warp_sort<2 * KS>(q);
+#pragma unroll
+          for (int j = 0; j < KS; ++j) L[j] = q[j];
+        }
       } else {
         // rare overflow: exact insertion over all the row's candidates
 #pragma unroll
         for (int j = 0; j < KS; ++j) L[j] = sent();
         const Cand tr = s_tau[r];
         const uint32_t prr = s_rp[r];
+        const int selfr = slot ? r : r0 + r;
+        const uint16_t *cr = cnt + r * lay.RS;
         Cand thr = sent();
         for (int vb = 0; vb < s; vb += 32) {
           const int vi = vb + lane;
           Cand c = sent();
           if (vi < s) {
-            int32_t v = vstaged ? s_vid[vi] : vp[vi];
-            if (v >= 0 && v != u && (slot == 0 || (vi ^ r) < slot)) {
-              uint32_t ps = vstaged ? s_vps[vi] : (uint32_t)a.psize[v];
-              uint32_t ci = cnt[(int64_t)vi * 32 + r];
-              c = Cand{ci | ((prr + ps - ci) << 16), v};
+            int32_t v = s_vid[vi];
+            if (v >= 0 && vi != selfr && (slot == 0 || (vi ^ r) < slot)) {
+              uint32_t ci = cr[vi];
+              c = Cand{ci | ((prr + s_vps[vi] - ci) << 16), v};
             }
           }
           bool bt = is_real(c) && better_c(c, tr) && better_c(c, thr);
@@ -813,23 +870,32 @@ __global__ void __launch_bounds__(TILE_T, 1) k_local_tile(TileArgs a) {
       for (int p = base + lane; p < kk; p += 32) dst[p] = c2_cand{-1, 0, 0};
     }
     __syncthreads();
-    // restore the all-zero M region
-    for (int i = tid; i < SM::WORDS; i += TILE_T) dyn[i] = 0;
+    // restore the all-zero M words the K8 region overwrote
+    if (SMEM_CNT) {
+      const int dw = min(lay.words, a.W + 1);
+      uint4 *z = reinterpret_cast<uint4 *>(dyn);
+      for (int i = tid; i < dw / 4; i += TILE_T) z[i] = make_uint4(0, 0, 0, 0);
+      for (int i = (dw & ~3) + tid; i < dw; i += TILE_T) dyn[i] = 0;
+    }
   }
 }
 
 typedef void (*TileKernel)(TileArgs);
 
-template <int NHI, int VPT>
+template <int NHI, int VPT, bool SM>
 static TileKernel pick_ks(int k) {
-  return k <= 32 ? k_local_tile<NHI, VPT, 1> : k_local_tile<NHI, VPT, 2>;
+  return k <= 32 ? k_local_tile<NHI, VPT, 1, SM> : k_local_tile<NHI, VPT, 2, SM>;
 }
-template <int NHI>
+template <int NHI, bool SM>
 static TileKernel pick_vpt(int vpt, int k) {
-  return vpt <= 1 ? pick_ks<NHI, 1>(k) : vpt <= 2 ? pick_ks<NHI, 2>(k) : pick_ks<NHI, 4>(k);
+  return vpt <= 1 ? pick_ks<NHI, 1, SM>(k) : vpt <= 2 ? pick_ks<NHI, 2, SM>(k) : pick_ks<NHI, 4, SM>(k);
 }
-static TileKernel pick_tile(int nhi, int vpt, int k) {
-  return nhi <= 4 ? pick_vpt<4>(vpt, k) : nhi <= 8 ? pick_vpt<8>(vpt, k) : pick_vpt<11>(vpt, k);
+template <bool SM>
+static TileKernel pick_nhi(int nhi, int vpt, int k) {
+  return nhi <= 4 ? pick_vpt<4, SM>(vpt, k) : nhi <= 8 ? pick_vpt<8, SM>(vpt, k) : pick_vpt<11, SM>(vpt, k);
+}
+static TileKernel pick_tile(int nhi, int vpt, int k, bool smem_cnt) {
+  return smem_cnt ? pick_nhi<true>(nhi, vpt, k) : pick_nhi<false>(nhi, vpt, k);
 }
 
 __global__ void k_init_pads(c2_cand *__restrict__ R, int64_t E) {
@@ -990,23 +1056,31 @@ int local_knn(c2_ctx *ctx, const Csr &csr, int t, const Clusters &cl, int k, c2_
   // ---- tile kernel configuration
   TileKernel tk = nullptr;
   int grid = 0;
-  const size_t smem = (size_t)std::max<int64_t>((W + 4) & ~3, k <= 32 ? K8Smem<1>::WORDS : K8Smem<2>::WORDS) * 4;
-  uint16_t *scratch = nullptr;
+  size_t smem = 0;
+  uint32_t *gscratch = nullptr;
   int *counters = nullptr;
-  const int32_t smax = (int32_t)((std::max<uint32_t>(maxs, 32) + 31) / 32 * 32);
+  const int32_t smax = (int32_t)std::max<uint32_t>(maxs, 32);
   if (nslices > 0) {
     int nbits = bits_for((int64_t)csr.max_len + 1);
     int nhi = std::max(nbits - 4, 1);
     int max_sl = (int)((maxs + 31) / 32);
     int vpt = max_sl <= TILE_WARPS ? 1 : max_sl <= 2 * TILE_WARPS ? 2 : 4;
-    tk = pick_tile(nhi, vpt, k);
+    const int k8w = k <= 32 ? K8Lay<1>(smax).words : K8Lay<2>(smax).words;
+    const size_t mw = (size_t)((W + 4) & ~3);
+    // counts in shared memory (aliased onto M) when one g0 group covers the largest cluster
+    // and the K8 region fits; else a per-CTA global scratch region
+    const bool smem_cnt = max_sl <= 4 * TILE_WARPS && (size_t)k8w * 4 <= ctx->smem_optin;
+    smem = (smem_cnt ? std::max(mw, (size_t)k8w) : mw) * 4;
+    tk = pick_tile(nhi, vpt, k, smem_cnt);
     C2_CUDA(ctx, cudaFuncSetAttribute(tk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int occ = 0;
     C2_CUDA(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, tk, TILE_T, smem));
     occ = std::max(occ, 1);
     grid = (int)std::min<int64_t>((int64_t)ctx->num_sms * occ, nslices);
-    scratch = (uint16_t *)ws_get(ctx, "tile_scratch", (size_t)grid * 32 * smax * 2, &rc);
-    if (rc) return rc;
+    if (!smem_cnt) {
+      gscratch = (uint32_t *)ws_get(ctx, "tile_scratch", (size_t)grid * k8w * 4, &rc);
+      if (rc) return rc;
+    }
     counters = (int *)ws_get(ctx, "tile_counter", 4 * (2 * C2_MAX_T + 2), &rc);
     if (rc) return rc;
     C2_CUDA(ctx, cudaMemsetAsync(counters, 0, 4 * (2 * C2_MAX_T + 2), st));
@@ -1014,7 +1088,7 @@ int local_knn(c2_ctx *ctx, const Csr &csr, int t, const Clusters &cl, int k, c2_
   auto launch_tiles = [&](int64_t lo, int64_t hi, int ci, const c2_cand *seed, c2_cand *dst) -> int {
     if (hi <= lo) return C2_OK;
     TileArgs ta{tiles, lo, hi, counters + ci, bcs, vperm, blk_len8, blk_off8, packed, csr.psize, n, W, nwin, k,
-                seed, dst, scratch, smax};
+                seed, dst, gscratch, smax};
     int g = (int)std::min<int64_t>(grid, hi - lo);
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     if (ctx->timing) {
