@@ -86,7 +86,7 @@ int build_device(c2_ctx *ctx, const int32_t *offs, const int32_t *items, int32_t
   int rc;
   // Steps 2+3 fused: function by function, every local neighbourhood is merged into the
   // running Alg. 3 result; the final lists equal merge(local lists) exactly.
-  c2_cand *run = (c2_cand *)ws_get(ctx, "runlist", (size_t)2 * n * k * sizeof(c2_cand), &rc);
+  c2_cand *run = (c2_cand *)ws_get(ctx, "runlist", (size_t)n * k * sizeof(c2_cand), &rc);
   if (rc) return rc;
   c2_cand *fin = nullptr;
   C2_TRY(local_knn(ctx, sims, t, cl, k, run, true, &fin));

@@ -329,9 +329,47 @@ __device__ __forceinline__ Cand from_out(c2_cand e) {
   return e.id >= 0 ? Cand{(uint32_t)e.inter | ((uint32_t)e.uni << 16), e.id} : sent();
 }
 
+// Sort key of a candidate: K = q32 << 32 | (2^32 - 1 - id), larger = better, where
+// q32 = floor(i/U * 2^32) (U >= 1; 2^32 - 1 for i == U) from the IEEE (correctly rounded) f64
+// quotient.  K orders candidates exactly as the fraction comparison (A13): equal fractions
+// give identical quotients; distinct fractions with U <= 65534 differ by >= 1/65534^2, i.e. by
+// >= 1.00006 after scaling by 2^32, far above the f64 rounding error (< 2^-20), so their
+// floors differ.  The payload iu = i | U << 16 rides along.  Sentinel: K = 0.
+struct KC {
+  uint64_t k;
+  uint32_t iu;
+};
+__device__ __forceinline__ KC to_kc(Cand c) {
+  if (!is_real(c)) return KC{0ull, 1u << 16};
+  const uint32_t i = c.iu & 0xFFFFu, U = c.iu >> 16;
+  const double q = (double)i / (double)U;
+  const uint32_t q32 = i >= U ? 0xFFFFFFFFu : (uint32_t)(q * 4294967296.0);
+  return KC{((uint64_t)q32 << 32) | (uint64_t)(0xFFFFFFFFu - (uint32_t)c.id), c.iu};
+}
+__device__ __forceinline__ int32_t kc_id(KC a) { return (int32_t)(0xFFFFFFFFu - (uint32_t)a.k); }
+__device__ __forceinline__ bool kc_real(KC a) { return a.k != 0ull; }
+__device__ __forceinline__ Cand kc_cand(KC a) { return kc_real(a) ? Cand{a.iu, kc_id(a)} : sent(); }
+__device__ __forceinline__ c2_cand kc_out(KC a) {
+  return kc_real(a) ? c2_cand{kc_id(a), (uint16_t)(a.iu & 0xFFFFu), (uint16_t)(a.iu >> 16)} : c2_cand{-1, 0, 0};
+}
+__device__ __forceinline__ bool better_e(KC a, KC b) { return a.k > b.k; }
+__device__ __forceinline__ bool better_e(Cand a, Cand b) { return better_c(a, b); }
+__device__ __forceinline__ KC shfl_e(KC a, int src) {
+  return KC{__shfl_sync(0xffffffffu, a.k, src), __shfl_sync(0xffffffffu, a.iu, src)};
+}
+__device__ __forceinline__ KC shfl_xor_e(KC a, int m) {
+  return KC{__shfl_xor_sync(0xffffffffu, a.k, m), __shfl_xor_sync(0xffffffffu, a.iu, m)};
+}
+__device__ __forceinline__ KC shfl_up_e(KC a) {
+  return KC{__shfl_up_sync(0xffffffffu, a.k, 1), __shfl_up_sync(0xffffffffu, a.iu, 1)};
+}
+__device__ __forceinline__ Cand shfl_e(Cand a, int src) { return shfl_c(a, src); }
+__device__ __forceinline__ Cand shfl_xor_e(Cand a, int m) { return shfl_xor_c(a, m); }
+__device__ __forceinline__ Cand shfl_up_e(Cand a) { return shfl_up_c(a); }
+
 // Bitonic sort of the 32R warp-held elements a[j] (position 32j + lane), best first.
-template <int R>
-__device__ __forceinline__ void warp_sort(Cand (&a)[R]) {
+template <int R, class E>
+__device__ __forceinline__ void warp_sort(E (&a)[R]) {
   const int lane = threadIdx.x & 31;
 #pragma unroll
   for (int size = 2; size <= 32 * R; size <<= 1) {
@@ -344,8 +382,8 @@ __device__ __forceinline__ void warp_sort(Cand (&a)[R]) {
           if ((j & js) == 0) {
             const int p = 32 * j + lane;
             const bool desc = (p & size) == 0;  // lower position takes the better element
-            Cand x = a[j], y = a[j + js];
-            if (desc ? better_c(y, x) : better_c(x, y)) {
+            E x = a[j], y = a[j + js];
+            if (desc ? better_e(y, x) : better_e(x, y)) {
               a[j] = y;
               a[j + js] = x;
             }
@@ -355,12 +393,11 @@ __device__ __forceinline__ void warp_sort(Cand (&a)[R]) {
 #pragma unroll
         for (int j = 0; j < R; ++j) {
           const int p = 32 * j + lane;
-          Cand o = shfl_xor_c(a[j], stride);
+          E o = shfl_xor_e(a[j], stride);
           const bool lower = (lane & stride) == 0;
           const bool desc = (p & size) == 0;
-          const bool ob = better_c(o, a[j]);
           // lower position of a descending block keeps the better one
-          if ((lower == desc) ? ob : better_c(a[j], o)) a[j] = o;
+          if ((lower == desc) ? better_e(o, a[j]) : better_e(a[j], o)) a[j] = o;
         }
       }
     }
@@ -368,8 +405,8 @@ __device__ __forceinline__ void warp_sort(Cand (&a)[R]) {
 }
 
 // Bitonic merge of a bitonic sequence of 32R warp-held elements into best-first order.
-template <int R>
-__device__ __forceinline__ void warp_bitonic_merge(Cand (&a)[R]) {
+template <int R, class E>
+__device__ __forceinline__ void warp_bitonic_merge(E (&a)[R]) {
   const int lane = threadIdx.x & 31;
 #pragma unroll
   for (int stride = 16 * R; stride > 0; stride >>= 1) {
@@ -377,35 +414,35 @@ __device__ __forceinline__ void warp_bitonic_merge(Cand (&a)[R]) {
       const int js = stride >> 5;
 #pragma unroll
       for (int j = 0; j < R; ++j)
-        if ((j & js) == 0 && better_c(a[j + js], a[j])) {
-          Cand x = a[j];
+        if ((j & js) == 0 && better_e(a[j + js], a[j])) {
+          E x = a[j];
           a[j] = a[j + js];
           a[j + js] = x;
         }
     } else {
 #pragma unroll
       for (int j = 0; j < R; ++j) {
-        Cand o = shfl_xor_c(a[j], stride);
+        E o = shfl_xor_e(a[j], stride);
         const bool lower = (lane & stride) == 0;
-        if (lower ? better_c(o, a[j]) : better_c(a[j], o)) a[j] = o;
+        if (lower ? better_e(o, a[j]) : better_e(a[j], o)) a[j] = o;
       }
     }
   }
 }
 
 // Insert x into the sorted warp list a (32R positions, best first); the worst drops out.
-template <int R>
-__device__ __forceinline__ void warp_insert(Cand (&a)[R], Cand x) {
+template <int R, class E>
+__device__ __forceinline__ void warp_insert(E (&a)[R], E x) {
   const int lane = threadIdx.x & 31;
   int pos = 0;
 #pragma unroll
-  for (int j = 0; j < R; ++j) pos += __popc(__ballot_sync(0xffffffffu, better_c(a[j], x)));
-  Cand up[R];
+  for (int j = 0; j < R; ++j) pos += __popc(__ballot_sync(0xffffffffu, better_e(a[j], x)));
+  E up[R];
 #pragma unroll
-  for (int j = 0; j < R; ++j) up[j] = shfl_up_c(a[j]);
+  for (int j = 0; j < R; ++j) up[j] = shfl_up_e(a[j]);
 #pragma unroll
   for (int j = 1; j < R; ++j) {
-    Cand last = shfl_c(a[j - 1], 31);
+    E last = shfl_e(a[j - 1], 31);
     if (lane == 0) up[j] = last;
   }
 #pragma unroll
@@ -416,13 +453,13 @@ __device__ __forceinline__ void warp_insert(Cand (&a)[R], Cand x) {
   }
 }
 
-template <int R>
-__device__ __forceinline__ Cand warp_get(const Cand (&a)[R], int p) {
-  Cand r = a[0];
+template <int R, class E>
+__device__ __forceinline__ E warp_get(const E (&a)[R], int p) {
+  E r = a[0];
 #pragma unroll
   for (int j = 1; j < R; ++j)
     if ((p >> 5) == j) r = a[j];
-  return shfl_c(r, p & 31);
+  return shfl_e(r, p & 31);
 }
 
 // ------------------------------------------------------------------ K7 tile kernel
@@ -744,12 +781,12 @@ __global__ void __launch_bounds__(TILE_T, 1) k_local_tile(TileArgs a) {
       // T_r = the k-th best of the row's tops (>= k distinct real candidates are >= T_r), or
       // tau when that is better (survivors must beat the running k-th best anyway)
       for (int r = warp; r < nr; r += TILE_WARPS) {
-        Cand e[KS];
+        KC e[KS];
 #pragma unroll
-        for (int j = 0; j < KS; ++j) e[j] = s_tops[r * TOPS + 32 * j + lane];
+        for (int j = 0; j < KS; ++j) e[j] = to_kc(s_tops[r * TOPS + 32 * j + lane]);
         warp_sort<KS>(e);
-        Cand Tr = warp_get<KS>(e, kk - 1);
-        if (lane == 0) s_T[r] = Tr;
+        KC Tr = warp_get<KS>(e, kk - 1);
+        if (lane == 0) s_T[r] = kc_cand(Tr);
       }
       __syncthreads();
     }
@@ -783,34 +820,38 @@ __global__ void __launch_bounds__(TILE_T, 1) k_local_tile(TileArgs a) {
       }
     }
     __syncthreads();
-    // final: per row (warp per row) sort the survivors, merge with the seed, write k
+    // final: per row (warp per row) sort the survivors, merge with the seed, write k.  Fused
+    // mode updates the running list in place (each user is in one cluster per function), so a
+    // row without survivors keeps its list untouched.
     for (int r = warp; r < nr; r += TILE_WARPS) {
       const int32_t u = s_ru[r];
       if (u < 0) continue;
       const int nq = s_qn[r];
-      const c2_cand *seed = a.seed ? a.seed + (int64_t)u * kk : nullptr;
+      if (a.seed && nq == 0) continue;
       c2_cand *dst = a.seed ? a.out + (int64_t)u * kk : a.out + ((int64_t)B.f * a.n + u) * kk;
-      Cand L[KS];  // top-k of this function's candidates above tau (sentinel padded)
+      KC L[KS];  // top-k of this function's candidates above tau (sentinel padded)
       if (nq <= QCAP) {
         if (nq <= 32 * KS) {
-          Cand q[KS];
+          KC q[KS];
 #pragma unroll
-          for (int j = 0; j < KS; ++j) q[j] = (32 * j + lane < nq) ? s_q[r * QCAP + 32 * j + lane] : sent();
+          for (int j = 0; j < KS; ++j) q[j] = to_kc((32 * j + lane < nq) ? s_q[r * QCAP + 32 * j + lane] : sent());
           warp_sort<KS>(q);
 #pragma unroll
           for (int j = 0; j < KS; ++j) L[j] = q[j];
         } else {
-          Cand q[2 * KS];
+          KC q[2 * KS];
 #pragma unroll
-          for (int j = 0; j < 2 * KS; ++j) q[j] = (32 * j + lane < nq) ? s_q[r * QCAP + 32 * j + lane] : sent();
+          for (int j = 0; j < 2 * KS; ++j)
+            q[j] = to_kc((32 * j + lane < nq) ? s_q[r * QCAP + 32 * j + lane] : sent());
           warp_sort<2 * KS>(q);
 #pragma unroll
           for (int j = 0; j < KS; ++j) L[j] = q[j];
         }
       } else {
         // rare overflow: exact insertion over all the row's candidates
+        Cand Lc[KS];
 #pragma unroll
-        for (int j = 0; j < KS; ++j) L[j] = sent();
+        for (int j = 0; j < KS; ++j) Lc[j] = sent();
         const Cand tr = s_tau[r];
         const uint32_t prr = s_rp[r];
         const int selfr = slot ? r : r0 + r;
@@ -833,38 +874,41 @@ __global__ void __launch_bounds__(TILE_T, 1) k_local_tile(TileArgs a) {
             mask &= mask - 1;
             Cand x = shfl_c(c, l);
             if (!better_c(x, thr)) continue;
-            warp_insert<KS>(L, x);
-            thr = warp_get<KS>(L, kk - 1);
+            warp_insert<KS>(Lc, x);
+            thr = warp_get<KS>(Lc, kk - 1);
           }
         }
+#pragma unroll
+        for (int j = 0; j < KS; ++j) L[j] = to_kc(Lc[j]);
       }
-      if (!seed) {
+      if (!a.seed) {
 #pragma unroll
         for (int j = 0; j < KS; ++j)
-          if (32 * j + lane < kk) dst[32 * j + lane] = to_out(L[j]);
+          if (32 * j + lane < kk) dst[32 * j + lane] = kc_out(L[j]);
         continue;
       }
-      // merge with the seed S (best first): bitonic sequence L(first k) ++ reverse(S)
-      Cand S[KS];
+      // merge with the running list S (best first): bitonic sequence L(first k) ++ reverse(S)
+      KC S[KS];
 #pragma unroll
-      for (int j = 0; j < KS; ++j) S[j] = (32 * j + lane < kk) ? from_out(seed[32 * j + lane]) : sent();
-      Cand m[2 * KS];
+      for (int j = 0; j < KS; ++j) S[j] = to_kc((32 * j + lane < kk) ? from_out(dst[32 * j + lane]) : sent());
+      KC m[2 * KS];
 #pragma unroll
-      for (int j = 0; j < KS; ++j) m[j] = (32 * j + lane < kk) ? L[j] : sent();
+      for (int j = 0; j < KS; ++j) m[j] = (32 * j + lane < kk) ? L[j] : KC{0ull, 1u << 16};
 #pragma unroll
-      for (int j = 0; j < KS; ++j) m[KS + j] = shfl_c(S[KS - 1 - j], 31 - lane);
+      for (int j = 0; j < KS; ++j) m[KS + j] = shfl_e(S[KS - 1 - j], 31 - lane);
       warp_bitonic_merge<2 * KS>(m);
       // drop adjacent duplicates (a repeated id carries identical values, A16); keep k
       int base = 0;
 #pragma unroll
       for (int j = 0; j < 2 * KS; ++j) {
-        int32_t prev = __shfl_up_sync(0xffffffffu, m[j].id, 1);
-        int32_t prevj = j > 0 ? __shfl_sync(0xffffffffu, m[j - 1].id, 31) : -2;
+        const uint32_t lo = (uint32_t)m[j].k;
+        uint32_t prev = __shfl_up_sync(0xffffffffu, lo, 1);
+        uint32_t prevj = j > 0 ? __shfl_sync(0xffffffffu, (uint32_t)m[j - 1].k, 31) : 0u;
         if (lane == 0) prev = prevj;
-        bool keep = is_real(m[j]) && m[j].id != prev;
+        bool keep = kc_real(m[j]) && (j + lane == 0 || lo != prev);
         unsigned bal = __ballot_sync(0xffffffffu, keep);
         int rank = base + __popc(bal & ((1u << lane) - 1));
-        if (keep && rank < kk) dst[rank] = to_out(m[j]);
+        if (keep && rank < kk) dst[rank] = kc_out(m[j]);
         base += __popc(bal);
       }
       for (int p = base + lane; p < kk; p += 32) dst[p] = c2_cand{-1, 0, 0};
@@ -978,9 +1022,8 @@ int local_knn(c2_ctx *ctx, const Csr &csr, int t, const Clusters &cl, int k, c2_
   }
   mix_lo[t] = nmix;
 
-  c2_cand *R[2] = {out, out + (int64_t)n * k};
   if (fused) {
-    k_init_pads<<<nblk((int64_t)n * k), 256, 0, st>>>(R[0], (int64_t)n * k);
+    k_init_pads<<<nblk((int64_t)n * k), 256, 0, st>>>(out, (int64_t)n * k);
     C2_LAUNCHED(ctx, "k_init_pads");
   }
 
@@ -1120,20 +1163,16 @@ int local_knn(c2_ctx *ctx, const Csr &csr, int t, const Clusters &cl, int k, c2_
     C2_TRY(launch_singles(0, nsingle, nullptr, out));
     if (result) *result = out;
   } else {
-    // Alg. 3 order: function by function, every user's running list (R[cur]) is merged with
-    // its neighbourhood in that function's cluster into R[cur ^ 1]
-    int64_t blo = 0, slo = 0;
-    int cur = 0;
+    // Alg. 3 order: function by function, every user's running list is merged in place with
+    // its neighbourhood in that function's cluster (singletons: nothing to merge)
+    int64_t blo = 0;
     for (int f = 0; f < t; ++f) {
-      int64_t bhi = blo + hfc[f * 8 + 0], shi = slo + hfc[f * 8 + 6];
-      C2_TRY(launch_tiles(blo, bhi, 2 * f, R[cur], R[cur ^ 1]));
-      C2_TRY(launch_tiles(nbigtiles + mix_lo[f], nbigtiles + mix_lo[f + 1], 2 * f + 1, R[cur], R[cur ^ 1]));
-      C2_TRY(launch_singles(slo, shi, R[cur], R[cur ^ 1]));
+      int64_t bhi = blo + hfc[f * 8 + 0];
+      C2_TRY(launch_tiles(blo, bhi, 2 * f, out, out));
+      C2_TRY(launch_tiles(nbigtiles + mix_lo[f], nbigtiles + mix_lo[f + 1], 2 * f + 1, out, out));
       blo = bhi;
-      slo = shi;
-      cur ^= 1;
     }
-    if (result) *result = R[cur];
+    if (result) *result = out;
   }
   return C2_OK;
 }
