@@ -87,7 +87,9 @@ enum {
   C2_OPT_SKETCH_DEPTH = 1, /* 1..8: sketch values kept per (function,user); deeper split
                               levels recompute from the CSR (A29).  Default 8. */
   C2_OPT_SYNC_CHECK = 2,   /* nonzero: synchronise + check errors after every launch */
-  C2_OPT_TIMING = 3        /* nonzero: record per-phase CUDA-event times into c2_stats */
+  C2_OPT_TIMING = 3,       /* nonzero: record per-phase CUDA-event times into c2_stats */
+  C2_OPT_KSTATS = 4        /* diagnostics: value = address of a dev uint64[16] the local kernel adds
+                              counters to (rows, survivors, sort sizes, overflows; 0 = off) */
 };
 C2_API int c2_ctx_set_option(c2_ctx *ctx, int key, int64_t value);
 

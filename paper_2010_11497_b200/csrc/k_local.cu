@@ -493,12 +493,12 @@ __device__ __forceinline__ void transpose32(uint32_t (&A)[32]) {
 //                            bank-conflict free
 //   vid  [s4] int32          member ids (positions >= s: INT32_MAX)
 //   vps  [s4] uint32         member |P_v| (positions >= s: 0)
-//   top  [32][32*KS] Cand    round-1 survivors per row (each thread's best 2*KS)
+//   top  [32][64*KS] Cand    round-1 survivors per row (each thread's best 4*KS)
 //   que  [32][64*KS] Cand    round-2 survivors per row
 template <int KS>
 struct K8Lay {
   static constexpr int QCAP = 64 * KS;
-  static constexpr int TOPS = 32 * KS;
+  static constexpr int TOPS = 64 * KS;
   int RS, vid, vps, top, que, words;
   __host__ __device__ __forceinline__ explicit K8Lay(int s) {
     RS = ((s + 63) / 64) * 64 + 4;
@@ -526,6 +526,7 @@ struct TileArgs {
   int k;
   const c2_cand *seed;  // fused: running lists before this function [n][k]; else nullptr
   c2_cand *out;         // local: cand [t][n][k]; fused: running lists after this function
+  unsigned long long *kstats;  // C2_OPT_KSTATS counters or nullptr
   uint32_t *gscratch;   // !SMEM_CNT only: per CTA K8Lay<KS>(smax).words words
   int32_t smax;
 };
@@ -596,7 +597,7 @@ __device__ __forceinline__ bool passes(uint32_t i, uint32_t ps, int32_t id, cons
 template <int NHI, int VPT, int KS, bool SMEM_CNT>
 __global__ void __launch_bounds__(TILE_T, 1) k_local_tile(TileArgs a) {
   using L = K8Lay<KS>;
-  constexpr int QCAP = L::QCAP, TOPS = L::TOPS, R1 = 2 * KS;
+  constexpr int QCAP = L::QCAP, TOPS = L::TOPS, R1 = 4 * KS;
   extern __shared__ __align__(16) uint32_t dyn[];
   uint32_t *M = dyn;  // phase A: W + 1 words, M[W] == 0
   __shared__ int s_item;
@@ -743,10 +744,14 @@ __global__ void __launch_bounds__(TILE_T, 1) k_local_tile(TileArgs a) {
     const int self = B.slot ? lane : r0 + lane;  // position of the row's own user
     const int slot = B.slot;  // mixed slice: candidates only inside the row's own slot group
     const uint16_t *crow = cnt + lane * lay.RS;
-    // round 1 only when the survivors of tau alone could overflow the queue
-    const bool round1 = s - 1 > QCAP - 4;
+    // Round 1 bounds each row's k-th best from below; it is needed only when the survivors of
+    // tau alone could overflow the queue: clusters larger than the queue whose rows do not all
+    // hold a full running list yet (first function).  Rows that still overflow are rescanned
+    // with a bound taken from their own queue (rescan_row).
+    const bool tau_all = __all_sync(0xffffffffu, !rowok || is_real(s_tau[lane]));
+    const bool round1 = s - 1 > QCAP - 4 && !tau_all;
     if (round1) {
-      // each thread's best R1 candidates of its interleaved share (any R1 distinct candidates
+      // each thread's best R1 candidates of its interleaved share (any k distinct candidates
       // of the row give a valid lower bound of the row's k-th best; the better, the tighter)
       Cand t[R1];
 #pragma unroll
@@ -778,14 +783,13 @@ __global__ void __launch_bounds__(TILE_T, 1) k_local_tile(TileArgs a) {
 #pragma unroll
       for (int j = 0; j < R1; ++j) s_tops[lane * TOPS + warp * R1 + j] = t[j];
       __syncthreads();
-      // T_r = the k-th best of the row's tops (>= k distinct real candidates are >= T_r), or
-      // tau when that is better (survivors must beat the running k-th best anyway)
+      // T_r = the k-th best of the row's tops (>= k distinct real candidates are >= T_r)
       for (int r = warp; r < nr; r += TILE_WARPS) {
-        KC e[KS];
+        KC e[TOPS / 32];
 #pragma unroll
-        for (int j = 0; j < KS; ++j) e[j] = to_kc(s_tops[r * TOPS + 32 * j + lane]);
-        warp_sort<KS>(e);
-        KC Tr = warp_get<KS>(e, kk - 1);
+        for (int j = 0; j < TOPS / 32; ++j) e[j] = to_kc(s_tops[r * TOPS + 32 * j + lane]);
+        warp_sort<TOPS / 32>(e);
+        KC Tr = warp_get<TOPS / 32>(e, kk - 1);
         if (lane == 0) s_T[r] = kc_cand(Tr);
       }
       __syncthreads();
@@ -820,35 +824,86 @@ __global__ void __launch_bounds__(TILE_T, 1) k_local_tile(TileArgs a) {
       }
     }
     __syncthreads();
-    // final: per row (warp per row) sort the survivors, merge with the seed, write k.  Fused
-    // mode updates the running list in place (each user is in one cluster per function), so a
-    // row without survivors keeps its list untouched.
+    // final: per row (warp per row) sort the survivors, merge with the running list, write k.
+    // Fused mode updates the running list in place (each user is in one cluster per function),
+    // so a row without survivors keeps its list untouched.
     for (int r = warp; r < nr; r += TILE_WARPS) {
       const int32_t u = s_ru[r];
       if (u < 0) continue;
-      const int nq = s_qn[r];
+      int nq = s_qn[r];
+      if (a.kstats && lane == 0) {
+        atomicAdd(&a.kstats[0], 1ull);
+        atomicAdd(&a.kstats[1], nq == 0 ? 1ull : 0ull);
+        atomicAdd(&a.kstats[2], (unsigned long long)nq);
+        atomicAdd(&a.kstats[3], nq > 32 * KS ? 1ull : 0ull);
+        atomicAdd(&a.kstats[4], nq > QCAP ? 1ull : 0ull);
+        if (r == 0) {
+          atomicAdd(&a.kstats[5], 1ull);
+          atomicAdd(&a.kstats[6], round1 ? 1ull : 0ull);
+          atomicAdd(&a.kstats[7], (unsigned long long)s);
+        }
+      }
       if (a.seed && nq == 0) continue;
       c2_cand *dst = a.seed ? a.out + (int64_t)u * kk : a.out + ((int64_t)B.f * a.n + u) * kk;
+      Cand *qr = s_q + r * QCAP;
+      // overflow: the queue holds QCAP distinct survivors; their k-th best bounds the row's
+      // k-th best from below, so rescanning the row (one warp) with it keeps every candidate of
+      // the top k and, short of massive ties, fits the queue.  A single group (big slices only:
+      // mixed slices have at most 31 candidates per row).
+      for (int pass = 0; pass < 2 && nq > QCAP; ++pass) {
+        KC e[2 * KS];
+#pragma unroll
+        for (int j = 0; j < 2 * KS; ++j) e[j] = to_kc(qr[32 * j + lane]);
+        warp_sort<2 * KS>(e);
+        const Ref T2 = make_ref(kc_cand(warp_get<2 * KS>(e, kk - 1)), s_rp[r], true);
+        __syncwarp();
+        const uint16_t *cr = cnt + r * lay.RS;
+        const int selfr = r0 + r;
+        const uint32_t prr = s_rp[r];
+        int m = 0;
+        for (int v4 = lane * 4; v4 - lane * 4 < s; v4 += 128) {
+          uint32_t iv[4] = {0, 0, 0, 0}, pv[4] = {0, 0, 0, 0};
+          int32_t dv[4] = {INT32_MAX, INT32_MAX, INT32_MAX, INT32_MAX};
+          if (v4 < s) {
+            const uint2 c = *reinterpret_cast<const uint2 *>(cr + v4);
+            const uint4 ps = *reinterpret_cast<const uint4 *>(s_vps + v4);
+            const int4 id = *reinterpret_cast<const int4 *>(s_vid + v4);
+            iv[0] = c.x & 0xFFFFu, iv[1] = c.x >> 16, iv[2] = c.y & 0xFFFFu, iv[3] = c.y >> 16;
+            pv[0] = ps.x, pv[1] = ps.y, pv[2] = ps.z, pv[3] = ps.w;
+            dv[0] = id.x, dv[1] = id.y, dv[2] = id.z, dv[3] = id.w;
+          }
+#pragma unroll
+          for (int e2 = 0; e2 < 4; ++e2) {
+            const bool ok = v4 + e2 != selfr && passes(iv[e2], pv[e2], dv[e2], T2);
+            const unsigned bal = __ballot_sync(0xffffffffu, ok);
+            const int p = m + __popc(bal & ((1u << lane) - 1));
+            if (ok && p < QCAP) qr[p] = Cand{iv[e2] | ((prr + pv[e2] - iv[e2]) << 16), dv[e2]};
+            m += __popc(bal);
+          }
+        }
+        __syncwarp();
+        nq = m;
+      }
       KC L[KS];  // top-k of this function's candidates above tau (sentinel padded)
       if (nq <= QCAP) {
         if (nq <= 32 * KS) {
           KC q[KS];
 #pragma unroll
-          for (int j = 0; j < KS; ++j) q[j] = to_kc((32 * j + lane < nq) ? s_q[r * QCAP + 32 * j + lane] : sent());
+          for (int j = 0; j < KS; ++j) q[j] = to_kc((32 * j + lane < nq) ? qr[32 * j + lane] : sent());
           warp_sort<KS>(q);
 #pragma unroll
           for (int j = 0; j < KS; ++j) L[j] = q[j];
         } else {
           KC q[2 * KS];
 #pragma unroll
-          for (int j = 0; j < 2 * KS; ++j)
-            q[j] = to_kc((32 * j + lane < nq) ? s_q[r * QCAP + 32 * j + lane] : sent());
+          for (int j = 0; j < 2 * KS; ++j) q[j] = to_kc((32 * j + lane < nq) ? qr[32 * j + lane] : sent());
           warp_sort<2 * KS>(q);
 #pragma unroll
           for (int j = 0; j < KS; ++j) L[j] = q[j];
         }
       } else {
-        // rare overflow: exact insertion over all the row's candidates
+        // pathological ties: exact insertion over all the row's candidates
+        if (a.kstats && lane == 0) atomicAdd(&a.kstats[8], 1ull);
         Cand Lc[KS];
 #pragma unroll
         for (int j = 0; j < KS; ++j) Lc[j] = sent();
@@ -1131,7 +1186,7 @@ int local_knn(c2_ctx *ctx, const Csr &csr, int t, const Clusters &cl, int k, c2_
   auto launch_tiles = [&](int64_t lo, int64_t hi, int ci, const c2_cand *seed, c2_cand *dst) -> int {
     if (hi <= lo) return C2_OK;
     TileArgs ta{tiles, lo, hi, counters + ci, bcs, vperm, blk_len8, blk_off8, packed, csr.psize, n, W, nwin, k,
-                seed, dst, gscratch, smax};
+                seed, dst, ctx->kstats, gscratch, smax};
     int g = (int)std::min<int64_t>(grid, hi - lo);
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     if (ctx->timing) {

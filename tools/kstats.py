@@ -1,0 +1,20 @@
+"""K7/K8 diagnostic counters per function (C2_OPT_KSTATS) on one config (dev tool)."""
+import os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+import synth
+import paper_2010_11497_b200 as c2
+
+name = sys.argv[1] if len(sys.argv) > 1 else "c4"
+C = synth.config(name)
+offs, items = synth.generate(name)
+d_o, d_i = torch.from_numpy(offs).cuda(), torch.from_numpy(items).cuda()
+ctx = c2.Context(0)
+ks = torch.zeros(16, dtype=torch.int64, device="cuda")
+c2.build(d_o, d_i, k=C.k, t=C.t, b=C.b, N=C.N, seed=C.hash_seed, ctx=ctx)
+ctx.set_option(c2.OPT_KSTATS, ks.data_ptr())
+c2.build(d_o, d_i, k=C.k, t=C.t, b=C.b, N=C.N, seed=C.hash_seed, ctx=ctx)
+torch.cuda.synchronize()
+k = ks.tolist()
+print(f"{name}: rows {k[0]} nq==0 {k[1]/k[0]:.3f} mean nq {k[2]/k[0]:.2f} nq>32KS {k[3]/k[0]:.4f} overflow {k[4]/k[0]:.5f} "
+      f"tiles {k[5]} round1 tiles {k[6]} mean s {k[7]/max(k[5],1):.1f}")
