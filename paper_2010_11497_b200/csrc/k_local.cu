@@ -493,21 +493,16 @@ __device__ __forceinline__ void transpose32(uint32_t (&A)[32]) {
 //                            bank-conflict free
 //   vid  [s4] int32          member ids (positions >= s: INT32_MAX)
 //   vps  [s4] uint32         member |P_v| (positions >= s: 0)
-//   top  [32][64*KS] Cand    round-1 survivors per row (each thread's best 4*KS)
-//   que  [32][64*KS] Cand    round-2 survivors per row
-template <int KS>
+//   que  [32][qcap] Cand     survivors per row (qcap >= 64*KS, as large as shared memory allows)
 struct K8Lay {
-  static constexpr int QCAP = 64 * KS;
-  static constexpr int TOPS = 64 * KS;
-  int RS, vid, vps, top, que, words;
-  __host__ __device__ __forceinline__ explicit K8Lay(int s) {
+  int RS, vid, vps, que, words;
+  __host__ __device__ __forceinline__ K8Lay(int s, int qcap) {
     RS = ((s + 63) / 64) * 64 + 4;
     const int s4 = (s + 3) & ~3;
     vid = 16 * RS;
     vps = vid + s4;
-    top = vps + s4;
-    que = top + 32 * TOPS * 2;
-    words = que + 32 * QCAP * 2;
+    que = vps + s4;
+    words = que + 32 * qcap * 2;
   }
 };
 
@@ -527,8 +522,9 @@ struct TileArgs {
   const c2_cand *seed;  // fused: running lists before this function [n][k]; else nullptr
   c2_cand *out;         // local: cand [t][n][k]; fused: running lists after this function
   unsigned long long *kstats;  // C2_OPT_KSTATS counters or nullptr
-  uint32_t *gscratch;   // !SMEM_CNT only: per CTA K8Lay<KS>(smax).words words
+  uint32_t *gscratch;   // !SMEM_CNT only: per CTA K8Lay(smax, qcap).words words
   int32_t smax;
+  int32_t qcap;         // survivor queue capacity per row
 };
 
 // 8 masks of one uint4 of packed u16 item ids
@@ -596,18 +592,17 @@ __device__ __forceinline__ bool passes(uint32_t i, uint32_t ps, int32_t id, cons
 
 template <int NHI, int VPT, int KS, bool SMEM_CNT>
 __global__ void __launch_bounds__(TILE_T, 1) k_local_tile(TileArgs a) {
-  using L = K8Lay<KS>;
-  constexpr int QCAP = L::QCAP, TOPS = L::TOPS, R1 = 4 * KS;
+  constexpr int R1 = 2 * KS;
+  const int qcap = a.qcap;
   extern __shared__ __align__(16) uint32_t dyn[];
   uint32_t *M = dyn;  // phase A: W + 1 words, M[W] == 0
   __shared__ int s_item;
   __shared__ int32_t s_ru[32];
   __shared__ uint32_t s_rp[32];
-  __shared__ int s_qn[32];
-  __shared__ Cand s_tau[32], s_T[32];
+  __shared__ Cand s_tau[32];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   for (int i = tid; i < a.W + 1; i += TILE_T) M[i] = 0;
-  uint32_t *kb = SMEM_CNT ? dyn : a.gscratch + (int64_t)blockIdx.x * L(a.smax).words;  // K8 region
+  uint32_t *kb = SMEM_CNT ? dyn : a.gscratch + (int64_t)blockIdx.x * K8Lay(a.smax, qcap).words;  // K8 region
   const int nwin = a.nwin;
   const uint32_t W = (uint32_t)a.W;
   const int kk = a.k;
@@ -624,17 +619,15 @@ __global__ void __launch_bounds__(TILE_T, 1) k_local_tile(TileArgs a) {
     const int r0 = T.j * 32;
     const int nr = min(32, s - r0);
     const int32_t *vp = a.vperm + B.vp_off;
-    const L lay(s);
+    const K8Lay lay(s, qcap);
     uint16_t *cnt = reinterpret_cast<uint16_t *>(kb);
     int32_t *s_vid = reinterpret_cast<int32_t *>(kb + lay.vid);
     uint32_t *s_vps = kb + lay.vps;
-    Cand *s_tops = reinterpret_cast<Cand *>(kb + lay.top);
     Cand *s_q = reinterpret_cast<Cand *>(kb + lay.que);
     if (tid < 32) {
       int32_t u = tid < nr ? vp[r0 + tid] : -1;
       s_ru[tid] = u;
       s_rp[tid] = u >= 0 ? (uint32_t)a.psize[u] : 0u;
-      s_qn[tid] = 0;
       s_tau[tid] = (u >= 0 && a.seed) ? from_out(a.seed[(int64_t)u * kk + kk - 1]) : sent();
     }
     // ================= phase A: counts |P_r ∩ P_v| for the 32 rows x all v of the cluster
@@ -737,131 +730,37 @@ __global__ void __launch_bounds__(TILE_T, 1) k_local_tile(TileArgs a) {
       }
     }
     __syncthreads();
-    // ================= K8: exact top-k per row (lane = row, warps split the candidates)
-    const int32_t ur = s_ru[lane];
-    const uint32_t pr = s_rp[lane];
-    const bool rowok = lane < nr && ur >= 0;
-    const int self = B.slot ? lane : r0 + lane;  // position of the row's own user
+    // ================= K8: exact top-k per row, one warp per row (no CTA barrier inside)
     const int slot = B.slot;  // mixed slice: candidates only inside the row's own slot group
-    const uint16_t *crow = cnt + lane * lay.RS;
-    // Round 1 bounds each row's k-th best from below; it is needed only when the survivors of
-    // tau alone could overflow the queue: clusters larger than the queue whose rows do not all
-    // hold a full running list yet (first function).  Rows that still overflow are rescanned
-    // with a bound taken from their own queue (rescan_row).
-    const bool tau_all = __all_sync(0xffffffffu, !rowok || is_real(s_tau[lane]));
-    const bool round1 = s - 1 > QCAP - 4 && !tau_all;
-    if (round1) {
-      // each thread's best R1 candidates of its interleaved share (any k distinct candidates
-      // of the row give a valid lower bound of the row's k-th best; the better, the tighter)
-      Cand t[R1];
-#pragma unroll
-      for (int j = 0; j < R1; ++j) t[j] = sent();
-      Ref wr = make_ref(sent(), pr, false);
-      if (rowok) {
-        for (int v4 = warp * 4; v4 < s; v4 += TILE_WARPS * 4) {
-          const uint2 c = *reinterpret_cast<const uint2 *>(crow + v4);
-          const uint4 ps = *reinterpret_cast<const uint4 *>(s_vps + v4);
-          const int4 id = *reinterpret_cast<const int4 *>(s_vid + v4);
-          const uint32_t iv[4] = {c.x & 0xFFFFu, c.x >> 16, c.y & 0xFFFFu, c.y >> 16};
-          const uint32_t pv[4] = {ps.x, ps.y, ps.z, ps.w};
-          const int32_t dv[4] = {id.x, id.y, id.z, id.w};
-#pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            if (v4 + e != self && passes(iv[e], pv[e], dv[e], wr)) {
-              Cand x{iv[e] | ((pr + pv[e] - iv[e]) << 16), dv[e]};
-#pragma unroll
-              for (int j = R1 - 1; j > 0; --j) {
-                if (better_c(x, t[j - 1])) t[j] = t[j - 1];
-                else if (better_c(x, t[j])) t[j] = x;
-              }
-              if (better_c(x, t[0])) t[0] = x;
-              wr = make_ref(t[R1 - 1], pr, false);
-            }
-          }
-        }
-      }
-#pragma unroll
-      for (int j = 0; j < R1; ++j) s_tops[lane * TOPS + warp * R1 + j] = t[j];
-      __syncthreads();
-      // T_r = the k-th best of the row's tops (>= k distinct real candidates are >= T_r)
-      for (int r = warp; r < nr; r += TILE_WARPS) {
-        KC e[TOPS / 32];
-#pragma unroll
-        for (int j = 0; j < TOPS / 32; ++j) e[j] = to_kc(s_tops[r * TOPS + 32 * j + lane]);
-        warp_sort<TOPS / 32>(e);
-        KC Tr = warp_get<TOPS / 32>(e, kk - 1);
-        if (lane == 0) s_T[r] = kc_cand(Tr);
-      }
-      __syncthreads();
-    }
-    // round 2: survivors (better than tau and not worse than T_r) to the row's queue
-    {
-      const Cand tau = s_tau[lane];
-      Ref ref = make_ref(tau, pr, false);
-      if (round1) {
-        const Cand Tr = s_T[lane];
-        if (is_real(Tr) && better_c(Tr, tau)) ref = make_ref(Tr, pr, true);
-      }
-      if (rowok) {
-        for (int v4 = warp * 4; v4 < s; v4 += TILE_WARPS * 4) {
-          const uint2 c = *reinterpret_cast<const uint2 *>(crow + v4);
-          const uint4 ps = *reinterpret_cast<const uint4 *>(s_vps + v4);
-          const int4 id = *reinterpret_cast<const int4 *>(s_vid + v4);
-          const uint32_t iv[4] = {c.x & 0xFFFFu, c.x >> 16, c.y & 0xFFFFu, c.y >> 16};
-          const uint32_t pv[4] = {ps.x, ps.y, ps.z, ps.w};
-          const int32_t dv[4] = {id.x, id.y, id.z, id.w};
-#pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const int vi = v4 + e;
-            bool ok = vi != self && passes(iv[e], pv[e], dv[e], ref);
-            if (slot) ok = ok && (vi ^ lane) < slot;
-            if (ok) {
-              int p = atomicAdd(&s_qn[lane], 1);
-              if (p < QCAP) s_q[lane * QCAP + p] = Cand{iv[e] | ((pr + pv[e] - iv[e]) << 16), dv[e]};
-            }
-          }
-        }
-      }
-    }
-    __syncthreads();
-    // final: per row (warp per row) sort the survivors, merge with the running list, write k.
-    // Fused mode updates the running list in place (each user is in one cluster per function),
-    // so a row without survivors keeps its list untouched.
     for (int r = warp; r < nr; r += TILE_WARPS) {
       const int32_t u = s_ru[r];
       if (u < 0) continue;
-      int nq = s_qn[r];
-      if (a.kstats && lane == 0) {
-        atomicAdd(&a.kstats[0], 1ull);
-        atomicAdd(&a.kstats[1], nq == 0 ? 1ull : 0ull);
-        atomicAdd(&a.kstats[2], (unsigned long long)nq);
-        atomicAdd(&a.kstats[3], nq > 32 * KS ? 1ull : 0ull);
-        atomicAdd(&a.kstats[4], nq > QCAP ? 1ull : 0ull);
-        if (r == 0) {
-          atomicAdd(&a.kstats[5], 1ull);
-          atomicAdd(&a.kstats[6], round1 ? 1ull : 0ull);
-          atomicAdd(&a.kstats[7], (unsigned long long)s);
-        }
-      }
-      if (a.seed && nq == 0) continue;
-      c2_cand *dst = a.seed ? a.out + (int64_t)u * kk : a.out + ((int64_t)B.f * a.n + u) * kk;
-      Cand *qr = s_q + r * QCAP;
-      // overflow: the queue holds QCAP distinct survivors; their k-th best bounds the row's
-      // k-th best from below, so rescanning the row (one warp) with it keeps every candidate of
-      // the top k and, short of massive ties, fits the queue.  A single group (big slices only:
-      // mixed slices have at most 31 candidates per row).
-      for (int pass = 0; pass < 2 && nq > QCAP; ++pass) {
-        KC e[2 * KS];
-#pragma unroll
-        for (int j = 0; j < 2 * KS; ++j) e[j] = to_kc(qr[32 * j + lane]);
-        warp_sort<2 * KS>(e);
-        const Ref T2 = make_ref(kc_cand(warp_get<2 * KS>(e, kk - 1)), s_rp[r], true);
-        __syncwarp();
-        const uint16_t *cr = cnt + r * lay.RS;
-        const int selfr = r0 + r;
-        const uint32_t prr = s_rp[r];
+      const uint32_t prr = s_rp[r];
+      const int selfr = slot ? r : r0 + r;
+      const uint16_t *cr = cnt + r * lay.RS;
+      Cand *qr = s_q + r * qcap;
+      const Cand tau = s_tau[r];
+      // survivors of T (strictly better than tau, not worse than a round-1 bound) -> qr by
+      // ballot compaction; returns their number (only the first qcap are stored)
+      auto scan = [&](const Ref &T) -> int {
         int m = 0;
-        for (int v4 = lane * 4; v4 - lane * 4 < s; v4 += 128) {
+        if (slot) {
+          const int lo = r & ~(slot - 1);
+          const int vi = lo + lane;
+          bool ok = false;
+          Cand x = sent();
+          if (lane < slot && vi != selfr) {
+            const uint32_t i = cr[vi], ps = s_vps[vi];
+            const int32_t id = s_vid[vi];
+            ok = passes(i, ps, id, T);
+            x = Cand{i | ((prr + ps - i) << 16), id};
+          }
+          const unsigned bal = __ballot_sync(0xffffffffu, ok);
+          if (ok) qr[__popc(bal & ((1u << lane) - 1))] = x;
+          return __popc(bal);
+        }
+        for (int base = 0; base < s; base += 128) {
+          const int v4 = base + lane * 4;
           uint32_t iv[4] = {0, 0, 0, 0}, pv[4] = {0, 0, 0, 0};
           int32_t dv[4] = {INT32_MAX, INT32_MAX, INT32_MAX, INT32_MAX};
           if (v4 < s) {
@@ -873,44 +772,143 @@ __global__ void __launch_bounds__(TILE_T, 1) k_local_tile(TileArgs a) {
             dv[0] = id.x, dv[1] = id.y, dv[2] = id.z, dv[3] = id.w;
           }
 #pragma unroll
-          for (int e2 = 0; e2 < 4; ++e2) {
-            const bool ok = v4 + e2 != selfr && passes(iv[e2], pv[e2], dv[e2], T2);
+          for (int e = 0; e < 4; ++e) {
+            const bool ok = v4 + e != selfr && passes(iv[e], pv[e], dv[e], T);
             const unsigned bal = __ballot_sync(0xffffffffu, ok);
             const int p = m + __popc(bal & ((1u << lane) - 1));
-            if (ok && p < QCAP) qr[p] = Cand{iv[e2] | ((prr + pv[e2] - iv[e2]) << 16), dv[e2]};
+            if (ok && p < qcap) qr[p] = Cand{iv[e] | ((prr + pv[e] - iv[e]) << 16), dv[e]};
             m += __popc(bal);
           }
         }
-        __syncwarp();
-        nq = m;
-      }
-      KC L[KS];  // top-k of this function's candidates above tau (sentinel padded)
-      if (nq <= QCAP) {
-        if (nq <= 32 * KS) {
-          KC q[KS];
+        return m;
+      };
+      // k-th best of the first 64*KS queue entries (all distinct real candidates): a valid
+      // lower bound of the row's k-th best
+      auto kth_of_queue = [&]() -> Ref {
+        KC e[2 * KS];
 #pragma unroll
-          for (int j = 0; j < KS; ++j) q[j] = to_kc((32 * j + lane < nq) ? qr[32 * j + lane] : sent());
-          warp_sort<KS>(q);
+        for (int j = 0; j < 2 * KS; ++j) e[j] = to_kc(qr[32 * j + lane]);
+        warp_sort<2 * KS>(e);
+        return make_ref(kc_cand(warp_get<2 * KS>(e, kk - 1)), prr, true);
+      };
+      Ref T = make_ref(tau, prr, false);
+      bool r1 = false;
+      if (!slot && !is_real(tau) && s - 1 > qcap) {
+        // round 1: every lane's best R1 candidates of its share; T_r = the k-th best of the
+        // 32*R1 tops (any k distinct candidates bound the row's k-th best from below)
+        r1 = true;
+        Cand t[R1];
 #pragma unroll
-          for (int j = 0; j < KS; ++j) L[j] = q[j];
-        } else {
-          KC q[2 * KS];
+        for (int j = 0; j < R1; ++j) t[j] = sent();
+        Ref wr = make_ref(sent(), prr, false);
+        for (int v4 = lane * 4; v4 < s; v4 += 128) {
+          const uint2 c = *reinterpret_cast<const uint2 *>(cr + v4);
+          const uint4 ps = *reinterpret_cast<const uint4 *>(s_vps + v4);
+          const int4 id = *reinterpret_cast<const int4 *>(s_vid + v4);
+          const uint32_t iv[4] = {c.x & 0xFFFFu, c.x >> 16, c.y & 0xFFFFu, c.y >> 16};
+          const uint32_t pv[4] = {ps.x, ps.y, ps.z, ps.w};
+          const int32_t dv[4] = {id.x, id.y, id.z, id.w};
 #pragma unroll
-          for (int j = 0; j < 2 * KS; ++j) q[j] = to_kc((32 * j + lane < nq) ? qr[32 * j + lane] : sent());
-          warp_sort<2 * KS>(q);
+          for (int e = 0; e < 4; ++e) {
+            if (v4 + e != selfr && passes(iv[e], pv[e], dv[e], wr)) {
+              Cand x{iv[e] | ((prr + pv[e] - iv[e]) << 16), dv[e]};
 #pragma unroll
-          for (int j = 0; j < KS; ++j) L[j] = q[j];
+              for (int j = R1 - 1; j > 0; --j) {
+                if (better_c(x, t[j - 1])) t[j] = t[j - 1];
+                else if (better_c(x, t[j])) t[j] = x;
+              }
+              if (better_c(x, t[0])) t[0] = x;
+              wr = make_ref(t[R1 - 1], prr, false);
+            }
+          }
         }
+        KC e[R1];
+#pragma unroll
+        for (int j = 0; j < R1; ++j) e[j] = to_kc(t[j]);
+        warp_sort<R1>(e);
+        const KC Tr = warp_get<R1>(e, kk - 1);
+        if (kc_real(Tr)) T = make_ref(kc_cand(Tr), prr, true);
+      }
+      int m = scan(T);
+      int rescans = 0;
+      for (; rescans < 2 && m > qcap; ++rescans) {
+        T = kth_of_queue();
+        __syncwarp();
+        m = scan(T);
+      }
+      // shrink a long queue in place: keep the entries not worse than the k-th best of its
+      // first 64*KS (stops when that makes no progress: massive ties)
+      while (m > 64 * KS && m <= qcap) {
+        const Ref T2 = kth_of_queue();
+        __syncwarp();
+        int w = 0;
+        for (int b0 = 0; b0 < m; b0 += 32) {
+          const int j = b0 + lane;
+          Cand x = j < m ? qr[j] : sent();
+          const uint32_t i = x.iu & 0xFFFFu, ps = (x.iu >> 16) + i - prr;
+          const bool ok = j < m && passes(i, ps, x.id, T2);
+          __syncwarp();
+          const unsigned bal = __ballot_sync(0xffffffffu, ok);
+          if (ok) qr[w + __popc(bal & ((1u << lane) - 1))] = x;
+          w += __popc(bal);
+        }
+        __syncwarp();
+        if (w == m) break;
+        m = w;
+      }
+      if (a.kstats && lane == 0) {
+        atomicAdd(&a.kstats[0], 1ull);
+        atomicAdd(&a.kstats[1], m == 0 ? 1ull : 0ull);
+        atomicAdd(&a.kstats[2], (unsigned long long)m);
+        atomicAdd(&a.kstats[3], m > 32 * KS ? 1ull : 0ull);
+        atomicAdd(&a.kstats[4], (unsigned long long)rescans);
+        atomicAdd(&a.kstats[6], r1 ? 1ull : 0ull);
+        if (r == 0) {
+          atomicAdd(&a.kstats[5], 1ull);
+          atomicAdd(&a.kstats[7], (unsigned long long)s);
+        }
+      }
+      if (a.seed && m == 0) continue;
+      c2_cand *dst = a.seed ? a.out + (int64_t)u * kk : a.out + ((int64_t)B.f * a.n + u) * kk;
+      if (a.seed && m <= 8) {
+        // few survivors: insert them one by one into the running list (duplicates skipped)
+        KC S[KS];
+#pragma unroll
+        for (int j = 0; j < KS; ++j) S[j] = to_kc((32 * j + lane < kk) ? from_out(dst[32 * j + lane]) : sent());
+        for (int j = 0; j < m; ++j) {
+          const KC x = to_kc(qr[j]);
+          bool dup = false;
+#pragma unroll
+          for (int jj = 0; jj < KS; ++jj) dup |= S[jj].k == x.k;
+          if (__any_sync(0xffffffffu, dup)) continue;
+          warp_insert<KS>(S, x);
+        }
+#pragma unroll
+        for (int j = 0; j < KS; ++j)
+          if (32 * j + lane < kk) dst[32 * j + lane] = kc_out(S[j]);
+        continue;
+      }
+      KC L[KS];  // top-k of this function's survivors (sentinel padded)
+      if (m <= 32 * KS) {
+        KC q[KS];
+#pragma unroll
+        for (int j = 0; j < KS; ++j) q[j] = to_kc((32 * j + lane < m) ? qr[32 * j + lane] : sent());
+        warp_sort<KS>(q);
+#pragma unroll
+        for (int j = 0; j < KS; ++j) L[j] = q[j];
+      } else if (m <= 64 * KS) {
+        KC q[2 * KS];
+#pragma unroll
+        for (int j = 0; j < 2 * KS; ++j) q[j] = to_kc((32 * j + lane < m) ? qr[32 * j + lane] : sent());
+        warp_sort<2 * KS>(q);
+#pragma unroll
+        for (int j = 0; j < KS; ++j) L[j] = q[j];
       } else {
-        // pathological ties: exact insertion over all the row's candidates
+        // pathological ties: exact insertion over the row's candidates
         if (a.kstats && lane == 0) atomicAdd(&a.kstats[8], 1ull);
         Cand Lc[KS];
 #pragma unroll
         for (int j = 0; j < KS; ++j) Lc[j] = sent();
-        const Cand tr = s_tau[r];
-        const uint32_t prr = s_rp[r];
-        const int selfr = slot ? r : r0 + r;
-        const uint16_t *cr = cnt + r * lay.RS;
         Cand thr = sent();
         for (int vb = 0; vb < s; vb += 32) {
           const int vi = vb + lane;
@@ -922,7 +920,7 @@ __global__ void __launch_bounds__(TILE_T, 1) k_local_tile(TileArgs a) {
               c = Cand{ci | ((prr + s_vps[vi] - ci) << 16), v};
             }
           }
-          bool bt = is_real(c) && better_c(c, tr) && better_c(c, thr);
+          bool bt = is_real(c) && better_c(c, tau) && better_c(c, thr);
           unsigned mask = __ballot_sync(0xffffffffu, bt);
           while (mask) {
             int l = __ffs(mask) - 1;
@@ -946,24 +944,24 @@ __global__ void __launch_bounds__(TILE_T, 1) k_local_tile(TileArgs a) {
       KC S[KS];
 #pragma unroll
       for (int j = 0; j < KS; ++j) S[j] = to_kc((32 * j + lane < kk) ? from_out(dst[32 * j + lane]) : sent());
-      KC m[2 * KS];
+      KC mm[2 * KS];
 #pragma unroll
-      for (int j = 0; j < KS; ++j) m[j] = (32 * j + lane < kk) ? L[j] : KC{0ull, 1u << 16};
+      for (int j = 0; j < KS; ++j) mm[j] = (32 * j + lane < kk) ? L[j] : KC{0ull, 1u << 16};
 #pragma unroll
-      for (int j = 0; j < KS; ++j) m[KS + j] = shfl_e(S[KS - 1 - j], 31 - lane);
-      warp_bitonic_merge<2 * KS>(m);
+      for (int j = 0; j < KS; ++j) mm[KS + j] = shfl_e(S[KS - 1 - j], 31 - lane);
+      warp_bitonic_merge<2 * KS>(mm);
       // drop adjacent duplicates (a repeated id carries identical values, A16); keep k
       int base = 0;
 #pragma unroll
       for (int j = 0; j < 2 * KS; ++j) {
-        const uint32_t lo = (uint32_t)m[j].k;
+        const uint32_t lo = (uint32_t)mm[j].k;
         uint32_t prev = __shfl_up_sync(0xffffffffu, lo, 1);
-        uint32_t prevj = j > 0 ? __shfl_sync(0xffffffffu, (uint32_t)m[j - 1].k, 31) : 0u;
+        uint32_t prevj = j > 0 ? __shfl_sync(0xffffffffu, (uint32_t)mm[j - 1].k, 31) : 0u;
         if (lane == 0) prev = prevj;
-        bool keep = kc_real(m[j]) && (j + lane == 0 || lo != prev);
+        bool keep = kc_real(mm[j]) && (j + lane == 0 || lo != prev);
         unsigned bal = __ballot_sync(0xffffffffu, keep);
         int rank = base + __popc(bal & ((1u << lane) - 1));
-        if (keep && rank < kk) dst[rank] = kc_out(m[j]);
+        if (keep && rank < kk) dst[rank] = kc_out(mm[j]);
         base += __popc(bal);
       }
       for (int p = base + lane; p < kk; p += 32) dst[p] = c2_cand{-1, 0, 0};
@@ -1154,6 +1152,7 @@ int local_knn(c2_ctx *ctx, const Csr &csr, int t, const Clusters &cl, int k, c2_
   // ---- tile kernel configuration
   TileKernel tk = nullptr;
   int grid = 0;
+  int qcap = 64;
   size_t smem = 0;
   uint32_t *gscratch = nullptr;
   int *counters = nullptr;
@@ -1163,7 +1162,11 @@ int local_knn(c2_ctx *ctx, const Csr &csr, int t, const Clusters &cl, int k, c2_
     int nhi = std::max(nbits - 4, 1);
     int max_sl = (int)((maxs + 31) / 32);
     int vpt = max_sl <= TILE_WARPS ? 1 : max_sl <= 2 * TILE_WARPS ? 2 : 4;
-    const int k8w = k <= 32 ? K8Lay<1>(smax).words : K8Lay<2>(smax).words;
+    // survivor queue per row: 256 entries where shared memory allows, at least 64*KS
+    const int qmin = k <= 32 ? 64 : 128;
+    qcap = 256;
+    while (qcap > qmin && (size_t)K8Lay(smax, qcap).words * 4 > ctx->smem_optin) qcap -= 64;
+    const int k8w = K8Lay(smax, qcap).words;
     const size_t mw = (size_t)((W + 4) & ~3);
     // counts in shared memory (aliased onto M) when one g0 group covers the largest cluster
     // and the K8 region fits; else a per-CTA global scratch region
@@ -1186,7 +1189,7 @@ int local_knn(c2_ctx *ctx, const Csr &csr, int t, const Clusters &cl, int k, c2_
   auto launch_tiles = [&](int64_t lo, int64_t hi, int ci, const c2_cand *seed, c2_cand *dst) -> int {
     if (hi <= lo) return C2_OK;
     TileArgs ta{tiles, lo, hi, counters + ci, bcs, vperm, blk_len8, blk_off8, packed, csr.psize, n, W, nwin, k,
-                seed, dst, ctx->kstats, gscratch, smax};
+                seed, dst, ctx->kstats, gscratch, smax, qcap};
     int g = (int)std::min<int64_t>(grid, hi - lo);
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     if (ctx->timing) {
