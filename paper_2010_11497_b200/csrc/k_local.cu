@@ -600,6 +600,7 @@ __global__ void __launch_bounds__(TILE_T, 1) k_local_tile(TileArgs a) {
   __shared__ int32_t s_ru[32];
   __shared__ uint32_t s_rp[32];
   __shared__ Cand s_tau[32];
+  __shared__ int s_row;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   for (int i = tid; i < a.W + 1; i += TILE_T) M[i] = 0;
   uint32_t *kb = SMEM_CNT ? dyn : a.gscratch + (int64_t)blockIdx.x * K8Lay(a.smax, qcap).words;  // K8 region
@@ -612,6 +613,7 @@ __global__ void __launch_bounds__(TILE_T, 1) k_local_tile(TileArgs a) {
     __syncthreads();
     const int64_t it = a.lo + s_item;
     if (it >= a.hi) break;
+    long long ck0 = a.kstats ? clock64() : 0, ck_r1 = 0, ck_scan = 0;
     const Tile T = a.tiles[it];
     const BigC B = a.bcs[T.bc];
     const int s = B.s;
@@ -624,6 +626,7 @@ __global__ void __launch_bounds__(TILE_T, 1) k_local_tile(TileArgs a) {
     int32_t *s_vid = reinterpret_cast<int32_t *>(kb + lay.vid);
     uint32_t *s_vps = kb + lay.vps;
     Cand *s_q = reinterpret_cast<Cand *>(kb + lay.que);
+    if (tid == 0) s_row = 0;
     if (tid < 32) {
       int32_t u = tid < nr ? vp[r0 + tid] : -1;
       s_ru[tid] = u;
@@ -720,6 +723,7 @@ __global__ void __launch_bounds__(TILE_T, 1) k_local_tile(TileArgs a) {
         }
       }
     }
+    const long long ck1 = a.kstats ? clock64() : 0;
     // member ids and sizes (positions s .. s4-1: never-passing pads)
     {
       const int s4 = (s + 3) & ~3;
@@ -732,7 +736,11 @@ __global__ void __launch_bounds__(TILE_T, 1) k_local_tile(TileArgs a) {
     __syncthreads();
     // ================= K8: exact top-k per row, one warp per row (no CTA barrier inside)
     const int slot = B.slot;  // mixed slice: candidates only inside the row's own slot group
-    for (int r = warp; r < nr; r += TILE_WARPS) {
+    for (;;) {  // rows taken dynamically: their costs differ a lot
+      int r = 0;
+      if (lane == 0) r = atomicAdd(&s_row, 1);
+      r = __shfl_sync(0xffffffffu, r, 0);
+      if (r >= nr) break;
       const int32_t u = s_ru[r];
       if (u < 0) continue;
       const uint32_t prr = s_rp[r];
@@ -791,12 +799,10 @@ __global__ void __launch_bounds__(TILE_T, 1) k_local_tile(TileArgs a) {
         warp_sort<2 * KS>(e);
         return make_ref(kc_cand(warp_get<2 * KS>(e, kk - 1)), prr, true);
       };
-      Ref T = make_ref(tau, prr, false);
-      bool r1 = false;
-      if (!slot && !is_real(tau) && s - 1 > qcap) {
-        // round 1: every lane's best R1 candidates of its share; T_r = the k-th best of the
-        // 32*R1 tops (any k distinct candidates bound the row's k-th best from below)
-        r1 = true;
+      long long ckr = a.kstats ? clock64() : 0;
+      // round 1: every lane's best R1 candidates of its share; T_r = the k-th best of the
+      // 32*R1 tops (any k distinct candidates bound the row's k-th best from below)
+      auto round1 = [&](Ref &T) {
         Cand t[R1];
 #pragma unroll
         for (int j = 0; j < R1; ++j) t[j] = sent();
@@ -827,9 +833,24 @@ __global__ void __launch_bounds__(TILE_T, 1) k_local_tile(TileArgs a) {
         for (int j = 0; j < R1; ++j) e[j] = to_kc(t[j]);
         warp_sort<R1>(e);
         const KC Tr = warp_get<R1>(e, kk - 1);
-        if (kc_real(Tr)) T = make_ref(kc_cand(Tr), prr, true);
+        if (kc_real(Tr) && better_c(kc_cand(Tr), tau)) T = make_ref(kc_cand(Tr), prr, true);
+      };
+      Ref T = make_ref(tau, prr, false);
+      // rows without a running list yet (tau = sentinel) whose candidates cannot all be queued
+      // start with round 1; rows whose tau lets too many through get it after the first scan
+      bool r1 = !slot && !is_real(tau) && s - 1 > qcap;
+      if (r1) round1(T);
+      if (a.kstats) {
+        const long long c = clock64();
+        ck_r1 += c - ckr;
+        ckr = c;
       }
       int m = scan(T);
+      if (m > qcap && !slot && !r1) {
+        r1 = true;
+        round1(T);
+        m = scan(T);
+      }
       int rescans = 0;
       for (; rescans < 2 && m > qcap; ++rescans) {
         T = kth_of_queue();
@@ -856,6 +877,7 @@ __global__ void __launch_bounds__(TILE_T, 1) k_local_tile(TileArgs a) {
         if (w == m) break;
         m = w;
       }
+      if (a.kstats) ck_scan += clock64() - ckr;
       if (a.kstats && lane == 0) {
         atomicAdd(&a.kstats[0], 1ull);
         atomicAdd(&a.kstats[1], m == 0 ? 1ull : 0ull);
@@ -966,7 +988,16 @@ __global__ void __launch_bounds__(TILE_T, 1) k_local_tile(TileArgs a) {
       }
       for (int p = base + lane; p < kk; p += 32) dst[p] = c2_cand{-1, 0, 0};
     }
+    const long long ck2 = a.kstats ? clock64() : 0;
     __syncthreads();
+    if (a.kstats && lane == 0) {
+      const long long ck3 = clock64();
+      atomicAdd(&a.kstats[9], (unsigned long long)(ck1 - ck0));    // phase A (+ tile head)
+      atomicAdd(&a.kstats[10], (unsigned long long)ck_r1);         // K8 round 1
+      atomicAdd(&a.kstats[11], (unsigned long long)ck_scan);       // K8 scan + queue shrink
+      atomicAdd(&a.kstats[12], (unsigned long long)(ck2 - ck1 - ck_r1 - ck_scan));  // K8 rest
+      atomicAdd(&a.kstats[13], (unsigned long long)(ck3 - ck2));   // wait at the K8 barrier
+    }
     // restore the all-zero M words the K8 region overwrote
     if (SMEM_CNT) {
       const int dw = min(lay.words, a.W + 1);

@@ -17,4 +17,7 @@ c2.build(d_o, d_i, k=C.k, t=C.t, b=C.b, N=C.N, seed=C.hash_seed, ctx=ctx)
 torch.cuda.synchronize()
 k = ks.tolist()
 print(f"{name}: rows {k[0]} nq==0 {k[1]/k[0]:.3f} mean nq {k[2]/k[0]:.2f} nq>32KS {k[3]/k[0]:.4f} overflow {k[4]/k[0]:.5f} "
-      f"tiles {k[5]} round1 tiles {k[6]} mean s {k[7]/max(k[5],1):.1f}")
+      f"tiles {k[5]} round1 rows {k[6]} mean s {k[7]/max(k[5],1):.1f} exact-fallback rows {k[8]}")
+tot = sum(k[9:14])
+print("  warp-cycles: " + " ".join(f"{n} {v / tot * 100:.1f}%" for n, v in
+      zip(["phaseA", "round1", "scan", "k8-rest", "k8-wait"], k[9:14])))
