@@ -171,6 +171,7 @@ int c2_ctx_set_option(c2_ctx *ctx, int key, int64_t value) {
     case C2_OPT_SYNC_CHECK: ctx->sync_check = value != 0; return C2_OK;
     case C2_OPT_TIMING: ctx->timing = value != 0; return C2_OK;
     case C2_OPT_KSTATS: ctx->kstats = (unsigned long long *)(intptr_t)value; return C2_OK;
+    case C2_OPT_RELABEL: ctx->relabel = value != 0; return C2_OK;
     default: return set_err(ctx, C2_EINVAL, "unknown option %d", key);
   }
 }

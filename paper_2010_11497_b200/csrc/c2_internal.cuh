@@ -27,7 +27,8 @@ struct c2_ctx {
   int sketch_depth = C2_SKETCH_D;
   bool sync_check = false;
   bool timing = false;
-  unsigned long long *kstats = nullptr;  // C2_OPT_KSTATS: dev [16] K7/K8 counters
+  unsigned long long *kstats = nullptr;
+  bool relabel = true;  // C2_OPT_RELABEL  // C2_OPT_KSTATS: dev [16] K7/K8 counters
   c2_stats stats{};
   // device workspace: name -> (ptr, bytes); grow-only
   std::map<std::string, std::pair<void *, size_t>> ws;

@@ -36,6 +36,7 @@ namespace c2 {
 // 2..32 users, each in its own aligned group of `slot` positions (empty positions are -1).
 struct BigC {
   int32_t f, s, vp_off, sl_off, slot;
+  int32_t kc;  // relabeled units: size of the unit's local item universe
 };
 struct Tile {
   int32_t bc, j;
@@ -119,7 +120,7 @@ __global__ void k_bc_fill(const uint32_t *__restrict__ sval, int64_t nbig, const
   int64_t c = g - ccum[f];
   const int32_t *off = offsets + (int64_t)f * (n + 1);
   int32_t s = off[c + 1] - off[c];
-  BigC b{f, s, vp_scan[i], sl_scan[i], 0};
+  BigC b{f, s, vp_scan[i], sl_scan[i], 0, 0};
   bcs[i] = b;
   bstart[i] = off[c];
   int ns = (s + 31) / 32;
@@ -158,7 +159,7 @@ __global__ void k_mix_bc(const MixGroup *__restrict__ groups, int ngroups, int64
   if (m >= nmix) return;
   int gi = 0;
   while (gi + 1 < ngroups && groups[gi + 1].first_slice <= m) ++gi;
-  bcs[nbig + m] = BigC{groups[gi].f, 32, (int32_t)(vp_base + m * 32), (int32_t)(sl_base + m), 1 << groups[gi].cls};
+  bcs[nbig + m] = BigC{groups[gi].f, 32, (int32_t)(vp_base + m * 32), (int32_t)(sl_base + m), 1 << groups[gi].cls, 0};
   tiles[sl_base + m] = Tile{(int32_t)(nbig + m), 0};
 }
 
@@ -299,6 +300,166 @@ __global__ void k_sl_fill(const Tile *__restrict__ tiles, int64_t nslices, const
   }
 }
 
+
+// ------------------------------------------------------------------ cluster-local relabeling
+// Only items held by >= 2 members of a cluster can contribute to an intersection, so every
+// cluster unit (a big cluster, or one mixed slice of small clusters) gets its own dense item
+// universe: the items of in-unit degree >= 2, numbered 0..kc-1 in increasing global id.  Each
+// member's list is rewritten in local ids (degree-1 items dropped, order kept) straight into the
+// packed [p/8][lane][8] u16 layout, padded with the sentinel kc.  The tile kernel then needs a
+// mask M of kc+1 words -- one window, far less shared memory than the global item range -- and
+// streams shorter lists.  Results are unchanged: |P_u ∩ P_v| is invariant under dropping items
+// that no other member of the unit holds and under renaming items injectively (|P_u| and the
+// union still come from the original profile sizes).
+
+// allocation bound per slice: ceil(max original |P_v| over its members / 8)
+__global__ void k_sl_maxlen(const Tile *__restrict__ tiles, int64_t nslices, const BigC *__restrict__ bcs,
+                            const int32_t *__restrict__ vperm, const int32_t *__restrict__ psize,
+                            int32_t *__restrict__ len8) {
+  const int lane = threadIdx.x & 31;
+  const int64_t sl = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (sl >= nslices) return;
+  const Tile T = tiles[sl];
+  const BigC b = bcs[T.bc];
+  const int vi = T.j * 32 + lane;
+  const int32_t v = vi < b.s ? vperm[b.vp_off + vi] : -1;
+  int c = v >= 0 ? psize[v] : 0;
+#pragma unroll
+  for (int o = 16; o; o >>= 1) c = max(c, __shfl_xor_sync(0xffffffffu, c, o));
+  if (lane == 0) len8[sl] = (c + 7) / 8;
+}
+
+constexpr int RL_T = 256;
+constexpr int RL_MAXS = 2048;  // members per unit handled by the relabel kernel
+
+// One CTA per unit (persistent).  Shared memory (nw = ceil(m/32) words each): seen, seen2 (item
+// bitmaps; all zero between units), wslot (word -> index in the touched list), touched (words
+// with any item of the unit), tbase (local-id base per touched word); slen[RL_MAXS].  Work is
+// O(items of the unit + touched words): local ids are numbered per touched word in the order
+// words were first touched (any injective numbering gives the same intersections).
+__global__ void __launch_bounds__(RL_T) k_relabel(BigC *__restrict__ bcs, int64_t nunits,
+                                                 const int32_t *__restrict__ vperm, const int32_t *__restrict__ offs,
+                                                 const int32_t *__restrict__ items, int32_t nw,
+                                                 const int32_t *__restrict__ blk_off8, int32_t *__restrict__ blk_len8,
+                                                 uint16_t *__restrict__ packed16, int *__restrict__ counter,
+                                                 int *__restrict__ max_kc) {
+  extern __shared__ __align__(16) uint32_t rsm[];
+  uint32_t *seen = rsm, *seen2 = rsm + nw, *wslot = rsm + 2 * nw, *touched = rsm + 3 * nw, *tbase = rsm + 4 * nw;
+  int32_t *slen = reinterpret_cast<int32_t *>(rsm + 5 * nw + 1);
+  __shared__ int s_unit, s_nt;
+  __shared__ uint32_t s_part[RL_T / 32];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr int NWARP = RL_T / 32;
+  for (int i = tid; i < 2 * nw; i += RL_T) rsm[i] = 0;
+  for (;;) {
+    __syncthreads();
+    if (tid == 0) {
+      s_unit = atomicAdd(counter, 1);
+      s_nt = 0;
+    }
+    __syncthreads();
+    const int64_t unit = s_unit;
+    if (unit >= nunits) break;
+    const BigC b = bcs[unit];
+    const int npos = ((b.s + 31) / 32) * 32;  // member positions incl. the last slice's tail
+    const int32_t *vp = vperm + b.vp_off;
+    // 1. in-unit degree (saturating at 2) of every item: seen / seen2 bitmaps; touched words
+    for (int i = warp; i < b.s; i += NWARP) {
+      const int32_t v = vp[i];
+      if (v < 0) continue;
+      for (int32_t p = offs[v] + lane; p < offs[v + 1]; p += 32) {
+        const int32_t x = items[p];
+        const uint32_t bit = 1u << (x & 31);
+        const uint32_t old = atomicOr(&seen[x >> 5], bit);
+        if (old == 0u) touched[atomicAdd(&s_nt, 1)] = (uint32_t)(x >> 5);
+        if (old & bit) atomicOr(&seen2[x >> 5], bit);
+      }
+    }
+    __syncthreads();
+    const int nt = s_nt;
+    // 2. tbase[i] = degree->=2 items in touched words before i (block-wide exclusive scan)
+    {
+      const int per = (nt + RL_T - 1) / RL_T;
+      const int i0 = min(tid * per, nt), i1 = min(i0 + per, nt);
+      uint32_t sum = 0;
+      for (int i = i0; i < i1; ++i) sum += __popc(seen2[touched[i]]);
+      uint32_t incl = sum;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+      }
+      if (lane == 31) s_part[warp] = incl;
+      __syncthreads();
+      if (warp == 0) {
+        uint32_t x = lane < NWARP ? s_part[lane] : 0u, xi = x;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const uint32_t y = __shfl_up_sync(0xffffffffu, xi, o);
+          if (lane >= o) xi += y;
+        }
+        if (lane < NWARP) s_part[lane] = xi - x;
+      }
+      __syncthreads();
+      uint32_t run = s_part[warp] + incl - sum;
+      for (int i = i0; i < i1; ++i) {
+        const uint32_t w = touched[i];
+        tbase[i] = run;
+        wslot[w] = (uint32_t)i;
+        run += __popc(seen2[w]);
+      }
+      if (i1 == nt && i0 < i1) tbase[nt] = run;
+      if (nt == 0 && tid == 0) tbase[0] = 0;
+    }
+    __syncthreads();
+    const uint32_t kc = tbase[nt];
+    // 3. compacted lists in local ids, written into the packed layout of each slice
+    for (int i = warp; i < npos; i += NWARP) {
+      const int32_t v = i < b.s ? vp[i] : -1;
+      int cnt = 0;
+      if (v >= 0) {
+        uint16_t *dst = packed16 + (int64_t)blk_off8[b.sl_off + (i >> 5)] * 256 + (i & 31) * 8;
+        for (int32_t p0 = offs[v]; p0 < offs[v + 1]; p0 += 32) {
+          const int32_t p = p0 + lane;
+          bool keep = false;
+          uint32_t lid = 0;
+          if (p < offs[v + 1]) {
+            const int32_t x = items[p];
+            const uint32_t w2 = seen2[x >> 5], bit = 1u << (x & 31);
+            keep = (w2 & bit) != 0;
+            if (keep) lid = tbase[wslot[x >> 5]] + __popc(w2 & (bit - 1));
+          }
+          const unsigned bal = __ballot_sync(0xffffffffu, keep);
+          const int pos = cnt + __popc(bal & ((1u << lane) - 1));
+          if (keep) dst[(pos >> 3) * 256 + (pos & 7)] = (uint16_t)lid;
+          cnt += __popc(bal);
+        }
+      }
+      if (lane == 0) slen[i] = cnt;
+    }
+    __syncthreads();
+    // 4. per slice: actual length (in 8s), pads = kc up to it; clear the touched words
+    for (int i = tid; i < npos; i += RL_T) {
+      int mx = slen[i];
+#pragma unroll
+      for (int o = 16; o; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+      const int len8 = (mx + 7) / 8;
+      const int sl = b.sl_off + (i >> 5);
+      if ((i & 31) == 0) blk_len8[sl] = len8;
+      uint16_t *dst = packed16 + (int64_t)blk_off8[sl] * 256 + (i & 31) * 8;
+      for (int pos = slen[i]; pos < len8 * 8; ++pos) dst[(pos >> 3) * 256 + (pos & 7)] = (uint16_t)kc;
+    }
+    for (int i = tid; i < nt; i += RL_T) {
+      const uint32_t w = touched[i];
+      seen[w] = 0;
+      seen2[w] = 0;
+    }
+    if (tid == 0) {
+      bcs[unit].kc = (int32_t)kc;
+      atomicMax(max_kc, (int)kc);
+    }
+  }
+}
 
 // ------------------------------------------------------------------ candidate lists
 // A candidate (v, i, U) is held as {iu = i | U << 16, id}.  The order (A13): a before b iff
@@ -525,6 +686,7 @@ struct TileArgs {
   uint32_t *gscratch;   // !SMEM_CNT only: per CTA K8Lay(smax, qcap).words words
   int32_t smax;
   int32_t qcap;         // survivor queue capacity per row
+  int relabel;          // 1: items are unit-local ids, the tile's window is [0, B.kc) (nwin == 1)
 };
 
 // 8 masks of one uint4 of packed u16 item ids
@@ -605,7 +767,6 @@ __global__ void __launch_bounds__(TILE_T, 1) k_local_tile(TileArgs a) {
   for (int i = tid; i < a.W + 1; i += TILE_T) M[i] = 0;
   uint32_t *kb = SMEM_CNT ? dyn : a.gscratch + (int64_t)blockIdx.x * K8Lay(a.smax, qcap).words;  // K8 region
   const int nwin = a.nwin;
-  const uint32_t W = (uint32_t)a.W;
   const int kk = a.k;
   for (;;) {
     __syncthreads();
@@ -621,6 +782,7 @@ __global__ void __launch_bounds__(TILE_T, 1) k_local_tile(TileArgs a) {
     const int r0 = T.j * 32;
     const int nr = min(32, s - r0);
     const int32_t *vp = a.vperm + B.vp_off;
+    const uint32_t W = a.relabel ? (uint32_t)B.kc : (uint32_t)a.W;
     const K8Lay lay(s, qcap);
     uint16_t *cnt = reinterpret_cast<uint16_t *>(kb);
     int32_t *s_vid = reinterpret_cast<int32_t *>(kb + lay.vid);
@@ -663,23 +825,23 @@ __global__ void __launch_bounds__(TILE_T, 1) k_local_tile(TileArgs a) {
             const int64_t bi = (int64_t)(B.sl_off + jj) * nwin + w;
             const int32_t len8 = a.blk_len8[bi];
             const uint4 *src = a.packed + (int64_t)a.blk_off8[bi] * 32 + lane;
-            int32_t p8 = 0;
-            for (; p8 + 1 < len8; p8 += 2) {
-              uint4 d0 = __ldg(src + (int64_t)p8 * 32);
-              uint4 d1 = __ldg(src + (int64_t)(p8 + 1) * 32);
+            // two 16-byte loads per step, the next step's pair prefetched (odd tails padded
+            // with the sentinel item W, whose mask M[W] is 0)
+            const uint32_t pw = W | (W << 16);
+            const uint4 padv = make_uint4(pw, pw, pw, pw);
+            uint4 d0 = len8 > 0 ? __ldg(src) : padv;
+            uint4 d1 = len8 > 1 ? __ldg(src + 32) : padv;
+            for (int32_t p8 = 0; p8 < len8; p8 += 2) {
+              const uint4 n0 = p8 + 2 < len8 ? __ldg(src + (int64_t)(p8 + 2) * 32) : padv;
+              const uint4 n1 = p8 + 3 < len8 ? __ldg(src + (int64_t)(p8 + 3) * 32) : padv;
               uint32_t m[8];
               masks8(M, d0, m);
               uint32_t e8a = C[q].add8(m);
               masks8(M, d1, m);
               uint32_t e8b = C[q].add8(m);
               C[q].add16(e8a, e8b);
-            }
-            if (p8 < len8) {
-              uint4 d0 = __ldg(src + (int64_t)p8 * 32);
-              uint32_t m[8];
-              masks8(M, d0, m);
-              uint32_t e8a = C[q].add8(m);
-              C[q].add16(e8a, 0u);
+              d0 = n0;
+              d1 = n1;
             }
           }
         }
@@ -1118,6 +1280,7 @@ int local_knn(c2_ctx *ctx, const Csr &csr, int t, const Clusters &cl, int k, c2_
   Tile *tiles = nullptr;
   int32_t *vperm = nullptr, *blk_len8 = nullptr, *blk_off8 = nullptr;
   uint4 *packed = nullptr;
+  bool relabel = false;
   const int32_t m = csr.max_item + 1;
   int32_t nwin = (int32_t)((m + 50000 - 1) / 50000);
   int32_t W = (int32_t)((m + nwin - 1) / nwin);
@@ -1163,21 +1326,60 @@ int local_knn(c2_ctx *ctx, const Csr &csr, int t, const Clusters &cl, int k, c2_
                                            tiles);
       C2_LAUNCHED(ctx, "k_mix_bc");
     }
-    const int64_t nb = nslices * nwin;
-    blk_len8 = (int32_t *)ws_get(ctx, "blk_len8", (size_t)(2 * nb + 2) * 4, &rc);
-    if (rc) return rc;
-    blk_off8 = blk_len8 + nb + 1;
-    k_sl_len<<<nblk(nslices * 32), 256, 0, st>>>(tiles, nslices, bcs, vperm, csr.offs, csr.items, W, nwin, blk_len8);
-    C2_LAUNCHED(ctx, "k_sl_len");
-    C2_TRY(scan_exclusive(ctx, blk_len8, blk_off8, nb));
-    int32_t tot8;
-    C2_CUDA(ctx, cudaMemcpyAsync(&tot8, blk_off8 + nb, 4, cudaMemcpyDeviceToHost, st));
-    C2_TRY(stream_sync(ctx, "packed size"));
-    packed = (uint4 *)ws_get(ctx, "packed", (size_t)tot8 * 32 * 16 + 16, &rc);
-    if (rc) return rc;
-    k_sl_fill<<<nblk(nslices * 32), 256, 0, st>>>(tiles, nslices, bcs, vperm, csr.offs, csr.items, W, nwin, blk_len8,
-                                                  blk_off8, packed);
-    C2_LAUNCHED(ctx, "k_sl_fill");
+    // cluster-local relabeling (one window of kc+1 words per tile) when the unit bitmaps fit
+    // in shared memory; otherwise windows over the global item range
+    const int32_t nwq = (m + 31) / 32;
+    const size_t rl_smem = (size_t)(5 * nwq + 1 + RL_MAXS) * 4;
+    // (pays off only when the global range needs several windows: a unit then usually fits one)
+    relabel = ctx->relabel && nwin >= 3 && maxs <= (uint32_t)RL_MAXS && rl_smem <= ctx->smem_optin;
+    if (relabel) {
+      blk_len8 = (int32_t *)ws_get(ctx, "blk_len8", (size_t)(2 * nslices + 2) * 4, &rc);
+      if (rc) return rc;
+      blk_off8 = blk_len8 + nslices + 1;
+      k_sl_maxlen<<<nblk(nslices * 32), 256, 0, st>>>(tiles, nslices, bcs, vperm, csr.psize, blk_len8);
+      C2_LAUNCHED(ctx, "k_sl_maxlen");
+      C2_TRY(scan_exclusive(ctx, blk_len8, blk_off8, nslices));
+      int32_t tot8;
+      C2_CUDA(ctx, cudaMemcpyAsync(&tot8, blk_off8 + nslices, 4, cudaMemcpyDeviceToHost, st));
+      C2_TRY(stream_sync(ctx, "packed size"));
+      packed = (uint4 *)ws_get(ctx, "packed", (size_t)tot8 * 32 * 16 + 16, &rc);
+      if (rc) return rc;
+      int *rl = (int *)ws_get(ctx, "relabel_ctr", 16, &rc);
+      if (rc) return rc;
+      C2_CUDA(ctx, cudaMemsetAsync(rl, 0, 16, st));
+      C2_CUDA(ctx, cudaFuncSetAttribute(k_relabel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rl_smem));
+      int rl_occ = 1;
+      C2_CUDA(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&rl_occ, k_relabel, RL_T, rl_smem));
+      k_relabel<<<ctx->num_sms * std::max(rl_occ, 1), RL_T, rl_smem, st>>>(bcs, ncl, vperm, csr.offs, csr.items, nwq, blk_off8, blk_len8,
+                                                     reinterpret_cast<uint16_t *>(packed), rl, rl + 1);
+      C2_LAUNCHED(ctx, "k_relabel");
+      int32_t hkc;
+      C2_CUDA(ctx, cudaMemcpyAsync(&hkc, rl + 1, 4, cudaMemcpyDeviceToHost, st));
+      C2_TRY(stream_sync(ctx, "unit universes"));
+      if (hkc + 1 <= 50000) {
+        nwin = 1;
+        W = hkc;
+      } else {
+        relabel = false;  // a unit universe too large for one window: global windows instead
+      }
+    }
+    if (!relabel) {
+      const int64_t nb = nslices * nwin;
+      blk_len8 = (int32_t *)ws_get(ctx, "blk_len8", (size_t)(2 * nb + 2) * 4, &rc);
+      if (rc) return rc;
+      blk_off8 = blk_len8 + nb + 1;
+      k_sl_len<<<nblk(nslices * 32), 256, 0, st>>>(tiles, nslices, bcs, vperm, csr.offs, csr.items, W, nwin, blk_len8);
+      C2_LAUNCHED(ctx, "k_sl_len");
+      C2_TRY(scan_exclusive(ctx, blk_len8, blk_off8, nb));
+      int32_t tot8;
+      C2_CUDA(ctx, cudaMemcpyAsync(&tot8, blk_off8 + nb, 4, cudaMemcpyDeviceToHost, st));
+      C2_TRY(stream_sync(ctx, "packed size"));
+      packed = (uint4 *)ws_get(ctx, "packed", (size_t)tot8 * 32 * 16 + 16, &rc);
+      if (rc) return rc;
+      k_sl_fill<<<nblk(nslices * 32), 256, 0, st>>>(tiles, nslices, bcs, vperm, csr.offs, csr.items, W, nwin,
+                                                    blk_len8, blk_off8, packed);
+      C2_LAUNCHED(ctx, "k_sl_fill");
+    }
   }
 
   // ---- tile kernel configuration
@@ -1220,7 +1422,7 @@ int local_knn(c2_ctx *ctx, const Csr &csr, int t, const Clusters &cl, int k, c2_
   auto launch_tiles = [&](int64_t lo, int64_t hi, int ci, const c2_cand *seed, c2_cand *dst) -> int {
     if (hi <= lo) return C2_OK;
     TileArgs ta{tiles, lo, hi, counters + ci, bcs, vperm, blk_len8, blk_off8, packed, csr.psize, n, W, nwin, k,
-                seed, dst, ctx->kstats, gscratch, smax, qcap};
+                seed, dst, ctx->kstats, gscratch, smax, qcap, relabel ? 1 : 0};
     int g = (int)std::min<int64_t>(grid, hi - lo);
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     if (ctx->timing) {

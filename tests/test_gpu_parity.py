@@ -357,3 +357,30 @@ def test_errors(ctx):
     with pytest.raises(c2.C2Error) as e:
         c2.build(empty_row, dev(np.asarray([1, 2], np.int32)), k=3, t=2, b=4, N=10, seed=0, ctx=ctx)
     assert e.value.code == c2.C2_EDATA
+
+
+# ------------------------------------------------------------------ Step 2 without relabeling
+@pytest.fixture(scope="module")
+def ctx_win():
+    """A ctx whose Step 2 streams global item windows instead of cluster-local ids
+    (C2_OPT_RELABEL = 0): the second operand layout must give the same bits."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    c = c2.Context(0)
+    c.set_option(c2.OPT_SYNC_CHECK, 1)
+    c.set_option(c2.OPT_RELABEL, 0)
+    yield c
+    c.close()
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_build_random_windows(ctx_win, seed):
+    offs, items, t, b, N, k, hs = random_case(seed)
+    check_build(ctx_win, offs, items, t, b, N, k, hs, mode=seed % 2)
+
+
+@pytest.mark.parametrize("cfg", ["c3", "c4"])
+def test_build_configs_windows(ctx_win, cfg):
+    C = synth.config(cfg)
+    offs, items = synth.generate(cfg)
+    check_build(ctx_win, offs, items, C.t, C.b, C.N, C.k, C.hash_seed)
