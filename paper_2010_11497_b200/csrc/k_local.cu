@@ -134,7 +134,8 @@ struct MixGroup {
 __global__ void k_mix_fill(const uint32_t *__restrict__ sval_small, int64_t nsmall, const int32_t *__restrict__ offsets,
                            const int32_t *__restrict__ ccum, int t, int32_t n, const int32_t *__restrict__ members,
                            const MixGroup *__restrict__ groups, int ngroups, int32_t vp_base,
-                           int32_t *__restrict__ vperm) {
+                           const int32_t *__restrict__ psize, int32_t *__restrict__ vperm,
+                           int32_t *__restrict__ vsize) {
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= nsmall) return;
   int gi = 0;
@@ -150,7 +151,12 @@ __global__ void k_mix_fill(const uint32_t *__restrict__ sval_small, int64_t nsma
   int64_t slice = G.first_slice + q / per;
   int pos = (q % per) << G.cls;
   int32_t *dst = vperm + vp_base + slice * 32 + pos;
-  for (int j = 0; j < s; ++j) dst[j] = members[(int64_t)f * n + st + j];
+  int32_t *dsz = vsize + vp_base + slice * 32 + pos;
+  for (int j = 0; j < s; ++j) {
+    const int32_t v = members[(int64_t)f * n + st + j];
+    dst[j] = v;
+    dsz[j] = psize[v];
+  }
 }
 
 __global__ void k_mix_bc(const MixGroup *__restrict__ groups, int ngroups, int64_t nmix, int64_t nbig, int32_t vp_base,
@@ -185,13 +191,18 @@ __global__ void k_singles(const uint32_t *__restrict__ sval_single, int64_t nsin
 // canonical order: performance only, results do not depend on it).
 __global__ void __launch_bounds__(1024) k_sl_sort(const BigC *__restrict__ bcs, const int32_t *__restrict__ bstart,
                                                   const int32_t *__restrict__ members, int32_t n,
-                                                  const int32_t *__restrict__ psize, int32_t *__restrict__ vperm) {
+                                                  const int32_t *__restrict__ psize, int32_t *__restrict__ vperm,
+                                                  int32_t *__restrict__ vsize) {
   __shared__ uint32_t key[2048];
   const BigC b = bcs[blockIdx.x];
   const int32_t *mem = members + (int64_t)b.f * n + bstart[blockIdx.x];
   int32_t *out = vperm + b.vp_off;
+  int32_t *osz = vsize + b.vp_off;
   if (b.s > 2048) {
-    for (int i = threadIdx.x; i < b.s; i += blockDim.x) out[i] = mem[i];
+    for (int i = threadIdx.x; i < b.s; i += blockDim.x) {
+      out[i] = mem[i];
+      osz[i] = psize[mem[i]];
+    }
     return;
   }
   int P = 64;
@@ -216,90 +227,76 @@ __global__ void __launch_bounds__(1024) k_sl_sort(const BigC *__restrict__ bcs, 
       __syncthreads();
     }
   }
-  for (int i = threadIdx.x; i < b.s; i += blockDim.x) out[i] = mem[key[i] & 0xFFFF];
+  for (int i = threadIdx.x; i < b.s; i += blockDim.x) {
+    const int32_t v = mem[key[i] & 0xFFFF];
+    out[i] = v;
+    osz[i] = psize[v];
+  }
 }
 
-// blk_len8[slice][w] = ceil(max over the slice's 32 lists of |list ∩ window w| / 8)
+// Packed operand lists.  One warp per member position (slice sl, lane slot e): lanes stride the
+// member's sorted items (coalesced reads); each window is a filter pass with ballot compaction.
+// blk_len8[slice][w] = ceil(max over the slice's 32 lists of |list ∩ window w| / 8) (atomicMax;
+// zeroed before).
 __global__ void k_sl_len(const Tile *__restrict__ tiles, int64_t nslices, const BigC *__restrict__ bcs,
                          const int32_t *__restrict__ vperm, const int32_t *__restrict__ offs,
                          const int32_t *__restrict__ items, int32_t W, int nwin, int32_t *__restrict__ blk_len8) {
-  int lane = threadIdx.x & 31;
-  int64_t sl = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  const int64_t g = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t sl = g >> 5;
   if (sl >= nslices) return;
-  Tile T = tiles[sl];
-  BigC b = bcs[T.bc];
-  int vi = T.j * 32 + lane;
-  int cnt[MAX_WIN];
+  const Tile T = tiles[sl];
+  const BigC b = bcs[T.bc];
+  const int vi = T.j * 32 + (int)(g & 31);
+  const int32_t v = vi < b.s ? vperm[b.vp_off + vi] : -1;
+  if (v < 0) return;
+  int c[MAX_WIN];
 #pragma unroll
-  for (int w = 0; w < MAX_WIN; ++w) cnt[w] = 0;
-  int32_t v = vi < b.s ? vperm[b.vp_off + vi] : -1;
-  if (v >= 0) {
-    int32_t p = offs[v], e = offs[v + 1];
-    int32_t bound = W;
-    int w = 0, run = 0;
-    for (; p < e; ++p) {
-      int32_t x = items[p];
-      while (x >= bound) {
+  for (int w = 0; w < MAX_WIN; ++w) c[w] = 0;
+  for (int32_t p0 = offs[v]; p0 < offs[v + 1]; p0 += 32) {
+    const int32_t p = p0 + lane;
+    const int wx = p < offs[v + 1] ? items[p] / W : -1;
 #pragma unroll
-        for (int q = 0; q < MAX_WIN; ++q)
-          if (q == w) cnt[q] = run;
-        ++w;
-        run = 0;
-        bound += W;
-      }
-      ++run;
-    }
-#pragma unroll
-    for (int q = 0; q < MAX_WIN; ++q)
-      if (q == w) cnt[q] = run;
+    for (int w = 0; w < MAX_WIN; ++w)
+      if (w < nwin) c[w] += __popc(__ballot_sync(0xffffffffu, wx == w));
   }
 #pragma unroll
-  for (int q = 0; q < MAX_WIN; ++q) {
-    if (q >= nwin) break;
-    int c = cnt[q];
-#pragma unroll
-    for (int o = 16; o; o >>= 1) c = max(c, __shfl_xor_sync(0xffffffffu, c, o));
-    if (lane == 0) blk_len8[sl * nwin + q] = (c + 7) / 8;
-  }
+  for (int w = 0; w < MAX_WIN; ++w)
+    if (w < nwin && lane == w && c[w]) atomicMax(&blk_len8[sl * nwin + w], (c[w] + 7) / 8);
 }
 
 __global__ void k_sl_fill(const Tile *__restrict__ tiles, int64_t nslices, const BigC *__restrict__ bcs,
                           const int32_t *__restrict__ vperm, const int32_t *__restrict__ offs,
                           const int32_t *__restrict__ items, int32_t W, int nwin,
                           const int32_t *__restrict__ blk_len8, const int32_t *__restrict__ blk_off8,
-                          uint4 *__restrict__ packed) {
-  int lane = threadIdx.x & 31;
-  int64_t sl = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+                          uint16_t *__restrict__ packed16) {
+  const int lane = threadIdx.x & 31;
+  const int64_t g = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t sl = g >> 5;
   if (sl >= nslices) return;
-  Tile T = tiles[sl];
-  BigC b = bcs[T.bc];
-  int vi = T.j * 32 + lane;
-  int32_t p = 0, e = 0;
-  int32_t v = vi < b.s ? vperm[b.vp_off + vi] : -1;
-  if (v >= 0) {
-    p = offs[v];
-    e = offs[v + 1];
-  }
-  const uint32_t pad = (uint32_t)W;
+  const int e = (int)(g & 31);
+  const Tile T = tiles[sl];
+  const BigC b = bcs[T.bc];
+  const int vi = T.j * 32 + e;
+  const int32_t v = vi < b.s ? vperm[b.vp_off + vi] : -1;
+  const int32_t pb = v >= 0 ? offs[v] : 0, pe = v >= 0 ? offs[v + 1] : 0;
   for (int w = 0; w < nwin; ++w) {
-    const int32_t hi = (w + 1) * W, lo = w * W;
-    const int32_t len8 = blk_len8[sl * nwin + w];
-    uint4 *dst = packed + (int64_t)blk_off8[sl * nwin + w] * 32 + lane;
-    for (int32_t g = 0; g < len8; ++g) {
-      uint32_t h[8];
-#pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        int32_t x = p < e ? items[p] : INT32_MAX;
-        bool in = x < hi;
-        h[q] = in ? (uint32_t)(x - lo) : pad;
-        p += in;
-      }
-      dst[(int64_t)g * 32] = make_uint4(h[0] | (h[1] << 16), h[2] | (h[3] << 16), h[4] | (h[5] << 16),
-                                        h[6] | (h[7] << 16));
+    const int32_t lo = w * W;
+    const int32_t len = blk_len8[sl * nwin + w] * 8;
+    uint16_t *dst = packed16 + (int64_t)blk_off8[sl * nwin + w] * 256 + e * 8;
+    int cnt = 0;
+    for (int32_t p0 = pb; p0 < pe; p0 += 32) {
+      const int32_t p = p0 + lane;
+      const int32_t r = p < pe ? items[p] - lo : -1;
+      const bool in = r >= 0 && r < W;
+      const unsigned bal = __ballot_sync(0xffffffffu, in);
+      const int pos = cnt + __popc(bal & ((1u << lane) - 1));
+      if (in) dst[(pos >> 3) * 256 + (pos & 7)] = (uint16_t)r;
+      cnt += __popc(bal);
     }
+    for (int pos = cnt + lane; pos < len; pos += 32) dst[(pos >> 3) * 256 + (pos & 7)] = (uint16_t)W;
   }
 }
-
 
 // ------------------------------------------------------------------ cluster-local relabeling
 // Only items held by >= 2 members of a cluster can contribute to an intersection, so every
@@ -673,6 +670,7 @@ struct TileArgs {
   int *counter;
   const BigC *bcs;
   const int32_t *vperm;
+  const int32_t *vsize;
   const int32_t *blk_len8;
   const int32_t *blk_off8;
   const uint4 *packed;
@@ -686,6 +684,7 @@ struct TileArgs {
   uint32_t *gscratch;   // !SMEM_CNT only: per CTA K8Lay(smax, qcap).words words
   int32_t smax;
   int32_t qcap;         // survivor queue capacity per row
+  int32_t rl_off;       // fused: word offset of the rows' running lists in shared memory
   int relabel;          // 1: items are unit-local ids, the tile's window is [0, B.kc) (nwin == 1)
 };
 
@@ -758,25 +757,48 @@ __global__ void __launch_bounds__(TILE_T, 1) k_local_tile(TileArgs a) {
   const int qcap = a.qcap;
   extern __shared__ __align__(16) uint32_t dyn[];
   uint32_t *M = dyn;  // phase A: W + 1 words, M[W] == 0
-  __shared__ int s_item;
-  __shared__ int32_t s_ru[32];
-  __shared__ uint32_t s_rp[32];
-  __shared__ Cand s_tau[32];
+  // tile descriptors, double-buffered: the next tile's are fetched during this tile's K8
+  __shared__ int64_t s_it[2];
+  __shared__ Tile s_T[2];
+  __shared__ BigC s_B[2];
+  __shared__ int32_t s_ru2[2][32];
+  __shared__ uint32_t s_rp2[2][32];
   __shared__ int s_row;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   for (int i = tid; i < a.W + 1; i += TILE_T) M[i] = 0;
   uint32_t *kb = SMEM_CNT ? dyn : a.gscratch + (int64_t)blockIdx.x * K8Lay(a.smax, qcap).words;  // K8 region
+  Cand *s_run = reinterpret_cast<Cand *>(dyn + a.rl_off);  // fused: the rows' running lists [32][k]
   const int nwin = a.nwin;
   const int kk = a.k;
-  for (;;) {
-    __syncthreads();
-    if (tid == 0) s_item = atomicAdd(a.counter, 1);
-    __syncthreads();
-    const int64_t it = a.lo + s_item;
-    if (it >= a.hi) break;
-    long long ck0 = a.kstats ? clock64() : 0, ck_r1 = 0, ck_scan = 0;
+  // one warp fetches the descriptors of tile item `it` into slot b
+  auto fetch = [&](int b) {
+    int64_t it = 0;
+    if (lane == 0) it = a.lo + atomicAdd(a.counter, 1);
+    it = __shfl_sync(0xffffffffu, it, 0);
+    if (lane == 0) s_it[b] = it;
+    if (it >= a.hi) return;
     const Tile T = a.tiles[it];
     const BigC B = a.bcs[T.bc];
+    if (lane == 0) {
+      s_T[b] = T;
+      s_B[b] = B;
+    }
+    const int r = T.j * 32 + lane;
+    const int32_t u = r < B.s ? a.vperm[B.vp_off + r] : -1;
+    s_ru2[b][lane] = u;
+    s_rp2[b][lane] = u >= 0 ? (uint32_t)a.psize[u] : 0u;
+  };
+  if (warp == 0) fetch(0);
+  int cur = 0;
+  for (;;) {
+    __syncthreads();
+    const int64_t it = s_it[cur];
+    if (it >= a.hi) break;
+    long long ck0 = a.kstats ? clock64() : 0, ck_r1 = 0, ck_scan = 0, ckb = 0, ckp = 0;
+    const Tile T = s_T[cur];
+    const BigC B = s_B[cur];
+    const int32_t *s_ru = s_ru2[cur];
+    const uint32_t *s_rp = s_rp2[cur];
     const int s = B.s;
     const int nsl = (s + 31) >> 5;
     const int r0 = T.j * 32;
@@ -789,35 +811,40 @@ __global__ void __launch_bounds__(TILE_T, 1) k_local_tile(TileArgs a) {
     uint32_t *s_vps = kb + lay.vps;
     Cand *s_q = reinterpret_cast<Cand *>(kb + lay.que);
     if (tid == 0) s_row = 0;
-    if (tid < 32) {
-      int32_t u = tid < nr ? vp[r0 + tid] : -1;
-      s_ru[tid] = u;
-      s_rp[tid] = u >= 0 ? (uint32_t)a.psize[u] : 0u;
-      s_tau[tid] = (u >= 0 && a.seed) ? from_out(a.seed[(int64_t)u * kk + kk - 1]) : sent();
-    }
+    // the rows' running lists (fused mode): loaded now, first used in K8 after phase A
+    if (a.seed)
+      for (int r = warp; r < nr; r += TILE_WARPS) {
+        const int32_t u = s_ru[r];
+        if (u < 0) continue;
+        for (int j = lane; j < kk; j += 32) s_run[r * kk + j] = from_out(a.seed[(int64_t)u * kk + j]);
+      }
     // ================= phase A: counts |P_r ∩ P_v| for the 32 rows x all v of the cluster
     for (int g0 = 0; g0 < nsl; g0 += VPT * TILE_WARPS) {
       Counter<NHI> C[VPT];
 #pragma unroll
       for (int q = 0; q < VPT; ++q) C[q].zero();
       for (int w = 0; w < nwin; ++w) {
-        // ---- build M for window w from the tile's own slice (rows), lane r -> bit r
-        {
-          const int64_t bi = (int64_t)(B.sl_off + T.j) * nwin + w;
-          const int32_t n4 = a.blk_len8[bi] * 32;
-          const uint4 *src = a.packed + (int64_t)a.blk_off8[bi] * 32;
-          for (int gi = tid; gi < n4; gi += TILE_T) {
-            uint4 d = src[gi];
-            uint32_t bit = 1u << (gi & 31);
-            uint32_t xs[8] = {d.x & 0xFFFFu, d.x >> 16, d.y & 0xFFFFu, d.y >> 16,
-                              d.z & 0xFFFFu, d.z >> 16, d.w & 0xFFFFu, d.w >> 16};
+        // ---- build M for window w from the tile's own slice (rows), lane r -> bit r (the first
+        //      16-byte group of every thread is kept for the clear below)
+        const int64_t bi0 = (int64_t)(B.sl_off + T.j) * nwin + w;
+        const int32_t n4r = a.blk_len8[bi0] * 32;
+        const uint4 *srcr = a.packed + (int64_t)a.blk_off8[bi0] * 32;
+        const uint32_t pw = W | (W << 16);
+        const uint4 padv = make_uint4(pw, pw, pw, pw);
+        const uint4 dkeep = tid < n4r ? srcr[tid] : padv;
+        for (int gi = tid; gi < n4r; gi += TILE_T) {
+          const uint4 d = gi == tid ? dkeep : srcr[gi];
+          const uint32_t bit = 1u << (gi & 31);
+          const uint32_t xs[8] = {d.x & 0xFFFFu, d.x >> 16, d.y & 0xFFFFu, d.y >> 16,
+                                  d.z & 0xFFFFu, d.z >> 16, d.w & 0xFFFFu, d.w >> 16};
 #pragma unroll
-            for (int q = 0; q < 8; ++q)
-              if (xs[q] < W) atomicOr(&M[xs[q]], bit);
-          }
+          for (int q = 0; q < 8; ++q)
+            if (xs[q] < W) atomicOr(&M[xs[q]], bit);
         }
         __syncthreads();
-        // ---- probe: each warp streams VPT slices of v lists
+        if (a.kstats) ckb += clock64();
+        // ---- probe: each warp streams VPT slices of v lists, two 16-byte loads per step with
+        //      the next two steps in flight (odd tails padded with the sentinel item W, M[W] = 0)
 #pragma unroll
         for (int q = 0; q < VPT; ++q) {
           const int jj = g0 + q * TILE_WARPS + warp;
@@ -825,15 +852,10 @@ __global__ void __launch_bounds__(TILE_T, 1) k_local_tile(TileArgs a) {
             const int64_t bi = (int64_t)(B.sl_off + jj) * nwin + w;
             const int32_t len8 = a.blk_len8[bi];
             const uint4 *src = a.packed + (int64_t)a.blk_off8[bi] * 32 + lane;
-            // two 16-byte loads per step, the next step's pair prefetched (odd tails padded
-            // with the sentinel item W, whose mask M[W] is 0)
-            const uint32_t pw = W | (W << 16);
-            const uint4 padv = make_uint4(pw, pw, pw, pw);
-            uint4 d0 = len8 > 0 ? __ldg(src) : padv;
-            uint4 d1 = len8 > 1 ? __ldg(src + 32) : padv;
+            auto ld = [&](int32_t p) { return p < len8 ? __ldg(src + (int64_t)p * 32) : padv; };
+            uint4 d0 = ld(0), d1 = ld(1), n0 = ld(2), n1 = ld(3);
             for (int32_t p8 = 0; p8 < len8; p8 += 2) {
-              const uint4 n0 = p8 + 2 < len8 ? __ldg(src + (int64_t)(p8 + 2) * 32) : padv;
-              const uint4 n1 = p8 + 3 < len8 ? __ldg(src + (int64_t)(p8 + 3) * 32) : padv;
+              const uint4 f0 = ld(p8 + 4), f1 = ld(p8 + 5);
               uint32_t m[8];
               masks8(M, d0, m);
               uint32_t e8a = C[q].add8(m);
@@ -842,23 +864,21 @@ __global__ void __launch_bounds__(TILE_T, 1) k_local_tile(TileArgs a) {
               C[q].add16(e8a, e8b);
               d0 = n0;
               d1 = n1;
+              n0 = f0;
+              n1 = f1;
             }
           }
         }
         __syncthreads();
+        if (a.kstats) ckp += clock64();
         // ---- clear M
-        {
-          const int64_t bi = (int64_t)(B.sl_off + T.j) * nwin + w;
-          const int32_t n4 = a.blk_len8[bi] * 32;
-          const uint4 *src = a.packed + (int64_t)a.blk_off8[bi] * 32;
-          for (int gi = tid; gi < n4; gi += TILE_T) {
-            uint4 d = src[gi];
-            uint32_t xs[8] = {d.x & 0xFFFFu, d.x >> 16, d.y & 0xFFFFu, d.y >> 16,
-                              d.z & 0xFFFFu, d.z >> 16, d.w & 0xFFFFu, d.w >> 16};
+        for (int gi = tid; gi < n4r; gi += TILE_T) {
+          const uint4 d = gi == tid ? dkeep : srcr[gi];
+          const uint32_t xs[8] = {d.x & 0xFFFFu, d.x >> 16, d.y & 0xFFFFu, d.y >> 16,
+                                  d.z & 0xFFFFu, d.z >> 16, d.w & 0xFFFFu, d.w >> 16};
 #pragma unroll
-            for (int q = 0; q < 8; ++q)
-              if (xs[q] < W) M[xs[q]] = 0;
-          }
+          for (int q = 0; q < 8; ++q)
+            if (xs[q] < W) M[xs[q]] = 0;
         }
         __syncthreads();
       }
@@ -890,15 +910,19 @@ __global__ void __launch_bounds__(TILE_T, 1) k_local_tile(TileArgs a) {
     {
       const int s4 = (s + 3) & ~3;
       for (int i = tid; i < s4; i += TILE_T) {
-        int32_t v = i < s ? vp[i] : INT32_MAX;
-        s_vid[i] = v;
-        s_vps[i] = (v >= 0 && v != INT32_MAX) ? (uint32_t)a.psize[v] : 0u;
+        s_vid[i] = i < s ? vp[i] : INT32_MAX;
+        s_vps[i] = i < s ? (uint32_t)a.vsize[B.vp_off + i] : 0u;
       }
     }
     __syncthreads();
     // ================= K8: exact top-k per row, one warp per row (no CTA barrier inside)
+    if (warp == 0) fetch(cur ^ 1);  // next tile's descriptors, hidden behind this K8
     const int slot = B.slot;  // mixed slice: candidates only inside the row's own slot group
+    uint32_t *zq = nullptr;  // queue words the warp's previous row wrote (re-zeroed: M alias)
+    int zn = 0;
     for (;;) {  // rows taken dynamically: their costs differ a lot
+      for (int i = lane; i < zn; i += 32) zq[i] = 0u;
+      zn = 0;
       int r = 0;
       if (lane == 0) r = atomicAdd(&s_row, 1);
       r = __shfl_sync(0xffffffffu, r, 0);
@@ -909,7 +933,7 @@ __global__ void __launch_bounds__(TILE_T, 1) k_local_tile(TileArgs a) {
       const int selfr = slot ? r : r0 + r;
       const uint16_t *cr = cnt + r * lay.RS;
       Cand *qr = s_q + r * qcap;
-      const Cand tau = s_tau[r];
+      const Cand tau = a.seed ? s_run[r * kk + kk - 1] : sent();
       // survivors of T (strictly better than tau, not worse than a round-1 bound) -> qr by
       // ballot compaction; returns their number (only the first qcap are stored)
       auto scan = [&](const Ref &T) -> int {
@@ -955,6 +979,7 @@ __global__ void __launch_bounds__(TILE_T, 1) k_local_tile(TileArgs a) {
       // k-th best of the first 64*KS queue entries (all distinct real candidates): a valid
       // lower bound of the row's k-th best
       auto kth_of_queue = [&]() -> Ref {
+        if (a.kstats && lane == 0) atomicAdd(&a.kstats[15], 1ull);
         KC e[2 * KS];
 #pragma unroll
         for (int j = 0; j < 2 * KS; ++j) e[j] = to_kc(qr[32 * j + lane]);
@@ -1008,16 +1033,22 @@ __global__ void __launch_bounds__(TILE_T, 1) k_local_tile(TileArgs a) {
         ckr = c;
       }
       int m = scan(T);
+      zq = reinterpret_cast<uint32_t *>(qr);
+      zn = 2 * min(m, qcap);
+      if (a.kstats && lane == 0) atomicAdd(&a.kstats[16 + min(m, 300) / 20], 1ull);
       if (m > qcap && !slot && !r1) {
+        if (a.kstats && lane == 0) atomicAdd(&a.kstats[14], 1ull);
         r1 = true;
         round1(T);
         m = scan(T);
+        zn = max(zn, 2 * min(m, qcap));
       }
       int rescans = 0;
       for (; rescans < 2 && m > qcap; ++rescans) {
         T = kth_of_queue();
         __syncwarp();
         m = scan(T);
+        zn = max(zn, 2 * min(m, qcap));
       }
       // shrink a long queue in place: keep the entries not worse than the k-th best of its
       // first 64*KS (stops when that makes no progress: massive ties)
@@ -1058,9 +1089,10 @@ __global__ void __launch_bounds__(TILE_T, 1) k_local_tile(TileArgs a) {
         // few survivors: insert them one by one into the running list (duplicates skipped)
         KC S[KS];
 #pragma unroll
-        for (int j = 0; j < KS; ++j) S[j] = to_kc((32 * j + lane < kk) ? from_out(dst[32 * j + lane]) : sent());
+        for (int j = 0; j < KS; ++j) S[j] = to_kc((32 * j + lane < kk) ? s_run[r * kk + 32 * j + lane] : sent());
+        const KC xk = to_kc(lane < m ? qr[lane] : sent());  // all survivors' keys at once
         for (int j = 0; j < m; ++j) {
-          const KC x = to_kc(qr[j]);
+          const KC x = shfl_e(xk, j);
           bool dup = false;
 #pragma unroll
           for (int jj = 0; jj < KS; ++jj) dup |= S[jj].k == x.k;
@@ -1127,7 +1159,7 @@ __global__ void __launch_bounds__(TILE_T, 1) k_local_tile(TileArgs a) {
       // merge with the running list S (best first): bitonic sequence L(first k) ++ reverse(S)
       KC S[KS];
 #pragma unroll
-      for (int j = 0; j < KS; ++j) S[j] = to_kc((32 * j + lane < kk) ? from_out(dst[32 * j + lane]) : sent());
+      for (int j = 0; j < KS; ++j) S[j] = to_kc((32 * j + lane < kk) ? s_run[r * kk + 32 * j + lane] : sent());
       KC mm[2 * KS];
 #pragma unroll
       for (int j = 0; j < KS; ++j) mm[j] = (32 * j + lane < kk) ? L[j] : KC{0ull, 1u << 16};
@@ -1159,14 +1191,30 @@ __global__ void __launch_bounds__(TILE_T, 1) k_local_tile(TileArgs a) {
       atomicAdd(&a.kstats[11], (unsigned long long)ck_scan);       // K8 scan + queue shrink
       atomicAdd(&a.kstats[12], (unsigned long long)(ck2 - ck1 - ck_r1 - ck_scan));  // K8 rest
       atomicAdd(&a.kstats[13], (unsigned long long)(ck3 - ck2));   // wait at the K8 barrier
+      if (warp == 0) {  // tile wall cycles by cluster size class: mixed, 33-256, 257-1024, >1024
+        const int cls = B.slot ? 0 : s <= 256 ? 1 : s <= 1024 ? 2 : 3;
+        atomicAdd(&a.kstats[32 + cls], (unsigned long long)(ck3 - ck0));
+        atomicAdd(&a.kstats[36 + cls], 1ull);
+        if (cls == 0) {  // mixed tiles: head+build / probe / clear+transpose+stage / K8 / wait
+          const long long tb = ckb - nwin * ck0;           // sum over windows of (build end - tile start)
+          atomicAdd(&a.kstats[40], (unsigned long long)(ckb - ck0 * nwin));
+          atomicAdd(&a.kstats[41], (unsigned long long)(ckp - ckb));
+          atomicAdd(&a.kstats[42], (unsigned long long)(ck1 - ck0) - (unsigned long long)(ckp - ckb));
+          atomicAdd(&a.kstats[43], (unsigned long long)(ck2 - ck1));
+          atomicAdd(&a.kstats[44], (unsigned long long)(ck3 - ck2));
+          (void)tb;
+        }
+      }
     }
     // restore the all-zero M words the K8 region overwrote
+    // (queues were re-zeroed row by row; here the counts and member arrays)
     if (SMEM_CNT) {
-      const int dw = min(lay.words, a.W + 1);
+      const int dw = min(lay.que, a.W + 1);
       uint4 *z = reinterpret_cast<uint4 *>(dyn);
       for (int i = tid; i < dw / 4; i += TILE_T) z[i] = make_uint4(0, 0, 0, 0);
       for (int i = (dw & ~3) + tid; i < dw; i += TILE_T) dyn[i] = 0;
     }
+    cur ^= 1;
   }
 }
 
@@ -1278,7 +1326,7 @@ int local_knn(c2_ctx *ctx, const Csr &csr, int t, const Clusters &cl, int k, c2_
   const int64_t nslices = nbigtiles + nmix;
   BigC *bcs = nullptr;
   Tile *tiles = nullptr;
-  int32_t *vperm = nullptr, *blk_len8 = nullptr, *blk_off8 = nullptr;
+  int32_t *vperm = nullptr, *vsize = nullptr, *blk_len8 = nullptr, *blk_off8 = nullptr;
   uint4 *packed = nullptr;
   bool relabel = false;
   const int32_t m = csr.max_item + 1;
@@ -1305,12 +1353,13 @@ int local_knn(c2_ctx *ctx, const Csr &csr, int t, const Clusters &cl, int k, c2_
       C2_TRY(stream_sync(ctx, "big cluster sizes"));
       nv_big = h1;
     }
-    vperm = (int32_t *)ws_get(ctx, "vperm", (size_t)(nv_big + nmix * 32 + 1) * 4, &rc);
+    vperm = (int32_t *)ws_get(ctx, "vperm", (size_t)(nv_big + nmix * 32 + 1) * 4 * 2, &rc);
     if (rc) return rc;
+    vsize = vperm + (nv_big + nmix * 32 + 1);  // |P_v| of every vperm entry (0 for holes)
     if (nbig > 0) {
       k_bc_fill<<<nblk(nbig), 256, 0, st>>>(sval, nbig, cl.offsets, ccum, t, n, vp_scan, sl_scan, bcs, tiles, bstart);
       C2_LAUNCHED(ctx, "k_bc_fill");
-      k_sl_sort<<<(unsigned)nbig, 1024, 0, st>>>(bcs, bstart, cl.members, n, csr.psize, vperm);
+      k_sl_sort<<<(unsigned)nbig, 1024, 0, st>>>(bcs, bstart, cl.members, n, csr.psize, vperm, vsize);
       C2_LAUNCHED(ctx, "k_sl_sort");
     }
     if (nmix > 0) {
@@ -1319,8 +1368,9 @@ int local_knn(c2_ctx *ctx, const Csr &csr, int t, const Clusters &cl, int k, c2_
       C2_CUDA(ctx, cudaMemcpyAsync(dgroups, groups.data(), groups.size() * sizeof(MixGroup), cudaMemcpyHostToDevice,
                                    st));
       C2_CUDA(ctx, cudaMemsetAsync(vperm + nv_big, 0xFF, (size_t)nmix * 32 * 4, st));
+      C2_CUDA(ctx, cudaMemsetAsync(vsize + nv_big, 0, (size_t)nmix * 32 * 4, st));
       k_mix_fill<<<nblk(nsmall), 256, 0, st>>>(sval + nbig, nsmall, cl.offsets, ccum, t, n, cl.members, dgroups,
-                                               (int)groups.size(), (int32_t)nv_big, vperm);
+                                               (int)groups.size(), (int32_t)nv_big, csr.psize, vperm, vsize);
       C2_LAUNCHED(ctx, "k_mix_fill");
       k_mix_bc<<<nblk(nmix), 256, 0, st>>>(dgroups, (int)groups.size(), nmix, nbig, (int32_t)nv_big, nbigtiles, bcs,
                                            tiles);
@@ -1368,7 +1418,9 @@ int local_knn(c2_ctx *ctx, const Csr &csr, int t, const Clusters &cl, int k, c2_
       blk_len8 = (int32_t *)ws_get(ctx, "blk_len8", (size_t)(2 * nb + 2) * 4, &rc);
       if (rc) return rc;
       blk_off8 = blk_len8 + nb + 1;
-      k_sl_len<<<nblk(nslices * 32), 256, 0, st>>>(tiles, nslices, bcs, vperm, csr.offs, csr.items, W, nwin, blk_len8);
+      C2_CUDA(ctx, cudaMemsetAsync(blk_len8, 0, (size_t)(nb + 1) * 4, st));
+      k_sl_len<<<nblk(nslices * 32 * 32), 256, 0, st>>>(tiles, nslices, bcs, vperm, csr.offs, csr.items, W, nwin,
+                                                        blk_len8);
       C2_LAUNCHED(ctx, "k_sl_len");
       C2_TRY(scan_exclusive(ctx, blk_len8, blk_off8, nb));
       int32_t tot8;
@@ -1376,8 +1428,8 @@ int local_knn(c2_ctx *ctx, const Csr &csr, int t, const Clusters &cl, int k, c2_
       C2_TRY(stream_sync(ctx, "packed size"));
       packed = (uint4 *)ws_get(ctx, "packed", (size_t)tot8 * 32 * 16 + 16, &rc);
       if (rc) return rc;
-      k_sl_fill<<<nblk(nslices * 32), 256, 0, st>>>(tiles, nslices, bcs, vperm, csr.offs, csr.items, W, nwin,
-                                                    blk_len8, blk_off8, packed);
+      k_sl_fill<<<nblk(nslices * 32 * 32), 256, 0, st>>>(tiles, nslices, bcs, vperm, csr.offs, csr.items, W, nwin,
+                                                         blk_len8, blk_off8, reinterpret_cast<uint16_t *>(packed));
       C2_LAUNCHED(ctx, "k_sl_fill");
     }
   }
@@ -1386,6 +1438,7 @@ int local_knn(c2_ctx *ctx, const Csr &csr, int t, const Clusters &cl, int k, c2_
   TileKernel tk = nullptr;
   int grid = 0;
   int qcap = 64;
+  int32_t rl_off = 0;
   size_t smem = 0;
   uint32_t *gscratch = nullptr;
   int *counters = nullptr;
@@ -1398,13 +1451,16 @@ int local_knn(c2_ctx *ctx, const Csr &csr, int t, const Clusters &cl, int k, c2_
     // survivor queue per row: 256 entries where shared memory allows, at least 64*KS
     const int qmin = k <= 32 ? 64 : 128;
     qcap = 256;
-    while (qcap > qmin && (size_t)K8Lay(smax, qcap).words * 4 > ctx->smem_optin) qcap -= 64;
+    const size_t budget = ctx->smem_optin - 2048;  // minus the kernel's static shared memory
+    const size_t rlw = fused ? (size_t)64 * k : 0;  // the rows' running lists (Cand = 2 words)
+    while (qcap > qmin && ((size_t)K8Lay(smax, qcap).words + rlw) * 4 > budget) qcap -= 64;
     const int k8w = K8Lay(smax, qcap).words;
     const size_t mw = (size_t)((W + 4) & ~3);
     // counts in shared memory (aliased onto M) when one g0 group covers the largest cluster
     // and the K8 region fits; else a per-CTA global scratch region
-    const bool smem_cnt = max_sl <= 4 * TILE_WARPS && (size_t)k8w * 4 <= ctx->smem_optin;
-    smem = (smem_cnt ? std::max(mw, (size_t)k8w) : mw) * 4;
+    const bool smem_cnt = max_sl <= 4 * TILE_WARPS && ((size_t)k8w + rlw) * 4 <= budget;
+    rl_off = (int32_t)(((smem_cnt ? std::max(mw, (size_t)k8w) : mw) + 3) & ~(size_t)3);
+    smem = ((size_t)rl_off + rlw) * 4;
     tk = pick_tile(nhi, vpt, k, smem_cnt);
     C2_CUDA(ctx, cudaFuncSetAttribute(tk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int occ = 0;
@@ -1421,8 +1477,8 @@ int local_knn(c2_ctx *ctx, const Csr &csr, int t, const Clusters &cl, int k, c2_
   }
   auto launch_tiles = [&](int64_t lo, int64_t hi, int ci, const c2_cand *seed, c2_cand *dst) -> int {
     if (hi <= lo) return C2_OK;
-    TileArgs ta{tiles, lo, hi, counters + ci, bcs, vperm, blk_len8, blk_off8, packed, csr.psize, n, W, nwin, k,
-                seed, dst, ctx->kstats, gscratch, smax, qcap, relabel ? 1 : 0};
+    TileArgs ta{tiles, lo, hi, counters + ci, bcs, vperm, vsize, blk_len8, blk_off8, packed, csr.psize, n, W, nwin, k,
+                seed, dst, ctx->kstats, gscratch, smax, qcap, rl_off, relabel ? 1 : 0};
     int g = (int)std::min<int64_t>(grid, hi - lo);
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     if (ctx->timing) {

@@ -10,7 +10,7 @@ C = synth.config(name)
 offs, items = synth.generate(name)
 d_o, d_i = torch.from_numpy(offs).cuda(), torch.from_numpy(items).cuda()
 ctx = c2.Context(0)
-ks = torch.zeros(16, dtype=torch.int64, device="cuda")
+ks = torch.zeros(48, dtype=torch.int64, device="cuda")
 c2.build(d_o, d_i, k=C.k, t=C.t, b=C.b, N=C.N, seed=C.hash_seed, ctx=ctx)
 ctx.set_option(c2.OPT_KSTATS, ks.data_ptr())
 c2.build(d_o, d_i, k=C.k, t=C.t, b=C.b, N=C.N, seed=C.hash_seed, ctx=ctx)
@@ -21,3 +21,11 @@ print(f"{name}: rows {k[0]} nq==0 {k[1]/k[0]:.3f} mean nq {k[2]/k[0]:.2f} nq>32K
 tot = sum(k[9:14])
 print("  warp-cycles: " + " ".join(f"{n} {v / tot * 100:.1f}%" for n, v in
       zip(["phaseA", "round1", "scan", "k8-rest", "k8-wait"], k[9:14])))
+print(f"  round1-after-overflow rows {k[14]}  kth_of_queue calls {k[15]}")
+print("  first-scan m histogram (bins of 20): " + " ".join(str(x) for x in k[16:32]))
+tt = sum(k[32:36]) or 1
+print("  tile cycles by class (share, tiles, mean cycles): " + " ".join(
+    f"{n}: {k[32 + i] / tt * 100:.1f}% {k[36 + i]} {k[32 + i] / max(k[36 + i], 1):.0f}" for i, n in enumerate(["mixed", "33-256", "257-1024", ">1024"])))
+mt = max(k[36], 1)
+print(f"  mixed tile (warp 0, mean cycles): sum(build ends - start) {k[40] / mt:.0f}  probe {k[41] / mt:.0f}  "
+      f"phaseA-other {k[42] / mt:.0f}  K8 {k[43] / mt:.0f}  wait {k[44] / mt:.0f}")
