@@ -42,6 +42,15 @@ struct Tile {
   int32_t bc, j;
 };
 
+// cp.async (sm_80+ async global->shared copies; completion by cp.async.wait_all)
+__device__ __forceinline__ void cp_async8(void *smem, const void *gmem) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"((unsigned)__cvta_generic_to_shared(smem)), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((unsigned)__cvta_generic_to_shared(smem)), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
 constexpr int TILE_T = 512;
 constexpr int TILE_WARPS = TILE_T / 32;
 constexpr int MAX_WIN = 16;
@@ -685,6 +694,7 @@ struct TileArgs {
   int32_t smax;
   int32_t qcap;         // survivor queue capacity per row
   int32_t rl_off;       // fused: word offset of the rows' running lists in shared memory
+  int32_t stg_off, stg_cap;  // staging buffer (word offset, capacity in 16-byte groups; 0: off)
   int relabel;          // 1: items are unit-local ids, the tile's window is [0, B.kc) (nwin == 1)
 };
 
@@ -763,11 +773,14 @@ __global__ void __launch_bounds__(TILE_T, 1) k_local_tile(TileArgs a) {
   __shared__ BigC s_B[2];
   __shared__ int32_t s_ru2[2][32];
   __shared__ uint32_t s_rp2[2][32];
+  __shared__ int32_t s_bl[2][MAX_WIN], s_bo[2][MAX_WIN], s_so[2][MAX_WIN];  // rows' blocks; staged offsets
+  __shared__ int s_stg[2];  // 1: the rows' blocks of every window are staged in stg
   __shared__ int s_row;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   for (int i = tid; i < a.W + 1; i += TILE_T) M[i] = 0;
   uint32_t *kb = SMEM_CNT ? dyn : a.gscratch + (int64_t)blockIdx.x * K8Lay(a.smax, qcap).words;  // K8 region
-  Cand *s_run = reinterpret_cast<Cand *>(dyn + a.rl_off);  // fused: the rows' running lists [32][k]
+  c2_cand *s_run = reinterpret_cast<c2_cand *>(dyn + a.rl_off);  // fused: the rows' running lists [32][k]
+  uint4 *stg = reinterpret_cast<uint4 *>(dyn + a.stg_off);       // staged rows' blocks of the next tile
   const int nwin = a.nwin;
   const int kk = a.k;
   // one warp fetches the descriptors of tile item `it` into slot b
@@ -787,10 +800,37 @@ __global__ void __launch_bounds__(TILE_T, 1) k_local_tile(TileArgs a) {
     const int32_t u = r < B.s ? a.vperm[B.vp_off + r] : -1;
     s_ru2[b][lane] = u;
     s_rp2[b][lane] = u >= 0 ? (uint32_t)a.psize[u] : 0u;
+    // the rows' packed blocks: copied to the staging buffer now (async), used by the build and
+    // the probe of the tile's own slice
+    const int64_t sb = (int64_t)(B.sl_off + T.j) * nwin;
+    const int32_t bl = lane < nwin ? a.blk_len8[sb + lane] : 0;
+    const int32_t bo = lane < nwin ? a.blk_off8[sb + lane] : 0;
+    int32_t incl = bl * 32;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    const int32_t tot = __shfl_sync(0xffffffffu, incl, 31);
+    const bool staged = tot <= a.stg_cap;
+    if (lane < nwin) {
+      s_bl[b][lane] = bl;
+      s_bo[b][lane] = bo;
+      s_so[b][lane] = incl - bl * 32;
+    }
+    if (lane == 0) s_stg[b] = staged ? 1 : 0;
+    if (staged)
+      for (int w = 0; w < nwin; ++w) {
+        const int32_t n4 = __shfl_sync(0xffffffffu, bl, w) * 32;
+        const int32_t so = __shfl_sync(0xffffffffu, incl - bl * 32, w);
+        const uint4 *g = a.packed + (int64_t)__shfl_sync(0xffffffffu, bo, w) * 32;
+        for (int i = lane; i < n4; i += 32) cp_async16(stg + so + i, g + i);
+      }
   };
   if (warp == 0) fetch(0);
   int cur = 0;
   for (;;) {
+    cp_async_wait_all();
     __syncthreads();
     const int64_t it = s_it[cur];
     if (it >= a.hi) break;
@@ -816,7 +856,7 @@ __global__ void __launch_bounds__(TILE_T, 1) k_local_tile(TileArgs a) {
       for (int r = warp; r < nr; r += TILE_WARPS) {
         const int32_t u = s_ru[r];
         if (u < 0) continue;
-        for (int j = lane; j < kk; j += 32) s_run[r * kk + j] = from_out(a.seed[(int64_t)u * kk + j]);
+        for (int j = lane; j < kk; j += 32) cp_async8(s_run + r * kk + j, a.seed + (int64_t)u * kk + j);
       }
     // ================= phase A: counts |P_r ∩ P_v| for the 32 rows x all v of the cluster
     for (int g0 = 0; g0 < nsl; g0 += VPT * TILE_WARPS) {
@@ -826,9 +866,9 @@ __global__ void __launch_bounds__(TILE_T, 1) k_local_tile(TileArgs a) {
       for (int w = 0; w < nwin; ++w) {
         // ---- build M for window w from the tile's own slice (rows), lane r -> bit r (the first
         //      16-byte group of every thread is kept for the clear below)
-        const int64_t bi0 = (int64_t)(B.sl_off + T.j) * nwin + w;
-        const int32_t n4r = a.blk_len8[bi0] * 32;
-        const uint4 *srcr = a.packed + (int64_t)a.blk_off8[bi0] * 32;
+        const bool stgd = s_stg[cur] != 0;
+        const int32_t n4r = s_bl[cur][w] * 32;
+        const uint4 *srcr = stgd ? stg + s_so[cur][w] : a.packed + (int64_t)s_bo[cur][w] * 32;
         const uint32_t pw = W | (W << 16);
         const uint4 padv = make_uint4(pw, pw, pw, pw);
         const uint4 dkeep = tid < n4r ? srcr[tid] : padv;
@@ -850,9 +890,10 @@ __global__ void __launch_bounds__(TILE_T, 1) k_local_tile(TileArgs a) {
           const int jj = g0 + q * TILE_WARPS + warp;
           if (jj < nsl) {
             const int64_t bi = (int64_t)(B.sl_off + jj) * nwin + w;
-            const int32_t len8 = a.blk_len8[bi];
-            const uint4 *src = a.packed + (int64_t)a.blk_off8[bi] * 32 + lane;
-            auto ld = [&](int32_t p) { return p < len8 ? __ldg(src + (int64_t)p * 32) : padv; };
+            const bool own = stgd && jj == T.j;  // the tile's own slice: staged
+            const int32_t len8 = own ? s_bl[cur][w] : a.blk_len8[bi];
+            const uint4 *src = (own ? stg + s_so[cur][w] : a.packed + (int64_t)a.blk_off8[bi] * 32) + lane;
+            auto ld = [&](int32_t p) { return p < len8 ? src[(int64_t)p * 32] : padv; };
             uint4 d0 = ld(0), d1 = ld(1), n0 = ld(2), n1 = ld(3);
             for (int32_t p8 = 0; p8 < len8; p8 += 2) {
               const uint4 f0 = ld(p8 + 4), f1 = ld(p8 + 5);
@@ -914,13 +955,19 @@ __global__ void __launch_bounds__(TILE_T, 1) k_local_tile(TileArgs a) {
         s_vps[i] = i < s ? (uint32_t)a.vsize[B.vp_off + i] : 0u;
       }
     }
+    cp_async_wait_all();  // the running lists
     __syncthreads();
     // ================= K8: exact top-k per row, one warp per row (no CTA barrier inside)
     if (warp == 0) fetch(cur ^ 1);  // next tile's descriptors, hidden behind this K8
     const int slot = B.slot;  // mixed slice: candidates only inside the row's own slot group
     uint32_t *zq = nullptr;  // queue words the warp's previous row wrote (re-zeroed: M alias)
     int zn = 0;
+    long long tfin = 0, acc_sel = 0, acc_fin = 0, nrow_b = 0;  // kstats: big tiles' per-row split
     for (;;) {  // rows taken dynamically: their costs differ a lot
+      if (a.kstats && tfin) {
+        acc_fin += clock64() - tfin;
+        tfin = 0;
+      }
       for (int i = lane; i < zn; i += 32) zq[i] = 0u;
       zn = 0;
       int r = 0;
@@ -933,7 +980,7 @@ __global__ void __launch_bounds__(TILE_T, 1) k_local_tile(TileArgs a) {
       const int selfr = slot ? r : r0 + r;
       const uint16_t *cr = cnt + r * lay.RS;
       Cand *qr = s_q + r * qcap;
-      const Cand tau = a.seed ? s_run[r * kk + kk - 1] : sent();
+      const Cand tau = a.seed ? from_out(s_run[r * kk + kk - 1]) : sent();
       // survivors of T (strictly better than tau, not worse than a round-1 bound) -> qr by
       // ballot compaction; returns their number (only the first qcap are stored)
       auto scan = [&](const Ref &T) -> int {
@@ -987,6 +1034,7 @@ __global__ void __launch_bounds__(TILE_T, 1) k_local_tile(TileArgs a) {
         return make_ref(kc_cand(warp_get<2 * KS>(e, kk - 1)), prr, true);
       };
       long long ckr = a.kstats ? clock64() : 0;
+      const long long ckr0 = ckr;
       // round 1: every lane's best R1 candidates of its share; T_r = the k-th best of the
       // 32*R1 tops (any k distinct candidates bound the row's k-th best from below)
       auto round1 = [&](Ref &T) {
@@ -1025,7 +1073,7 @@ __global__ void __launch_bounds__(TILE_T, 1) k_local_tile(TileArgs a) {
       Ref T = make_ref(tau, prr, false);
       // rows without a running list yet (tau = sentinel) whose candidates cannot all be queued
       // start with round 1; rows whose tau lets too many through get it after the first scan
-      bool r1 = !slot && !is_real(tau) && s - 1 > qcap;
+      bool r1 = !slot && !is_real(tau) && s - 1 > 64 * KS;
       if (r1) round1(T);
       if (a.kstats) {
         const long long c = clock64();
@@ -1036,7 +1084,7 @@ __global__ void __launch_bounds__(TILE_T, 1) k_local_tile(TileArgs a) {
       zq = reinterpret_cast<uint32_t *>(qr);
       zn = 2 * min(m, qcap);
       if (a.kstats && lane == 0) atomicAdd(&a.kstats[16 + min(m, 300) / 20], 1ull);
-      if (m > qcap && !slot && !r1) {
+      if (m > 64 * KS && !slot && !r1) {
         if (a.kstats && lane == 0) atomicAdd(&a.kstats[14], 1ull);
         r1 = true;
         round1(T);
@@ -1070,7 +1118,15 @@ __global__ void __launch_bounds__(TILE_T, 1) k_local_tile(TileArgs a) {
         if (w == m) break;
         m = w;
       }
-      if (a.kstats) ck_scan += clock64() - ckr;
+      if (a.kstats) {
+        const long long c = clock64();
+        ck_scan += c - ckr;
+        if (s > 1024) {
+          acc_sel += c - ckr0;
+          tfin = c;
+          ++nrow_b;
+        }
+      }
       if (a.kstats && lane == 0) {
         atomicAdd(&a.kstats[0], 1ull);
         atomicAdd(&a.kstats[1], m == 0 ? 1ull : 0ull);
@@ -1089,7 +1145,7 @@ __global__ void __launch_bounds__(TILE_T, 1) k_local_tile(TileArgs a) {
         // few survivors: insert them one by one into the running list (duplicates skipped)
         KC S[KS];
 #pragma unroll
-        for (int j = 0; j < KS; ++j) S[j] = to_kc((32 * j + lane < kk) ? s_run[r * kk + 32 * j + lane] : sent());
+        for (int j = 0; j < KS; ++j) S[j] = to_kc((32 * j + lane < kk) ? from_out(s_run[r * kk + 32 * j + lane]) : sent());
         const KC xk = to_kc(lane < m ? qr[lane] : sent());  // all survivors' keys at once
         for (int j = 0; j < m; ++j) {
           const KC x = shfl_e(xk, j);
@@ -1159,7 +1215,7 @@ __global__ void __launch_bounds__(TILE_T, 1) k_local_tile(TileArgs a) {
       // merge with the running list S (best first): bitonic sequence L(first k) ++ reverse(S)
       KC S[KS];
 #pragma unroll
-      for (int j = 0; j < KS; ++j) S[j] = to_kc((32 * j + lane < kk) ? s_run[r * kk + 32 * j + lane] : sent());
+      for (int j = 0; j < KS; ++j) S[j] = to_kc((32 * j + lane < kk) ? from_out(s_run[r * kk + 32 * j + lane]) : sent());
       KC mm[2 * KS];
 #pragma unroll
       for (int j = 0; j < KS; ++j) mm[j] = (32 * j + lane < kk) ? L[j] : KC{0ull, 1u << 16};
@@ -1195,14 +1251,18 @@ __global__ void __launch_bounds__(TILE_T, 1) k_local_tile(TileArgs a) {
         const int cls = B.slot ? 0 : s <= 256 ? 1 : s <= 1024 ? 2 : 3;
         atomicAdd(&a.kstats[32 + cls], (unsigned long long)(ck3 - ck0));
         atomicAdd(&a.kstats[36 + cls], 1ull);
-        if (cls == 0) {  // mixed tiles: head+build / probe / clear+transpose+stage / K8 / wait
-          const long long tb = ckb - nwin * ck0;           // sum over windows of (build end - tile start)
-          atomicAdd(&a.kstats[40], (unsigned long long)(ckb - ck0 * nwin));
-          atomicAdd(&a.kstats[41], (unsigned long long)(ckp - ckb));
-          atomicAdd(&a.kstats[42], (unsigned long long)(ck1 - ck0) - (unsigned long long)(ckp - ckb));
-          atomicAdd(&a.kstats[43], (unsigned long long)(ck2 - ck1));
-          atomicAdd(&a.kstats[44], (unsigned long long)(ck3 - ck2));
-          (void)tb;
+        if (nrow_b) {
+          atomicAdd(&a.kstats[60], (unsigned long long)acc_sel);
+          atomicAdd(&a.kstats[61], (unsigned long long)acc_fin);
+          atomicAdd(&a.kstats[62], (unsigned long long)nrow_b);
+        }
+        {  // per class: build (window sum) / probe / rest of phase A / K8 / wait
+          unsigned long long *kc5 = a.kstats + 40 + 5 * cls;
+          atomicAdd(&kc5[0], (unsigned long long)(ckb - ck0 * nwin));
+          atomicAdd(&kc5[1], (unsigned long long)(ckp - ckb));
+          atomicAdd(&kc5[2], (unsigned long long)(ck1 - ck0) - (unsigned long long)(ckp - ckb));
+          atomicAdd(&kc5[3], (unsigned long long)(ck2 - ck1));
+          atomicAdd(&kc5[4], (unsigned long long)(ck3 - ck2));
         }
       }
     }
@@ -1438,7 +1498,7 @@ int local_knn(c2_ctx *ctx, const Csr &csr, int t, const Clusters &cl, int k, c2_
   TileKernel tk = nullptr;
   int grid = 0;
   int qcap = 64;
-  int32_t rl_off = 0;
+  int32_t rl_off = 0, stg_off = 0, stg_cap = 0;
   size_t smem = 0;
   uint32_t *gscratch = nullptr;
   int *counters = nullptr;
@@ -1453,14 +1513,18 @@ int local_knn(c2_ctx *ctx, const Csr &csr, int t, const Clusters &cl, int k, c2_
     qcap = 256;
     const size_t budget = ctx->smem_optin - 2048;  // minus the kernel's static shared memory
     const size_t rlw = fused ? (size_t)64 * k : 0;  // the rows' running lists (Cand = 2 words)
-    while (qcap > qmin && ((size_t)K8Lay(smax, qcap).words + rlw) * 4 > budget) qcap -= 64;
+    const size_t stgw = 4096;  // staging of the next tile's row blocks: at least 16 KB
+    while (qcap > qmin && ((size_t)K8Lay(smax, qcap).words + rlw + stgw) * 4 > budget) qcap -= 64;
     const int k8w = K8Lay(smax, qcap).words;
     const size_t mw = (size_t)((W + 4) & ~3);
     // counts in shared memory (aliased onto M) when one g0 group covers the largest cluster
     // and the K8 region fits; else a per-CTA global scratch region
     const bool smem_cnt = max_sl <= 4 * TILE_WARPS && ((size_t)k8w + rlw) * 4 <= budget;
     rl_off = (int32_t)(((smem_cnt ? std::max(mw, (size_t)k8w) : mw) + 3) & ~(size_t)3);
-    smem = ((size_t)rl_off + rlw) * 4;
+    stg_off = (int32_t)(((size_t)rl_off + rlw + 3) & ~(size_t)3);
+    stg_cap = (int32_t)std::min<int64_t>(4096, ((int64_t)budget / 4 - stg_off) / 4);  // 16-byte groups
+    if (stg_cap < 64) stg_cap = 0;
+    smem = ((size_t)stg_off + (size_t)stg_cap * 4) * 4;
     tk = pick_tile(nhi, vpt, k, smem_cnt);
     C2_CUDA(ctx, cudaFuncSetAttribute(tk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int occ = 0;
@@ -1478,7 +1542,7 @@ int local_knn(c2_ctx *ctx, const Csr &csr, int t, const Clusters &cl, int k, c2_
   auto launch_tiles = [&](int64_t lo, int64_t hi, int ci, const c2_cand *seed, c2_cand *dst) -> int {
     if (hi <= lo) return C2_OK;
     TileArgs ta{tiles, lo, hi, counters + ci, bcs, vperm, vsize, blk_len8, blk_off8, packed, csr.psize, n, W, nwin, k,
-                seed, dst, ctx->kstats, gscratch, smax, qcap, rl_off, relabel ? 1 : 0};
+                seed, dst, ctx->kstats, gscratch, smax, qcap, rl_off, stg_off, stg_cap, relabel ? 1 : 0};
     int g = (int)std::min<int64_t>(grid, hi - lo);
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     if (ctx->timing) {

@@ -10,7 +10,7 @@ C = synth.config(name)
 offs, items = synth.generate(name)
 d_o, d_i = torch.from_numpy(offs).cuda(), torch.from_numpy(items).cuda()
 ctx = c2.Context(0)
-ks = torch.zeros(48, dtype=torch.int64, device="cuda")
+ks = torch.zeros(64, dtype=torch.int64, device="cuda")
 c2.build(d_o, d_i, k=C.k, t=C.t, b=C.b, N=C.N, seed=C.hash_seed, ctx=ctx)
 ctx.set_option(c2.OPT_KSTATS, ks.data_ptr())
 c2.build(d_o, d_i, k=C.k, t=C.t, b=C.b, N=C.N, seed=C.hash_seed, ctx=ctx)
@@ -26,6 +26,10 @@ print("  first-scan m histogram (bins of 20): " + " ".join(str(x) for x in k[16:
 tt = sum(k[32:36]) or 1
 print("  tile cycles by class (share, tiles, mean cycles): " + " ".join(
     f"{n}: {k[32 + i] / tt * 100:.1f}% {k[36 + i]} {k[32 + i] / max(k[36 + i], 1):.0f}" for i, n in enumerate(["mixed", "33-256", "257-1024", ">1024"])))
-mt = max(k[36], 1)
-print(f"  mixed tile (warp 0, mean cycles): sum(build ends - start) {k[40] / mt:.0f}  probe {k[41] / mt:.0f}  "
-      f"phaseA-other {k[42] / mt:.0f}  K8 {k[43] / mt:.0f}  wait {k[44] / mt:.0f}")
+for i, nm in enumerate(["mixed", "33-256", "257-1024", ">1024"]):
+    mt = max(k[36 + i], 1)
+    b = 40 + 5 * i
+    print(f"  {nm:9s} tile (warp 0, mean cycles): build-sum {k[b] / mt:.0f}  probe {k[b + 1] / mt:.0f}  "
+          f"phaseA-rest {k[b + 2] / mt:.0f}  K8 {k[b + 3] / mt:.0f}  wait {k[b + 4] / mt:.0f}")
+nb = max(k[62], 1)
+print(f"  rows of >1024 tiles (warp 0 sample): select {k[60] / nb:.0f} cycles/row  final {k[61] / nb:.0f} cycles/row  rows {k[62]}")
