@@ -201,6 +201,16 @@ def run_ours(args):
         # ALU peak: 148 SMs x 4 SMSP x 32 lanes x 1 int op/clk at sm_max_mhz (B200_PROFILING.md)
         sm_mhz = peaks.get("sm_max_mhz", 1965.0)
         alu_peak = 148 * 128 * sm_mhz * 1e6 / 1e12  # Tops/s
+        # DRAM traffic of one K7 launch from the committed ncu --set full capture (profiles/)
+        traffic, traffic_note = None, None
+        try:
+            with open(os.path.join(ROOT, "profiles", "r01_ncu_tile_traffic.json")) as f:
+                tj = json.load(f)
+            if tj.get("config") == C.name:
+                traffic = tj["dram_bytes_read"] + tj["dram_bytes_write"]
+                traffic_note = f"bytes per launch, {tj['launch']}; {tj['source']}"
+        except (OSError, KeyError, ValueError):
+            pass
         achieved = steps_total / n_tile / (tile_avg_ms * 1e-3) / 1e12
         line = {
             "metric": METRIC,
@@ -221,7 +231,8 @@ def run_ours(args):
                        " + per-step scratch)", "parallelism": f"independent datasets per rank x{ws}"},
             "roofline": {"kernel": "k_local_tile (K7 local Jaccard + K8 top-k)", "bound": "alu",
                          "achieved": achieved, "peak": alu_peak, "unit": "Tops/s (two-pointer comparisons)",
-                         "frac": achieved / alu_peak, "traffic": None,
+                         "frac": achieved / alu_peak, "traffic": traffic,
+                         "traffic_note": traffic_note,
                          "peak_source": f"{peak_src}: 148 SM x 128 int lanes x {sm_mhz:.0f} MHz",
                          "kernel_ms_per_launch": tile_avg_ms, "launches_per_step": n_tile,
                          "share_of_step": tile_avg_ms * n_tile / ms},
