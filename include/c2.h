@@ -88,7 +88,7 @@ enum {
                               levels recompute from the CSR (A29).  Default 8. */
   C2_OPT_SYNC_CHECK = 2,   /* nonzero: synchronise + check errors after every launch */
   C2_OPT_TIMING = 3,       /* nonzero: record per-phase CUDA-event times into c2_stats */
-  C2_OPT_KSTATS = 4,       /* diagnostics: value = address of a dev uint64[64] the local kernel adds
+  C2_OPT_KSTATS = 4,       /* diagnostics: value = address of a dev uint64[80] the local kernel adds
                               counters to (rows, survivors, sort sizes, overflows; 0 = off) */
   C2_OPT_RELABEL = 5       /* nonzero (default): when the item range needs >= 3 shared-memory windows,
                               Step 2 renumbers each cluster's shared items densely (one window per

@@ -885,6 +885,8 @@ __global__ void __launch_bounds__(TILE_T, 1) k_local_tile(TileArgs a) {
         if (a.kstats) ckb += clock64();
         // ---- probe: each warp streams VPT slices of v lists, two 16-byte loads per step with
         //      the next two steps in flight (odd tails padded with the sentinel item W, M[W] = 0)
+        const long long ckpb = a.kstats ? clock64() : 0;
+        int nsteps = 0;
 #pragma unroll
         for (int q = 0; q < VPT; ++q) {
           const int jj = g0 + q * TILE_WARPS + warp;
@@ -907,8 +909,13 @@ __global__ void __launch_bounds__(TILE_T, 1) k_local_tile(TileArgs a) {
               d1 = n1;
               n0 = f0;
               n1 = f1;
+              ++nsteps;
             }
           }
+        }
+        if (a.kstats && lane == 0 && s > 1024) {  // probe busy time per step (big tiles)
+          atomicAdd(&a.kstats[64], (unsigned long long)(clock64() - ckpb));
+          atomicAdd(&a.kstats[65], (unsigned long long)nsteps);
         }
         __syncthreads();
         if (a.kstats) ckp += clock64();

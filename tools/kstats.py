@@ -10,7 +10,7 @@ C = synth.config(name)
 offs, items = synth.generate(name)
 d_o, d_i = torch.from_numpy(offs).cuda(), torch.from_numpy(items).cuda()
 ctx = c2.Context(0)
-ks = torch.zeros(64, dtype=torch.int64, device="cuda")
+ks = torch.zeros(80, dtype=torch.int64, device="cuda")
 c2.build(d_o, d_i, k=C.k, t=C.t, b=C.b, N=C.N, seed=C.hash_seed, ctx=ctx)
 ctx.set_option(c2.OPT_KSTATS, ks.data_ptr())
 c2.build(d_o, d_i, k=C.k, t=C.t, b=C.b, N=C.N, seed=C.hash_seed, ctx=ctx)
@@ -33,3 +33,4 @@ for i, nm in enumerate(["mixed", "33-256", "257-1024", ">1024"]):
           f"phaseA-rest {k[b + 2] / mt:.0f}  K8 {k[b + 3] / mt:.0f}  wait {k[b + 4] / mt:.0f}")
 nb = max(k[62], 1)
 print(f"  rows of >1024 tiles (warp 0 sample): select {k[60] / nb:.0f} cycles/row  final {k[61] / nb:.0f} cycles/row  rows {k[62]}")
+print(f"  probe of >1024 tiles: busy cycles per warp-step {k[64] / max(k[65], 1):.0f}  steps {k[65]}")
