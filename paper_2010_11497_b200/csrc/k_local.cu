@@ -274,12 +274,17 @@ __global__ void k_sl_len(const Tile *__restrict__ tiles, int64_t nslices, const 
     if (w < nwin && lane == w && c[w]) atomicMax(&blk_len8[sl * nwin + w], (c[w] + 7) / 8);
 }
 
-__global__ void k_sl_fill(const Tile *__restrict__ tiles, int64_t nslices, const BigC *__restrict__ bcs,
-                          const int32_t *__restrict__ vperm, const int32_t *__restrict__ offs,
-                          const int32_t *__restrict__ items, int32_t W, int nwin,
-                          const int32_t *__restrict__ blk_len8, const int32_t *__restrict__ blk_off8,
-                          uint16_t *__restrict__ packed16) {
-  const int lane = threadIdx.x & 31;
+// Order within a list does not matter to the counts, so each member's window list is laid out
+// by bank: key = (x - e) mod 32 for the member in lane e (the mask word of item x sits in bank
+// x mod 32).  At any step the 32 lanes then read words of ~32 different banks instead of random
+// ones (random: ~3.4 shared-memory wavefronts per mask load, which binds the probe).
+__global__ void __launch_bounds__(256) k_sl_fill(const Tile *__restrict__ tiles, int64_t nslices,
+                                                 const BigC *__restrict__ bcs, const int32_t *__restrict__ vperm,
+                                                 const int32_t *__restrict__ offs, const int32_t *__restrict__ items,
+                                                 int32_t W, int nwin, const int32_t *__restrict__ blk_len8,
+                                                 const int32_t *__restrict__ blk_off8, uint16_t *__restrict__ packed16) {
+  __shared__ int hist[8][32];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int64_t g = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t sl = g >> 5;
   if (sl >= nslices) return;
@@ -289,21 +294,41 @@ __global__ void k_sl_fill(const Tile *__restrict__ tiles, int64_t nslices, const
   const int vi = T.j * 32 + e;
   const int32_t v = vi < b.s ? vperm[b.vp_off + vi] : -1;
   const int32_t pb = v >= 0 ? offs[v] : 0, pe = v >= 0 ? offs[v + 1] : 0;
+  int *h = hist[wib];
   for (int w = 0; w < nwin; ++w) {
     const int32_t lo = w * W;
     const int32_t len = blk_len8[sl * nwin + w] * 8;
     uint16_t *dst = packed16 + (int64_t)blk_off8[sl * nwin + w] * 256 + e * 8;
+    h[lane] = 0;
+    __syncwarp();
     int cnt = 0;
     for (int32_t p0 = pb; p0 < pe; p0 += 32) {
       const int32_t p = p0 + lane;
       const int32_t r = p < pe ? items[p] - lo : -1;
       const bool in = r >= 0 && r < W;
-      const unsigned bal = __ballot_sync(0xffffffffu, in);
-      const int pos = cnt + __popc(bal & ((1u << lane) - 1));
-      if (in) dst[(pos >> 3) * 256 + (pos & 7)] = (uint16_t)r;
-      cnt += __popc(bal);
+      if (in) atomicAdd(&h[(r - e) & 31], 1);
+      cnt += __popc(__ballot_sync(0xffffffffu, in));
+    }
+    __syncwarp();
+    int c = h[lane], x = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    __syncwarp();
+    h[lane] = x - c;  // bucket starts
+    __syncwarp();
+    for (int32_t p0 = pb; p0 < pe; p0 += 32) {
+      const int32_t p = p0 + lane;
+      const int32_t r = p < pe ? items[p] - lo : -1;
+      if (r >= 0 && r < W) {
+        const int pos = atomicAdd(&h[(r - e) & 31], 1);
+        dst[(pos >> 3) * 256 + (pos & 7)] = (uint16_t)r;
+      }
     }
     for (int pos = cnt + lane; pos < len; pos += 32) dst[(pos >> 3) * 256 + (pos & 7)] = (uint16_t)W;
+    __syncwarp();
   }
 }
 
@@ -776,7 +801,9 @@ __global__ void __launch_bounds__(TILE_T, 1) k_local_tile(TileArgs a) {
   __shared__ int32_t s_bl[2][MAX_WIN], s_bo[2][MAX_WIN], s_so[2][MAX_WIN];  // rows' blocks; staged offsets
   __shared__ int s_stg[2];  // 1: the rows' blocks of every window are staged in stg
   __shared__ int s_row;
+  __shared__ int s_wq[TILE_WARPS];  // per-warp survivor counters of the K8 scan (0 between scans)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid < TILE_WARPS) s_wq[tid] = 0;
   for (int i = tid; i < a.W + 1; i += TILE_T) M[i] = 0;
   uint32_t *kb = SMEM_CNT ? dyn : a.gscratch + (int64_t)blockIdx.x * K8Lay(a.smax, qcap).words;  // K8 region
   c2_cand *s_run = reinterpret_cast<c2_cand *>(dyn + a.rl_off);  // fused: the rows' running lists [32][k]
@@ -1021,13 +1048,19 @@ __global__ void __launch_bounds__(TILE_T, 1) k_local_tile(TileArgs a) {
           }
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
-            const bool ok = v4 + e != selfr && passes(iv[e], pv[e], dv[e], T);
-            const unsigned bal = __ballot_sync(0xffffffffu, ok);
-            const int p = m + __popc(bal & ((1u << lane) - 1));
-            if (ok && p < qcap) qr[p] = Cand{iv[e] | ((prr + pv[e] - iv[e]) << 16), dv[e]};
-            m += __popc(bal);
+            // survivors are few: a shared counter bumped by the passing lanes only (queue order
+            // is irrelevant, the survivors are sorted by the exact key afterwards)
+            if (v4 + e != selfr && passes(iv[e], pv[e], dv[e], T)) {
+              const int p = atomicAdd(&s_wq[warp], 1);
+              if (p < qcap) qr[p] = Cand{iv[e] | ((prr + pv[e] - iv[e]) << 16), dv[e]};
+            }
           }
         }
+        __syncwarp();
+        m = s_wq[warp];
+        __syncwarp();
+        if (lane == 0) s_wq[warp] = 0;
+        __syncwarp();
         return m;
       };
       // k-th best of the first 64*KS queue entries (all distinct real candidates): a valid
