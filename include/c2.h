@@ -77,7 +77,9 @@ enum {
 
 /* ---------------------------------------------------------------- context */
 /* Create a context on CUDA device `device`, enqueueing on `cuda_stream` (a cudaStream_t;
- * NULL -> the ctx creates and owns a non-blocking stream).  *out receives the ctx. */
+ * NULL -> the ctx creates and owns a non-blocking stream, NOT ordered with the legacy default
+ * stream; pass cudaStreamLegacy, i.e. (void *)1, to enqueue on the legacy default stream).
+ * *out receives the ctx. */
 C2_API int c2_ctx_create(c2_ctx **out, int device, void *cuda_stream);
 C2_API void c2_ctx_destroy(c2_ctx *ctx);
 /* Message for the last non-OK return of this ctx (static storage owned by the ctx). */

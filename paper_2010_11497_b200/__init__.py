@@ -27,6 +27,7 @@ C2_OK, C2_EINVAL, C2_EDATA, C2_ENOMEM, C2_ECUDA = 0, -1, -2, -3, -4
 SIM_EXACT, SIM_GF1024 = 0, 1
 OPT_SKETCH_DEPTH, OPT_SYNC_CHECK, OPT_TIMING, OPT_KSTATS, OPT_RELABEL = 1, 2, 3, 4, 5
 ABSENT = 0xFFFF
+CUDA_STREAM_LEGACY = 0x1  # cudaStreamLegacy: the legacy default stream
 
 _lib = None
 _lock = threading.Lock()
@@ -100,7 +101,10 @@ class Context:
         self.device = device
         self.stream = stream if stream is not None else torch.cuda.current_stream(device)
         h = _P()
-        rc = lib().c2_ctx_create(ctypes.byref(h), device, _P(self.stream.cuda_stream))
+        # torch's default stream has handle 0, which c2_ctx_create reads as "make your own
+        # stream"; pass cudaStreamLegacy for it so the library's work is ordered with torch's
+        handle = self.stream.cuda_stream or CUDA_STREAM_LEGACY
+        rc = lib().c2_ctx_create(ctypes.byref(h), device, _P(handle))
         if rc != C2_OK:
             raise C2Error(rc, "c2_ctx_create failed")
         self.h = h

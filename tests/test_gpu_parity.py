@@ -384,3 +384,21 @@ def test_build_configs_windows(ctx_win, cfg):
     C = synth.config(cfg)
     offs, items = synth.generate(cfg)
     check_build(ctx_win, offs, items, C.t, C.b, C.N, C.k, C.hash_seed)
+
+
+def test_ctx_reuse_across_sizes():
+    """One context serving problems of different sizes in turn (workspaces grow between calls)
+    must give the same bits as a fresh context."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    c = c2.Context(0)
+    try:
+        for cfg in ["c1", "c2", "c1", "c3", "c2"]:
+            C = synth.config(cfg)
+            offs, items = synth.generate(cfg)
+            nbr, inter, uni, _ = c2.build(dev(offs), dev(items), k=C.k, t=C.t, b=C.b, N=C.N, seed=C.hash_seed, ctx=c)
+            o = oracle.build_graph(offs, items, k=C.k, t=C.t, b=C.b, N=C.N, seed=C.hash_seed)
+            assert np.array_equal(npy(nbr), o["nbr"]), cfg
+            assert np.array_equal(npy(inter), o["inter"]) and np.array_equal(npy(uni), o["uni"]), cfg
+    finally:
+        c.close()
