@@ -247,41 +247,52 @@ __global__ void __launch_bounds__(1024) k_sl_sort(const BigC *__restrict__ bcs, 
 // member's sorted items (coalesced reads); each window is a filter pass with ballot compaction.
 // blk_len8[slice][w] = ceil(max over the slice's 32 lists of |list ∩ window w| / 8) (atomicMax;
 // zeroed before).
+__device__ __forceinline__ int32_t lower_bound_items(const int32_t *__restrict__ items, int32_t lo, int32_t hi,
+                                                     int32_t x) {  // first p in [lo,hi) with items[p] >= x
+  while (lo < hi) {
+    const int32_t mid = (lo + hi) >> 1;
+    if (items[mid] < x) lo = mid + 1;
+    else hi = mid;
+  }
+  return lo;
+}
+
+// Rows are sorted, so window w of a member's list is the contiguous range [lb(wW), lb((w+1)W)):
+// one thread per member position finds its window boundaries by binary search (no item walk)
+// and folds the lengths into the slice maxima.
 __global__ void k_sl_len(const Tile *__restrict__ tiles, int64_t nslices, const BigC *__restrict__ bcs,
                          const int32_t *__restrict__ vperm, const int32_t *__restrict__ offs,
-                         const int32_t *__restrict__ items, int32_t W, int nwin, int32_t *__restrict__ blk_len8) {
+                         const int32_t *__restrict__ items, int32_t W, int nwin, int32_t *__restrict__ blk_len8,
+                         int32_t *__restrict__ bounds) {
   const int lane = threadIdx.x & 31;
-  const int64_t g = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int64_t sl = g >> 5;
+  const int64_t sl = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (sl >= nslices) return;
   const Tile T = tiles[sl];
   const BigC b = bcs[T.bc];
-  const int vi = T.j * 32 + (int)(g & 31);
+  const int vi = T.j * 32 + lane;
   const int32_t v = vi < b.s ? vperm[b.vp_off + vi] : -1;
-  if (v < 0) return;
-  int c[MAX_WIN];
+  int32_t p = v >= 0 ? offs[v] : 0;
+  const int32_t pe = v >= 0 ? offs[v + 1] : 0;
+  int32_t *bd = bounds + (sl * 32 + lane) * (nwin + 1);  // window w of this member: [bd[w], bd[w+1])
+  bd[0] = p;
+  for (int w = 0; w < nwin; ++w) {
+    const int32_t q = w + 1 < nwin ? lower_bound_items(items, p, pe, (w + 1) * W) : pe;
+    bd[w + 1] = q;
+    int c = q - p;
+    p = q;
 #pragma unroll
-  for (int w = 0; w < MAX_WIN; ++w) c[w] = 0;
-  for (int32_t p0 = offs[v]; p0 < offs[v + 1]; p0 += 32) {
-    const int32_t p = p0 + lane;
-    const int wx = p < offs[v + 1] ? items[p] / W : -1;
-#pragma unroll
-    for (int w = 0; w < MAX_WIN; ++w)
-      if (w < nwin) c[w] += __popc(__ballot_sync(0xffffffffu, wx == w));
+    for (int o = 16; o; o >>= 1) c = max(c, __shfl_xor_sync(0xffffffffu, c, o));
+    if (lane == 0) blk_len8[sl * nwin + w] = (c + 7) / 8;
   }
-#pragma unroll
-  for (int w = 0; w < MAX_WIN; ++w)
-    if (w < nwin && lane == w && c[w]) atomicMax(&blk_len8[sl * nwin + w], (c[w] + 7) / 8);
 }
 
 // Order within a list does not matter to the counts, so each member's window list is laid out
 // by bank: key = (x - e) mod 32 for the member in lane e (the mask word of item x sits in bank
 // x mod 32).  At any step the 32 lanes then read words of ~32 different banks instead of random
 // ones (random: ~3.4 shared-memory wavefronts per mask load, which binds the probe).
-__global__ void __launch_bounds__(256) k_sl_fill(const Tile *__restrict__ tiles, int64_t nslices,
-                                                 const BigC *__restrict__ bcs, const int32_t *__restrict__ vperm,
-                                                 const int32_t *__restrict__ offs, const int32_t *__restrict__ items,
-                                                 int32_t W, int nwin, const int32_t *__restrict__ blk_len8,
+__global__ void __launch_bounds__(256) k_sl_fill(int64_t nslices, const int32_t *__restrict__ bounds,
+                                                 const int32_t *__restrict__ items, int32_t W, int nwin,
+                                                 const int32_t *__restrict__ blk_len8,
                                                  const int32_t *__restrict__ blk_off8, uint16_t *__restrict__ packed16) {
   __shared__ int hist[8][32];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
@@ -289,14 +300,12 @@ __global__ void __launch_bounds__(256) k_sl_fill(const Tile *__restrict__ tiles,
   const int64_t sl = g >> 5;
   if (sl >= nslices) return;
   const int e = (int)(g & 31);
-  const Tile T = tiles[sl];
-  const BigC b = bcs[T.bc];
-  const int vi = T.j * 32 + e;
-  const int32_t v = vi < b.s ? vperm[b.vp_off + vi] : -1;
-  const int32_t pb = v >= 0 ? offs[v] : 0, pe = v >= 0 ? offs[v + 1] : 0;
+  const int32_t *bd = bounds + g * (nwin + 1);
   int *h = hist[wib];
   for (int w = 0; w < nwin; ++w) {
     const int32_t lo = w * W;
+    // this window's items: the contiguous range [pb, pe) of the sorted row (from k_sl_len)
+    const int32_t pb = bd[w], pe = bd[w + 1];
     const int32_t len = blk_len8[sl * nwin + w] * 8;
     uint16_t *dst = packed16 + (int64_t)blk_off8[sl * nwin + w] * 256 + e * 8;
     h[lane] = 0;
@@ -1518,9 +1527,10 @@ int local_knn(c2_ctx *ctx, const Csr &csr, int t, const Clusters &cl, int k, c2_
       blk_len8 = (int32_t *)ws_get(ctx, "blk_len8", (size_t)(2 * nb + 2) * 4, &rc);
       if (rc) return rc;
       blk_off8 = blk_len8 + nb + 1;
-      C2_CUDA(ctx, cudaMemsetAsync(blk_len8, 0, (size_t)(nb + 1) * 4, st));
-      k_sl_len<<<nblk(nslices * 32 * 32), 256, 0, st>>>(tiles, nslices, bcs, vperm, csr.offs, csr.items, W, nwin,
-                                                        blk_len8);
+      int32_t *bounds = (int32_t *)ws_get(ctx, "sl_bounds", (size_t)nslices * 32 * (nwin + 1) * 4, &rc);
+      if (rc) return rc;
+      k_sl_len<<<nblk(nslices * 32), 256, 0, st>>>(tiles, nslices, bcs, vperm, csr.offs, csr.items, W, nwin,
+                                                   blk_len8, bounds);
       C2_LAUNCHED(ctx, "k_sl_len");
       C2_TRY(scan_exclusive(ctx, blk_len8, blk_off8, nb));
       int32_t tot8;
@@ -1528,8 +1538,8 @@ int local_knn(c2_ctx *ctx, const Csr &csr, int t, const Clusters &cl, int k, c2_
       C2_TRY(stream_sync(ctx, "packed size"));
       packed = (uint4 *)ws_get(ctx, "packed", (size_t)tot8 * 32 * 16 + 16, &rc);
       if (rc) return rc;
-      k_sl_fill<<<nblk(nslices * 32 * 32), 256, 0, st>>>(tiles, nslices, bcs, vperm, csr.offs, csr.items, W, nwin,
-                                                         blk_len8, blk_off8, reinterpret_cast<uint16_t *>(packed));
+      k_sl_fill<<<nblk(nslices * 32 * 32), 256, 0, st>>>(nslices, bounds, csr.items, W, nwin, blk_len8, blk_off8,
+                                                         reinterpret_cast<uint16_t *>(packed));
       C2_LAUNCHED(ctx, "k_sl_fill");
     }
   }
