@@ -663,6 +663,41 @@ __device__ __forceinline__ E warp_get(const E (&a)[R], int p) {
   return shfl_e(r, p & 31);
 }
 
+// Out-of-line copies of the K8 sorting networks: one body per size instead of one per call site
+// (the fully unrolled networks otherwise dominate the kernel's code and its i-cache misses).
+template <int R>
+struct KCA {
+  KC e[R];
+};
+template <int R>
+__device__ __noinline__ KCA<R> sort_kc_ni(KCA<R> a) {
+  warp_sort<R>(a.e);
+  return a;
+}
+template <int R>
+__device__ __noinline__ KCA<R> merge_kc_ni(KCA<R> a) {
+  warp_bitonic_merge<R>(a.e);
+  return a;
+}
+template <int R>
+__device__ __forceinline__ void sort_kc(KC (&x)[R]) {
+  KCA<R> t;
+#pragma unroll
+  for (int j = 0; j < R; ++j) t.e[j] = x[j];
+  t = sort_kc_ni<R>(t);
+#pragma unroll
+  for (int j = 0; j < R; ++j) x[j] = t.e[j];
+}
+template <int R>
+__device__ __forceinline__ void merge_kc(KC (&x)[R]) {
+  KCA<R> t;
+#pragma unroll
+  for (int j = 0; j < R; ++j) t.e[j] = x[j];
+  t = merge_kc_ni<R>(t);
+#pragma unroll
+  for (int j = 0; j < R; ++j) x[j] = t.e[j];
+}
+
 // ------------------------------------------------------------------ K7 tile kernel
 __device__ __forceinline__ void csa(uint32_t &h, uint32_t &l, uint32_t a, uint32_t b, uint32_t c) {
   uint32_t u = a ^ b;
@@ -1079,7 +1114,7 @@ __global__ void __launch_bounds__(TILE_T, 1) k_local_tile(TileArgs a) {
         KC e[2 * KS];
 #pragma unroll
         for (int j = 0; j < 2 * KS; ++j) e[j] = to_kc(qr[32 * j + lane]);
-        warp_sort<2 * KS>(e);
+        sort_kc<2 * KS>(e);
         return make_ref(kc_cand(warp_get<2 * KS>(e, kk - 1)), prr, true);
       };
       long long ckr = a.kstats ? clock64() : 0;
@@ -1115,7 +1150,7 @@ __global__ void __launch_bounds__(TILE_T, 1) k_local_tile(TileArgs a) {
         KC e[R1];
 #pragma unroll
         for (int j = 0; j < R1; ++j) e[j] = to_kc(t[j]);
-        warp_sort<R1>(e);
+        sort_kc<R1>(e);
         const KC Tr = warp_get<R1>(e, kk - 1);
         if (kc_real(Tr) && better_c(kc_cand(Tr), tau)) T = make_ref(kc_cand(Tr), prr, true);
       };
@@ -1214,14 +1249,14 @@ __global__ void __launch_bounds__(TILE_T, 1) k_local_tile(TileArgs a) {
         KC q[KS];
 #pragma unroll
         for (int j = 0; j < KS; ++j) q[j] = to_kc((32 * j + lane < m) ? qr[32 * j + lane] : sent());
-        warp_sort<KS>(q);
+        sort_kc<KS>(q);
 #pragma unroll
         for (int j = 0; j < KS; ++j) L[j] = q[j];
       } else if (m <= 64 * KS) {
         KC q[2 * KS];
 #pragma unroll
         for (int j = 0; j < 2 * KS; ++j) q[j] = to_kc((32 * j + lane < m) ? qr[32 * j + lane] : sent());
-        warp_sort<2 * KS>(q);
+        sort_kc<2 * KS>(q);
 #pragma unroll
         for (int j = 0; j < KS; ++j) L[j] = q[j];
       } else {
@@ -1270,7 +1305,7 @@ __global__ void __launch_bounds__(TILE_T, 1) k_local_tile(TileArgs a) {
       for (int j = 0; j < KS; ++j) mm[j] = (32 * j + lane < kk) ? L[j] : KC{0ull, 1u << 16};
 #pragma unroll
       for (int j = 0; j < KS; ++j) mm[KS + j] = shfl_e(S[KS - 1 - j], 31 - lane);
-      warp_bitonic_merge<2 * KS>(mm);
+      merge_kc<2 * KS>(mm);
       // drop adjacent duplicates (a repeated id carries identical values, A16); keep k
       int base = 0;
 #pragma unroll
