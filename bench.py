@@ -97,6 +97,20 @@ def dist_env():
     return ws, rank, local
 
 
+def reduce_over_ranks(ms, pairs, device):
+    """Weak scaling over independent datasets: the job's step time is the MAX over ranks of the
+    device-timed step, its work the SUM of the ranks' pairs.  No-op on one process."""
+    import torch
+    import torch.distributed as dist
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
+        return float(ms), float(pairs)
+    tmax = torch.tensor([float(ms)], dtype=torch.float64, device=device)
+    tsum = torch.tensor([float(pairs)], dtype=torch.float64, device=device)
+    dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
+    dist.all_reduce(tsum, op=dist.ReduceOp.SUM)
+    return float(tmax[0]), float(tsum[0])
+
+
 def cfg_for_rank(name, rank):
     C = synth.config(name)
     return synth.config(name, data_seed=C.data_seed + 1000 * rank) if rank else C
@@ -150,15 +164,7 @@ def run_ours(args):
     ms = ev0.elapsed_time(ev1) / args.steps
     st = ctx.stats()
     pairs = st["pairs"]
-    # max over ranks of the step time, sum of pairs
-    if ws > 1:
-        t = torch.tensor([ms, float(pairs)], dtype=torch.float64, device=dev)
-        tmax = t.clone()
-        dist.all_reduce(tmax[:1], op=dist.ReduceOp.MAX)
-        dist.all_reduce(t[1:], op=dist.ReduceOp.SUM)
-        ms_max, pairs_all = float(tmax[0]), float(t[1])
-    else:
-        ms_max, pairs_all = ms, float(pairs)
+    ms_max, pairs_all = reduce_over_ranks(ms, pairs, dev)
     value = pairs_all / (ms_max * 1e-3)
 
     # ---- e2e: the same build through the C ABI with host buffers (pinned), copies inside
@@ -183,10 +189,7 @@ def run_ours(args):
     e1.record(stream)
     torch.cuda.synchronize(dev)
     e2e_ms = e0.elapsed_time(e1) / e2e_steps
-    if ws > 1:
-        t = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_ms = float(t[0])
+    e2e_ms, _ = reduce_over_ranks(e2e_ms, 0, dev)
     h2d = (n + 1) * 4 + nnz * 4
     d2h = n * C.k * (4 + 2 + 2 + 4)
 
