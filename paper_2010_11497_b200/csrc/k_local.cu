@@ -1041,17 +1041,23 @@ __global__ void __launch_bounds__(TILE_T, 1) k_local_tile(TileArgs a) {
     uint32_t *zq = nullptr;  // queue words the warp's previous row wrote (re-zeroed: M alias)
     int zn = 0;
     long long tfin = 0, acc_sel = 0, acc_fin = 0, nrow_b = 0;  // kstats: big tiles' per-row split
-    for (;;) {  // rows taken dynamically: their costs differ a lot
+    // rows are taken dynamically, the expensive ones first: rows without a full running list
+    // (round 1 in big clusters), then the others
+    const unsigned heavy = __ballot_sync(0xffffffffu, lane < nr && s_ru[lane] >= 0 &&
+                                                          !(a.seed && s_run[lane * kk + kk - 1].id >= 0));
+    const int nheavy = __popc(heavy);
+    for (;;) {
       if (a.kstats && tfin) {
         acc_fin += clock64() - tfin;
         tfin = 0;
       }
       for (int i = lane; i < zn; i += 32) zq[i] = 0u;
       zn = 0;
-      int r = 0;
-      if (lane == 0) r = atomicAdd(&s_row, 1);
-      r = __shfl_sync(0xffffffffu, r, 0);
-      if (r >= nr) break;
+      int idx = 0;
+      if (lane == 0) idx = atomicAdd(&s_row, 1);
+      idx = __shfl_sync(0xffffffffu, idx, 0);
+      if (idx >= nr) break;
+      const int r = idx < nheavy ? (int)__fns(heavy, 0, idx + 1) : (int)__fns(~heavy, 0, idx - nheavy + 1);
       const int32_t u = s_ru[r];
       if (u < 0) continue;
       const uint32_t prr = s_rp[r];

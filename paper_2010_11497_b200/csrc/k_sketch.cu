@@ -31,10 +31,7 @@ __global__ void __launch_bounds__(256) k_sketch(const int32_t *__restrict__ offs
 #pragma unroll
   for (int j = 0; j < C2_SKETCH_D; ++j) s[j] = C2_ABSENT16;
   const int32_t p0 = offs[u], p1 = offs[u + 1];
-  for (int32_t p = p0; p < p1; ++p) {
-    uint32_t x = (uint32_t)__ldg(items + p);
-    uint32_t v = TABLE ? (active ? (uint32_t)__ldg(htab + (int64_t)f * m + x) : C2_ABSENT16)
-                       : c2d::item_hash(ca, cc, x, b);
+  auto insert = [&](uint32_t v) {
     if (v < s[C2_SKETCH_D - 1]) {
       bool dup = false;
 #pragma unroll
@@ -45,7 +42,23 @@ __global__ void __launch_bounds__(256) k_sketch(const int32_t *__restrict__ offs
         s[0] = min(s[0], v);
       }
     }
+  };
+  auto hash = [&](uint32_t x) -> uint32_t {
+    return TABLE ? (active ? (uint32_t)__ldg(htab + (int64_t)f * m + x) : C2_ABSENT16) : c2d::item_hash(ca, cc, x, b);
+  };
+  // eight items in flight per step (the loads do not depend on the insertions)
+  int32_t p = p0;
+  for (; p + 8 <= p1; p += 8) {
+    uint32_t x[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) x[q] = (uint32_t)__ldg(items + p + q);
+    uint32_t v[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) v[q] = hash(x[q]);
+#pragma unroll
+    for (int q = 0; q < 8; ++q) insert(v[q]);
   }
+  for (; p < p1; ++p) insert(hash((uint32_t)__ldg(items + p)));
   if (!active) return;
   uint16_t *o = out + ((int64_t)f * n + u) * D;
   if (D == C2_SKETCH_D) {
