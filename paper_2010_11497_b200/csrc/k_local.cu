@@ -1231,8 +1231,9 @@ __global__ void __launch_bounds__(TILE_T, 1) k_local_tile(TileArgs a) {
       }
       if (a.seed && m == 0) continue;
       c2_cand *dst = a.seed ? a.out + (int64_t)u * kk : a.out + ((int64_t)B.f * a.n + u) * kk;
-      if (a.seed && m <= 8) {
-        // few survivors: insert them one by one into the running list (duplicates skipped)
+      if (a.seed && m <= 16) {
+        // few survivors (one insertion ~20 instructions, sort-32 + merge-64 ~320): insert them one
+        // by one into the running list (duplicates skipped)
         KC S[KS];
 #pragma unroll
         for (int j = 0; j < KS; ++j) S[j] = to_kc((32 * j + lane < kk) ? from_out(s_run[r * kk + 32 * j + lane]) : sent());
