@@ -38,6 +38,32 @@ __global__ void k_level0(const uint16_t *__restrict__ sk, int64_t TN, int32_t n,
   c2d::agg_inc(mask, &size0[k], k);
 }
 
+// Same as k_level0 with the node sizes counted in a shared-memory histogram over the b buckets
+// of the chunk's first function (blocks cover consecutive (f,u)); one global atomic per non-empty
+// bucket per block.  Entries of a later function (chunks crossing a function boundary) count
+// directly in global memory.
+__global__ void __launch_bounds__(512) k_level0h(const uint16_t *__restrict__ sk, int64_t TN, int32_t n, int32_t b,
+                                                 int64_t chunk, int32_t *__restrict__ key,
+                                                 uint16_t *__restrict__ curval, int32_t *__restrict__ size0) {
+  extern __shared__ int32_t hb[];
+  const int64_t q0 = (int64_t)blockIdx.x * chunk, q1 = min(q0 + chunk, TN);
+  const int32_t f0 = (int32_t)(q0 / n);
+  for (int i = threadIdx.x; i < b; i += blockDim.x) hb[i] = 0;
+  __syncthreads();
+  for (int64_t q = q0 + threadIdx.x; q < q1; q += blockDim.x) {
+    const int32_t f = (int32_t)(q / n);
+    const uint16_t v = sk[q * C2_SKETCH_D];  // H_f(u)
+    const int32_t k = f * b + v;
+    key[q] = k;
+    curval[q] = v;
+    if (f == f0) atomicAdd(&hb[v], 1);
+    else atomicAdd(&size0[k], 1);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < b; i += blockDim.x)
+    if (hb[i]) atomicAdd(&size0[(int64_t)f0 * b + i], hb[i]);
+}
+
 __global__ void k_flag_gt(const int32_t *__restrict__ cnt, int64_t E, int64_t N, int32_t *__restrict__ flag) {
   int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (e < E) flag[e] = cnt[e] > N ? 1 : 0;
@@ -290,8 +316,16 @@ int fastrandomhash(c2_ctx *ctx, const Csr &csr, int t, int b, int64_t N, const H
   // ---- K2 level 0: Alg. 1, B_f[H_f(u)] <- B_f[H_f(u)] ∪ {u}
   C2_CUDA(ctx, cudaMemsetAsync(size0, 0, (size_t)TB * 4, st));
   C2_CUDA(ctx, cudaMemsetAsync(acc, 0, 64, st));
-  k_level0<<<nblk(TN), 256, 0, st>>>(sk, TN, n, b, key, curval, size0);
-  C2_LAUNCHED(ctx, "k_level0");
+  if (b <= 16384) {
+    const int64_t chunk = 8192;
+    C2_CUDA(ctx, cudaFuncSetAttribute(k_level0h, cudaFuncAttributeMaxDynamicSharedMemorySize, b * 4));
+    k_level0h<<<(unsigned)((TN + chunk - 1) / chunk), 512, (size_t)b * 4, st>>>(sk, TN, n, b, chunk, key, curval,
+                                                                              size0);
+    C2_LAUNCHED(ctx, "k_level0h");
+  } else {
+    k_level0<<<nblk(TN), 256, 0, st>>>(sk, TN, n, b, key, curval, size0);
+    C2_LAUNCHED(ctx, "k_level0");
+  }
   k_flag_gt<<<nblk(TB), 256, 0, st>>>(size0, TB, N, aflag0);
   C2_LAUNCHED(ctx, "k_flag_gt");
   C2_TRY(scan_exclusive(ctx, aflag0, ascan0, TB));
