@@ -247,6 +247,34 @@ __global__ void __launch_bounds__(1024) k_sl_sort(const BigC *__restrict__ bcs, 
 // member's sorted items (coalesced reads); each window is a filter pass with ballot compaction.
 // blk_len8[slice][w] = ceil(max over the slice's 32 lists of |list ∩ window w| / 8) (atomicMax;
 // zeroed before).
+// One 512-byte descriptor record per tile item, so the tile kernel's next-tile fetch is a
+// single cp.async instead of a chain of dependent loads: [0,2) Tile, [2,8) BigC, [8,24) rows'
+// block lengths per window, [24,40) block offsets, [64,96) row user ids, [96,128) row |P_u|.
+constexpr int REC_W = 128;
+__global__ void k_tile_rec(const Tile *__restrict__ tiles, int64_t nslices, const BigC *__restrict__ bcs,
+                           const int32_t *__restrict__ vperm, const int32_t *__restrict__ vsize,
+                           const int32_t *__restrict__ blk_len8, const int32_t *__restrict__ blk_off8, int nwin,
+                           int32_t *__restrict__ rec) {
+  const int lane = threadIdx.x & 31;
+  const int64_t it = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (it >= nslices) return;
+  const Tile T = tiles[it];
+  const BigC B = bcs[T.bc];
+  int32_t *r = rec + it * REC_W;
+  const int vi = T.j * 32 + lane;
+  r[64 + lane] = vi < B.s ? vperm[B.vp_off + vi] : -1;
+  r[96 + lane] = vi < B.s ? vsize[B.vp_off + vi] : 0;
+  const int64_t sb = (int64_t)(B.sl_off + T.j) * nwin;
+  if (lane < 16) {
+    r[8 + lane] = lane < nwin ? blk_len8[sb + lane] : 0;
+    r[24 + lane] = lane < nwin ? blk_off8[sb + lane] : 0;
+  }
+  if (lane == 0) {
+    r[0] = T.bc, r[1] = T.j;
+    r[2] = B.f, r[3] = B.s, r[4] = B.vp_off, r[5] = B.sl_off, r[6] = B.slot, r[7] = B.kc;
+  }
+}
+
 __device__ __forceinline__ int32_t lower_bound_items(const int32_t *__restrict__ items, int32_t lo, int32_t hi,
                                                      int32_t x) {  // first p in [lo,hi) with items[p] >= x
   while (lo < hi) {
@@ -749,6 +777,7 @@ struct TileArgs {
   const BigC *bcs;
   const int32_t *vperm;
   const int32_t *vsize;
+  const int32_t *rec;   // k_tile_rec records [nslices][REC_W]
   const int32_t *blk_len8;
   const int32_t *blk_off8;
   const uint4 *packed;
@@ -844,6 +873,7 @@ __global__ void __launch_bounds__(TILE_T, 1) k_local_tile(TileArgs a) {
   __shared__ uint32_t s_rp2[2][32];
   __shared__ int32_t s_bl[2][MAX_WIN], s_bo[2][MAX_WIN], s_so[2][MAX_WIN];  // rows' blocks; staged offsets
   __shared__ int s_stg[2];  // 1: the rows' blocks of every window are staged in stg
+  __shared__ __align__(16) int32_t s_rec[2][REC_W];  // fetched tile records
   __shared__ int s_row;
   __shared__ int s_wq[TILE_WARPS];  // per-warp survivor counters of the K8 scan (0 between scans)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -861,21 +891,20 @@ __global__ void __launch_bounds__(TILE_T, 1) k_local_tile(TileArgs a) {
     it = __shfl_sync(0xffffffffu, it, 0);
     if (lane == 0) s_it[b] = it;
     if (it >= a.hi) return;
-    const Tile T = a.tiles[it];
-    const BigC B = a.bcs[T.bc];
+    cp_async16(&s_rec[b][lane * 4], a.rec + it * REC_W + lane * 4);
+    cp_async_wait_all();
+    __syncwarp();
+    const int32_t *rc = s_rec[b];
     if (lane == 0) {
-      s_T[b] = T;
-      s_B[b] = B;
+      s_T[b] = Tile{rc[0], rc[1]};
+      s_B[b] = BigC{rc[2], rc[3], rc[4], rc[5], rc[6], rc[7]};
     }
-    const int r = T.j * 32 + lane;
-    const int32_t u = r < B.s ? a.vperm[B.vp_off + r] : -1;
-    s_ru2[b][lane] = u;
-    s_rp2[b][lane] = u >= 0 ? (uint32_t)a.psize[u] : 0u;
+    s_ru2[b][lane] = rc[64 + lane];
+    s_rp2[b][lane] = (uint32_t)rc[96 + lane];
     // the rows' packed blocks: copied to the staging buffer now (async), used by the build and
     // the probe of the tile's own slice
-    const int64_t sb = (int64_t)(B.sl_off + T.j) * nwin;
-    const int32_t bl = lane < nwin ? a.blk_len8[sb + lane] : 0;
-    const int32_t bo = lane < nwin ? a.blk_off8[sb + lane] : 0;
+    const int32_t bl = lane < nwin ? rc[8 + lane] : 0;
+    const int32_t bo = lane < nwin ? rc[24 + lane] : 0;
     int32_t incl = bl * 32;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -1586,6 +1615,15 @@ int local_knn(c2_ctx *ctx, const Csr &csr, int t, const Clusters &cl, int k, c2_
     }
   }
 
+  // ---- per-tile descriptor records
+  int32_t *trec = nullptr;
+  if (nslices > 0) {
+    trec = (int32_t *)ws_get(ctx, "tile_rec", (size_t)nslices * REC_W * 4, &rc);
+    if (rc) return rc;
+    k_tile_rec<<<nblk(nslices * 32), 256, 0, st>>>(tiles, nslices, bcs, vperm, vsize, blk_len8, blk_off8, nwin, trec);
+    C2_LAUNCHED(ctx, "k_tile_rec");
+  }
+
   // ---- tile kernel configuration
   TileKernel tk = nullptr;
   int grid = 0;
@@ -1603,7 +1641,7 @@ int local_knn(c2_ctx *ctx, const Csr &csr, int t, const Clusters &cl, int k, c2_
     // survivor queue per row: 256 entries where shared memory allows, at least 64*KS
     const int qmin = k <= 32 ? 64 : 128;
     qcap = 256;
-    const size_t budget = ctx->smem_optin - 2048;  // minus the kernel's static shared memory
+    const size_t budget = ctx->smem_optin - 4096;  // minus the kernel's static shared memory (~2.1 KB)
     const size_t rlw = fused ? (size_t)64 * k : 0;  // the rows' running lists (Cand = 2 words)
     const size_t stgw = 4096;  // staging of the next tile's row blocks: at least 16 KB
     while (qcap > qmin && ((size_t)K8Lay(smax, qcap).words + rlw + stgw) * 4 > budget) qcap -= 64;
@@ -1633,7 +1671,7 @@ int local_knn(c2_ctx *ctx, const Csr &csr, int t, const Clusters &cl, int k, c2_
   }
   auto launch_tiles = [&](int64_t lo, int64_t hi, int ci, const c2_cand *seed, c2_cand *dst) -> int {
     if (hi <= lo) return C2_OK;
-    TileArgs ta{tiles, lo, hi, counters + ci, bcs, vperm, vsize, blk_len8, blk_off8, packed, csr.psize, n, W, nwin, k,
+    TileArgs ta{tiles, lo, hi, counters + ci, bcs, vperm, vsize, trec, blk_len8, blk_off8, packed, csr.psize, n, W, nwin, k,
                 seed, dst, ctx->kstats, gscratch, smax, qcap, rl_off, stg_off, stg_cap, relabel ? 1 : 0};
     int g = (int)std::min<int64_t>(grid, hi - lo);
     cudaEvent_t e0 = nullptr, e1 = nullptr;
