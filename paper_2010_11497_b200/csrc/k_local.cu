@@ -1246,6 +1246,14 @@ __global__ void __launch_bounds__(TILE_T, 1) k_local_tile(TileArgs a) {
           ++nrow_b;
         }
       }
+      if (a.kstats) {  // pair evaluations of this row: its cluster-mates (debug work accounting)
+        int ev = s - 1;
+        if (slot) {
+          const int lo = r & ~(slot - 1);
+          ev = __popc(__ballot_sync(0xffffffffu, lane < slot && s_vid[lo + lane] >= 0)) - 1;
+        }
+        if (lane == 0) atomicAdd(&a.kstats[70], (unsigned long long)ev);
+      }
       if (a.kstats && lane == 0) {
         atomicAdd(&a.kstats[0], 1ull);
         atomicAdd(&a.kstats[1], m == 0 ? 1ull : 0ull);

@@ -402,3 +402,26 @@ def test_ctx_reuse_across_sizes():
             assert np.array_equal(npy(inter), o["inter"]) and np.array_equal(npy(uni), o["uni"]), cfg
     finally:
         c.close()
+
+
+@pytest.mark.parametrize("cfg", ["c1", "c3", "c4"])
+def test_pair_evaluations_equal_2P(ctx, cfg):
+    """Work accounting: the local kernel evaluates every ordered pair of
+    cluster-mates exactly once per row, i.e. 2P with P = sum over clusters of s(s-1)/2 computed
+    from the returned cluster arrays (C2_OPT_KSTATS counter 70)."""
+    C = synth.config(cfg)
+    offs, items = synth.generate(cfg)
+    ks = torch.zeros(80, dtype=torch.int64, device="cuda")
+    ctx.set_option(c2.OPT_KSTATS, ks.data_ptr())
+    try:
+        c2.build(dev(offs), dev(items), k=C.k, t=C.t, b=C.b, N=C.N, seed=C.hash_seed, ctx=ctx)
+        torch.cuda.synchronize()
+    finally:
+        ctx.set_option(c2.OPT_KSTATS, 0)
+    o = oracle.cluster(offs, items, oracle.hash_table(C.hash_seed, C.t, C.b, mval(items)), C.N)
+    P = 0
+    for f in range(C.t):
+        sz = np.diff(o["offsets"][f][: int(o["n_clusters"][f]) + 1]).astype(np.int64)
+        P += int((sz * (sz - 1) // 2).sum())
+    assert int(ks[70]) == 2 * P
+    assert ctx.stats()["pairs"] == P
