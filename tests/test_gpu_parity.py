@@ -425,3 +425,12 @@ def test_pair_evaluations_equal_2P(ctx, cfg):
         P += int((sz * (sz - 1) // 2).sum())
     assert int(ks[70]) == 2 * P
     assert ctx.stats()["pairs"] == P
+
+
+@pytest.mark.parametrize("k,n,N", [(50, 2600, 2600), (64, 3000, 1800), (33, 2300, 2300)])
+def test_build_big_clusters_large_k(ctx, k, n, N):
+    """Clusters past 2048 members (count matrix in global scratch) and k > 32 (two-register
+    running lists, 128-entry queues, round 1 on 64-candidate tops) against the oracle."""
+    rng = np.random.default_rng(k * 7 + n)
+    offs, items = synth.random_instance(rng, n, 400, 3, 60, zipf=0.8)
+    check_build(ctx, offs, items, 2, 1, N, k, 5)
