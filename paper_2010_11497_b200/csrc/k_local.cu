@@ -321,7 +321,8 @@ __global__ void k_sl_len(const Tile *__restrict__ tiles, int64_t nslices, const 
 __global__ void __launch_bounds__(256) k_sl_fill(int64_t nslices, const int32_t *__restrict__ bounds,
                                                  const int32_t *__restrict__ items, int32_t W, int nwin,
                                                  const int32_t *__restrict__ blk_len8,
-                                                 const int32_t *__restrict__ blk_off8, uint16_t *__restrict__ packed16) {
+                                                 const int32_t *__restrict__ blk_off8, uint16_t *__restrict__ packed16,
+                                                 int bank_order) {
   __shared__ int hist[8][32];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int64_t g = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -336,6 +337,20 @@ __global__ void __launch_bounds__(256) k_sl_fill(int64_t nslices, const int32_t 
     const int32_t pb = bd[w], pe = bd[w + 1];
     const int32_t len = blk_len8[sl * nwin + w] * 8;
     uint16_t *dst = packed16 + (int64_t)blk_off8[sl * nwin + w] * 256 + e * 8;
+    if (!bank_order) {  // plain order: one pass, ballot compaction
+      int cnt = 0;
+      for (int32_t p0 = pb; p0 < pe; p0 += 32) {
+        const int32_t p = p0 + lane;
+        const int32_t r = p < pe ? items[p] - lo : -1;
+        const bool in = r >= 0 && r < W;
+        const unsigned bal = __ballot_sync(0xffffffffu, in);
+        const int pos = cnt + __popc(bal & ((1u << lane) - 1));
+        if (in) dst[(pos >> 3) * 256 + (pos & 7)] = (uint16_t)r;
+        cnt += __popc(bal);
+      }
+      for (int pos = cnt + lane; pos < len; pos += 32) dst[(pos >> 3) * 256 + (pos & 7)] = (uint16_t)W;
+      continue;
+    }
     h[lane] = 0;
     __syncwarp();
     int cnt = 0;
@@ -1617,8 +1632,9 @@ int local_knn(c2_ctx *ctx, const Csr &csr, int t, const Clusters &cl, int k, c2_
       C2_TRY(stream_sync(ctx, "packed size"));
       packed = (uint4 *)ws_get(ctx, "packed", (size_t)tot8 * 32 * 16 + 16, &rc);
       if (rc) return rc;
+      // bank-rotated order pays for its second pass only when lists are long (one window)
       k_sl_fill<<<nblk(nslices * 32 * 32), 256, 0, st>>>(nslices, bounds, csr.items, W, nwin, blk_len8, blk_off8,
-                                                         reinterpret_cast<uint16_t *>(packed));
+                                                         reinterpret_cast<uint16_t *>(packed), nwin == 1 ? 1 : 0);
       C2_LAUNCHED(ctx, "k_sl_fill");
     }
   }
