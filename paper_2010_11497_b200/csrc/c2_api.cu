@@ -91,7 +91,7 @@ int build_device(c2_ctx *ctx, const int32_t *offs, const int32_t *items, int32_t
   c2_cand *fin = nullptr;
   C2_TRY(local_knn(ctx, sims, t, cl, k, run, true, &fin));
   if (ctx->timing) cudaEventRecord(ctx->ev[4], st);
-  C2_TRY(merge(ctx, 1, n, k, fin, nbr, inter, uni, sim));
+  C2_TRY(copyout(ctx, n, k, fin, nbr, inter, uni, sim));
   if (ctx->timing) cudaEventRecord(ctx->ev[5], st);
   return C2_OK;
 }

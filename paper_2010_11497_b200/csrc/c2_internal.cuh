@@ -99,7 +99,9 @@ int gf_encode(c2_ctx *ctx, const Csr &csr, const HashParams *hp, Csr *gf);
 int local_knn(c2_ctx *ctx, const Csr &csr, int t, const Clusters &cl, int k, c2_cand *out, bool fused,
               c2_cand **result);
 
-// Step 3 (k_merge.cu).
+// Step 3 (k_merge.cu).  copyout: c2_build's final format conversion of the fused running lists.
+int copyout(c2_ctx *ctx, int n, int k, const c2_cand *run, int32_t *nbr, uint16_t *inter, uint16_t *uni,
+            float *sim);
 int merge(c2_ctx *ctx, int t, int n, int k, const c2_cand *cand, int32_t *nbr, uint16_t *inter, uint16_t *uni,
           float *sim);
 

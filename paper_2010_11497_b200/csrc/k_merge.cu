@@ -79,6 +79,29 @@ __global__ void __launch_bounds__(128) k_merge(const c2_cand *__restrict__ cand,
   }
 }
 
+// c2_build's final step: the fused path's running lists are already Alg. 3's result (sorted
+// best-first, distinct ids, pads last), so the outputs are an element-wise format conversion
+// (coalesced; the same IEEE division for sim as k_merge).
+__global__ void k_copyout(const c2_cand *__restrict__ run, int64_t E, int32_t *__restrict__ nbr,
+                          uint16_t *__restrict__ inter, uint16_t *__restrict__ uni, float *__restrict__ sim) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= E) return;
+  const c2_cand c = run[e];
+  const bool real = c.id >= 0;
+  nbr[e] = real ? c.id : -1;
+  inter[e] = real ? c.inter : 0;
+  uni[e] = real ? c.uni : 0;
+  if (sim) sim[e] = real ? __fdiv_rn((float)c.inter, (float)c.uni) : 0.0f;
+}
+
+int copyout(c2_ctx *ctx, int n, int k, const c2_cand *run, int32_t *nbr, uint16_t *inter, uint16_t *uni,
+            float *sim) {
+  const int64_t E = (int64_t)n * k;
+  k_copyout<<<(unsigned)((E + 255) / 256), 256, 0, ctx->stream>>>(run, E, nbr, inter, uni, sim);
+  C2_LAUNCHED(ctx, "k_copyout");
+  return C2_OK;
+}
+
 int merge(c2_ctx *ctx, int t, int n, int k, const c2_cand *cand, int32_t *nbr, uint16_t *inter, uint16_t *uni,
           float *sim) {
   unsigned blocks = (unsigned)((n + 127) / 128);
