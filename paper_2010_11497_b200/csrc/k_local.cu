@@ -198,7 +198,7 @@ __global__ void k_singles(const uint32_t *__restrict__ sval_single, int64_t nsin
 // vperm: members of each big cluster sorted by |P_v| descending (ties by position).  One CTA
 // per cluster, bitonic sort in shared memory for s <= 2048 (larger clusters keep the
 // canonical order: performance only, results do not depend on it).
-__global__ void __launch_bounds__(1024) k_sl_sort(const BigC *__restrict__ bcs, const int32_t *__restrict__ bstart,
+__global__ void __launch_bounds__(256) k_sl_sort(const BigC *__restrict__ bcs, const int32_t *__restrict__ bstart,
                                                   const int32_t *__restrict__ members, int32_t n,
                                                   const int32_t *__restrict__ psize, int32_t *__restrict__ vperm,
                                                   int32_t *__restrict__ vsize) {
@@ -1562,7 +1562,7 @@ int local_knn(c2_ctx *ctx, const Csr &csr, int t, const Clusters &cl, int k, c2_
     if (nbig > 0) {
       k_bc_fill<<<nblk(nbig), 256, 0, st>>>(sval, nbig, cl.offsets, ccum, t, n, vp_scan, sl_scan, bcs, tiles, bstart);
       C2_LAUNCHED(ctx, "k_bc_fill");
-      k_sl_sort<<<(unsigned)nbig, 1024, 0, st>>>(bcs, bstart, cl.members, n, csr.psize, vperm, vsize);
+      k_sl_sort<<<(unsigned)nbig, 256, 0, st>>>(bcs, bstart, cl.members, n, csr.psize, vperm, vsize);
       C2_LAUNCHED(ctx, "k_sl_sort");
     }
     if (nmix > 0) {
