@@ -16,7 +16,7 @@ struct HashArgs {
 
 // G consecutive lanes share one user (its items are loaded once, broadcast to the group) and
 // lane g of the group handles function f0 + g, so a warp covers 32/G users.
-template <int G, bool TABLE>
+template <int G, bool TABLE, bool POW2>
 __global__ void __launch_bounds__(256) k_sketch(const int32_t *__restrict__ offs, const int32_t *__restrict__ items,
                                                 int32_t n, int t, int f0, uint32_t b, HashArgs ha,
                                                 const uint16_t *__restrict__ htab, int32_t m, int D,
@@ -44,7 +44,10 @@ __global__ void __launch_bounds__(256) k_sketch(const int32_t *__restrict__ offs
     }
   };
   auto hash = [&](uint32_t x) -> uint32_t {
-    return TABLE ? (active ? (uint32_t)__ldg(htab + (int64_t)f * m + x) : C2_ABSENT16) : c2d::item_hash(ca, cc, x, b);
+    if (TABLE) return active ? (uint32_t)__ldg(htab + (int64_t)f * m + x) : C2_ABSENT16;
+    // h(x) = floor(z * b / 2^64): for b = 2^M (every config) the top M bits of z = a*x + c
+    if (POW2) return (uint32_t)((ca * (uint64_t)x + cc) >> (65 - __ffs(b)));  // b >= 2
+    return c2d::item_hash(ca, cc, x, b);
   };
   // eight items in flight per step (the loads do not depend on the insertions)
   int32_t p = p0;
@@ -76,11 +79,14 @@ static int launch_sketch(c2_ctx *ctx, const Csr &csr, int t, int f0, int b, cons
                          const uint16_t *htab, int32_t m, int D, uint16_t *out) {
   unsigned blocks = (unsigned)(((int64_t)csr.n * G + 255) / 256);
   if (htab)
-    k_sketch<G, true><<<blocks, 256, 0, ctx->stream>>>(csr.offs, csr.items, csr.n, t, f0, (uint32_t)b, ha, htab, m,
+    k_sketch<G, true, false><<<blocks, 256, 0, ctx->stream>>>(csr.offs, csr.items, csr.n, t, f0, (uint32_t)b, ha, htab, m,
                                                        D, out);
+  else if (b >= 2 && (b & (b - 1)) == 0)
+    k_sketch<G, false, true><<<blocks, 256, 0, ctx->stream>>>(csr.offs, csr.items, csr.n, t, f0, (uint32_t)b, ha,
+                                                              nullptr, 0, D, out);
   else
-    k_sketch<G, false><<<blocks, 256, 0, ctx->stream>>>(csr.offs, csr.items, csr.n, t, f0, (uint32_t)b, ha, nullptr,
-                                                        0, D, out);
+    k_sketch<G, false, false><<<blocks, 256, 0, ctx->stream>>>(csr.offs, csr.items, csr.n, t, f0, (uint32_t)b, ha,
+                                                               nullptr, 0, D, out);
   C2_LAUNCHED(ctx, "k_sketch");
   return C2_OK;
 }
