@@ -12,18 +12,20 @@
 //              [p/8][lane][8] and padded to the slice's longest list with W (M[W] == 0).
 //    A warp then streams the 32 lists of a slice with one 16-byte coalesced load per lane per
 //    8 items, with no divergence and no bounds checks.
-// K7 k_local_tile: persistent CTAs, one work item = one slice R (32 rows) of cluster C.  For
-//    every item window, shared memory holds the transposed membership mask M[x] = {r in R :
-//    x in P_r} (bit r).  Each thread owns VPT slices' lanes (one v each) and accumulates the
-//    32 counts |P_r ∩ P_v| bit-sliced with Harley-Seal carry-save adders over 16 masks, so
-//    one LDS + ~3 LOP3 serve 32 pairs.  A 32x32 bit transpose turns the planes into counts.
-// K8 (in K7): exact top-k per row under the order i1*U2 > i2*U1, ties by lower id.  Lane =
-//    row, the 16 warps scan interleaved candidate segments: round 1 keeps each thread's best
-//    2 (4 if k > 32) -> 32 (64) "tops" per row, whose k-th best T_r is a valid lower bound of
-//    the row's k-th best; round 2 queues the few candidates >= T_r; one warp sorts the queue.
-//    In fused mode (c2_build) candidates must also beat tau = the running Alg. 3 result's
-//    k-th best (it never decreases, so the pruning is exact); the queue is merged with that
-//    running list (duplicate ids dropped) instead of being written as a per-function list.
+// K7 k_local_tile: persistent CTAs (one per SM), one work item = one slice R (32 rows) of cluster
+//    C.  For every item window, shared memory holds the transposed membership mask M[x] =
+//    {r in R : x in P_r} (bit r).  Each thread owns VPT slices' lanes (one v each) and
+//    accumulates the 32 counts |P_r ∩ P_v| bit-sliced with carry-save adders over 16 masks, so
+//    one LDS + ~4 LOP3 serve 32 pairs.  A 32x32 bit transpose turns the planes into counts,
+//    stored as cnt[row][member] in shared memory aliased onto the dead M.  The next tile's
+//    descriptor record, row blocks and running lists arrive by cp.async during this tile.
+// K8 (in K7): exact top-k per row under the order i1*U2 > i2*U1, ties by lower id; one warp per
+//    row (rows taken dynamically).  A candidate must beat tau = the row's running Alg. 3 k-th
+//    best (fused mode; it never decreases, so the pruning is exact) -- a 2-IMAD test; rows
+//    without a full running list, or whose tau lets more than 64 through, first get a bound
+//    from round 1 (each lane's best two -> the k-th best of those 64).  Survivors go to a
+//    private queue, then are inserted one by one (<= 16) or sorted on exact 64-bit keys and
+//    merged into the running list in place, duplicate ids dropped.
 #include <algorithm>
 #include <vector>
 
