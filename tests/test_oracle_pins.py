@@ -444,3 +444,39 @@ def test_rejects_malformed_csr():
         items = np.asarray([x for r in rows for x in r], np.int32)
         with pytest.raises(ValueError):
             oracle.frh(offs, items, np.zeros((1, 8), np.uint16))
+
+
+# ----------------------------------------------------------------- round-2 pins
+def test_item_hash_bigint_non_power_of_two_b():
+    # A1/A26: h(x) = floor(((a*x + c) mod 2^64) * b / 2^64) for ANY 1 <= b <= 32768, written
+    # here with Python's exact big integers (a third, independent implementation).  A 32-bit
+    # (Lemire-style) reduction or a modulo reduction fails this for non-power-of-two b.
+    rng = np.random.default_rng(11)
+    bs = [3, 5, 7, 10, 100, 1000, 1023, 1025, 3000, 4095, 4097, 10007, 32767]
+    for _ in range(400):
+        a, c = (int(v) for v in rng.integers(0, 2**63, 2))
+        a = a * 2 + 1
+        x = int(rng.integers(0, 2**31))
+        for b in bs:
+            z = (a * x + c) % 2**64
+            assert oracle.item_hash(a, c, x, b) == (z * b) >> 64
+    # and the table the oracle builds from its SplitMix64 parameters uses the same rule
+    a, c = oracle.hash_params(42, 3)
+    tab = oracle.hash_table(42, 3, 1000, 500)
+    for f in range(3):
+        for x in (0, 1, 2, 17, 499):
+            z = (int(a[f]) * x + int(c[f])) % 2**64
+            assert int(tab[f][x]) == (z * 1000) >> 64
+
+
+def test_a7_fold_hand_built():
+    g = gold("a7_fold.json")
+    offs, items = csr(g["profiles"])
+    htab = np.asarray([g["h"]], np.uint16)
+    for form in (0, 1):  # recursive and prefix-trie formulations
+        cl = oracle.cluster(offs, items, htab, g["N"], form)
+        got = [cl["members"][0][cl["offsets"][0][c]:cl["offsets"][0][c + 1]].tolist()
+               for c in range(cl["n_clusters"][0])]
+        assert got == g["expected_clusters"], form
+        assert cl["stats"]["split_nodes"] == g["expected_split_nodes"]
+        assert cl["stats"]["folded_singletons"] == g["expected_folded_singletons"]
