@@ -23,6 +23,9 @@
  *  - CSR input: csr_offsets dev int32[n_users+1] (offsets[0] = 0), item_ids dev int32[nnz],
  *    each row non-empty, strictly ascending, ids >= 0, |P_u| <= 32767 (A17, A18, A28).
  *    Rows violating this make the call return C2_EDATA (first bad row in c2_last_error).
+ *    Any id in [0, 2^31) is accepted; Step 2 renames ids densely (order-preserving, which leaves
+ *    every intersection unchanged) when they exceed its 800,000-id window range, and returns
+ *    C2_EDATA if the CSR holds more than 800,000 DISTINCT item ids.
  *  - Scalars: 1 <= t <= 64; 1 <= b <= 32768 (A26); N >= 2 (A27); 1 <= k <= 64;
  *    1 <= n_users < 2^29; t * n_users < 2^31.  Otherwise C2_EINVAL, nothing enqueued.
  *  - Errors: integer codes below; c2_last_error() describes the last failure of that ctx.
@@ -118,7 +121,8 @@ C2_API int c2_fastrandomhash(c2_ctx *ctx, const int32_t *csr_offsets, const int3
                       int32_t t, int32_t b, int32_t max_cluster_N, uint64_t seed, c2_clusters *out);
 
 /* As c2_fastrandomhash but h_f(x) = htab[f*m + x] (dev uint16 [t][m], values < b), for the
- * paper's worked examples.  Item ids must be < m. */
+ * paper's worked examples.  Item ids must be < m (else C2_EDATA); a table
+ * value >= b returns C2_EINVAL (checked on the device, one extra stream synchronisation). */
 C2_API int c2_fastrandomhash_table(c2_ctx *ctx, const int32_t *csr_offsets, const int32_t *item_ids, int32_t n_users,
                             int32_t t, int32_t b, int32_t max_cluster_N, const uint16_t *htab, int32_t m,
                             c2_clusters *out);
@@ -134,7 +138,8 @@ C2_API int c2_sketch(c2_ctx *ctx, const int32_t *csr_offsets, const int32_t *ite
  * users v in C \ {u} under the order "v1 before v2 iff i1*U2 > i2*U1, ties by lower id"
  * (i = |P_u ∩ P_v|, U = |P_u ∪ P_v|; A13-A15), padded with {-1,0,0}.
  * cand: dev [t][n_users][k], list of (f,u) at cand[(f*n_users + u)*k].  `clusters` must be
- * a canonical assignment of the same CSR (e.g. from c2_fastrandomhash; n_clusters host).
+ * a canonical assignment of the same CSR (e.g. from c2_fastrandomhash; n_clusters host); all
+ * four of its pointers are required (NULL -> C2_EINVAL).
  * sim_mode C2_SIM_GF1024 uses the fingerprints derived from `seed` (A19). */
 C2_API int c2_local_knn(c2_ctx *ctx, const int32_t *csr_offsets, const int32_t *item_ids, int32_t n_users, int32_t t,
                  const c2_clusters *clusters, int32_t k, int32_t sim_mode, uint64_t seed, c2_cand *cand);

@@ -228,9 +228,14 @@ def split_cand(cand):
 
 def merge(cand, k=None, with_sim=True, ctx: Context | None = None):
     import torch
+    if not (cand.is_cuda and cand.dtype == torch.int32 and cand.is_contiguous() and cand.dim() == 4
+            and cand.shape[3] == 2):
+        raise TypeError("cand must be a contiguous int32 CUDA tensor [t][n][k][2] (c2_cand records)")
     ctx = ctx or default_context(cand.device.index or 0)
     t, n, kk, _ = cand.shape
-    k = kk if k is None else k
+    if k is not None and k != kk:
+        raise ValueError(f"k={k} differs from the list length cand.shape[2]={kk} (c2_merge uses k as both)")
+    k = kk
     dev = cand.device
     nbr = torch.empty((n, k), dtype=torch.int32, device=dev)
     inter = torch.empty((n, k), dtype=torch.uint16, device=dev)

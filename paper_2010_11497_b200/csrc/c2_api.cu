@@ -62,6 +62,14 @@ __global__ void k_cl_maxsize(const int32_t *__restrict__ offsets, int t, int32_t
   if ((threadIdx.x & 31) == 0) atomicMax(out, v);
 }
 
+__global__ void k_u16_max(const uint16_t *__restrict__ x, int64_t E, int32_t *__restrict__ out) {
+  int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  int v = e < E ? (int)x[e] : 0;
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v = max(v, __shfl_xor_sync(0xffffffffu, v, o));
+  if ((threadIdx.x & 31) == 0) atomicMax(out, v);
+}
+
 float ev_ms(cudaEvent_t a, cudaEvent_t b) {
   float ms = 0;
   cudaEventElapsedTime(&ms, a, b);
@@ -199,6 +207,19 @@ static int frh_common(c2_ctx *ctx, const int32_t *offs, const int32_t *items, in
   Csr csr{offs, items, n, -1, 0, 0, nullptr};
   C2_TRY(validate_csr(ctx, &csr));
   if (htab && csr.max_item >= m) return set_err(ctx, C2_EDATA, "item id %d >= table width m=%d", csr.max_item, m);
+  if (htab) {  // every table value must be a bucket in [0, b) (it indexes per-bucket histograms)
+    int rc;
+    int32_t *mx = (int32_t *)ws_get(ctx, "htab_max", 4, &rc);
+    if (rc) return rc;
+    C2_CUDA(ctx, cudaMemsetAsync(mx, 0, 4, ctx->stream));
+    const int64_t E = (int64_t)t * m;
+    k_u16_max<<<(unsigned)((E + 255) / 256), 256, 0, ctx->stream>>>(htab, E, mx);
+    C2_LAUNCHED(ctx, "k_u16_max");
+    int32_t hmx = 0;
+    C2_CUDA(ctx, cudaMemcpyAsync(&hmx, mx, 4, cudaMemcpyDeviceToHost, ctx->stream));
+    C2_TRY(stream_sync(ctx, "table check"));
+    if (hmx >= b) return set_err(ctx, C2_EINVAL, "hash table value %d >= b=%d", hmx, b);
+  }
   HashParams hp;
   make_hash_params(seed, t, &hp);
   Clusters cl;
@@ -226,8 +247,8 @@ int c2_local_knn(c2_ctx *ctx, const int32_t *csr_offsets, const int32_t *item_id
                  const c2_clusters *clusters, int32_t k, int32_t sim_mode, uint64_t seed, c2_cand *cand) {
   C2_TRY(check_common(ctx, csr_offsets, item_ids, n_users, t));
   C2_TRY(check_k(ctx, k, sim_mode));
-  if (!clusters || !clusters->offsets || !clusters->members || !clusters->n_clusters || !cand)
-    return set_err(ctx, C2_EINVAL, "NULL clusters or cand");
+  if (!clusters || !clusters->offsets || !clusters->members || !clusters->cluster_of || !clusters->n_clusters || !cand)
+    return set_err(ctx, C2_EINVAL, "NULL clusters (offsets, members, cluster_of, n_clusters) or cand");
   begin(ctx);
   Csr csr{csr_offsets, item_ids, n_users, -1, 0, 0, nullptr};
   C2_TRY(validate_csr(ctx, &csr));

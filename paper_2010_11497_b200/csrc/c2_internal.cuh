@@ -28,7 +28,7 @@ struct c2_ctx {
   bool sync_check = false;
   bool timing = false;
   unsigned long long *kstats = nullptr;
-  bool relabel = true;  // C2_OPT_RELABEL  // C2_OPT_KSTATS: dev [16] K7/K8 counters
+  bool relabel = true;  // C2_OPT_RELABEL  (C2_OPT_KSTATS: kstats = dev [80] K7/K8 counters)
   c2_stats stats{};
   // device workspace: name -> (ptr, bytes); grow-only
   std::map<std::string, std::pair<void *, size_t>> ws;
@@ -95,7 +95,7 @@ int fastrandomhash(c2_ctx *ctx, const Csr &csr, int t, int b, int64_t N, const H
 // Step 2 (k_local.cu).
 int gf_encode(c2_ctx *ctx, const Csr &csr, const HashParams *hp, Csr *gf);
 // fused=false: cand [t][n][k] per-function lists (c2_local_knn).  fused=true: out = the running
-// final lists (2*n*k entries, ping-pong; Alg. 3 applied function by function, c2_build).
+// final lists [n][k], updated in place function by function (Alg. 3 fused, c2_build).
 int local_knn(c2_ctx *ctx, const Csr &csr, int t, const Clusters &cl, int k, c2_cand *out, bool fused,
               c2_cand **result);
 

@@ -309,12 +309,14 @@ int validate_csr(c2_ctx *ctx, Csr *csr) {
   int blocks = ctx->num_sms * 8;
   k_validate<<<blocks, 256, 0, ctx->stream>>>(csr->offs, csr->items, csr->n, psize, flags);
   C2_LAUNCHED(ctx, "k_validate");
-  int32_t h[4];
+  int32_t h[5];
   C2_CUDA(ctx, cudaMemcpyAsync(h, flags, 16, cudaMemcpyDeviceToHost, ctx->stream));
+  C2_CUDA(ctx, cudaMemcpyAsync(h + 4, csr->offs + csr->n, 4, cudaMemcpyDeviceToHost, ctx->stream));
   C2_TRY(stream_sync(ctx, "validate"));
   if (h[0] != INT32_MAX)
     return set_err(ctx, C2_EDATA, "CSR row %d violates the input rules (empty, unsorted, duplicate, negative id or "
                    "|P_u| > 32767)", h[0]);
+  csr->nnz = h[4];
   csr->max_item = h[1];
   csr->max_len = h[2];
   csr->psize = psize;
