@@ -20,7 +20,8 @@ import os
 import threading
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "lib", "libc2.so")
+# C2_LIB: dev override for A/B runs of a variant build of the same sources (tools/ab.sh)
+LIB_PATH = os.environ.get("C2_LIB") or os.path.join(HERE, "lib", "libc2.so")
 HEADER = os.path.join(os.path.dirname(HERE), "include", "c2.h")
 
 C2_OK, C2_EINVAL, C2_EDATA, C2_ENOMEM, C2_ECUDA = 0, -1, -2, -3, -4

@@ -36,14 +36,17 @@ def up_to_date() -> bool:
     return all(os.path.getmtime(d) <= t for d in _deps())
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and up_to_date():
+def build(force: bool = False, verbose: bool = False, out: str | None = None, defines=()) -> str:
+    """Build libc2.so; `out`/`defines` build a variant (-D flags) elsewhere for A/B timing runs."""
+    lib = out or LIB
+    if not force and not out and up_to_date():
         return LIB
-    os.makedirs(os.path.join(LIBDIR, "obj"), exist_ok=True)
+    objdir = os.path.join(LIBDIR, "obj" if not out else "obj_" + os.path.basename(out).replace(".so", ""))
+    os.makedirs(objdir, exist_ok=True)
 
     def compile_one(src):
-        obj = os.path.join(LIBDIR, "obj", os.path.basename(src) + ".o")
-        cmd = [NVCC, *ARCH, *FLAGS, "-c", src, "-o", obj]
+        obj = os.path.join(objdir, os.path.basename(src) + ".o")
+        cmd = [NVCC, *ARCH, *FLAGS, *[f"-D{d}" for d in defines], "-c", src, "-o", obj]
         if verbose:
             cmd += ["-Xptxas", "-v"]
         r = subprocess.run(cmd, capture_output=True, text=True)
@@ -56,14 +59,17 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if verbose:
         for _, err in res:
             sys.stderr.write(err)
-    tmp = LIB + f".tmp{os.getpid()}"
+    tmp = lib + f".tmp{os.getpid()}"
     cmd = [NVCC, *ARCH, "-shared", "-o", tmp] + [o for o, _ in res] + ["-Xcompiler", "-fPIC"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stderr}")
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, lib)
+    return lib
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="--verbose" in sys.argv))
+    args = sys.argv[1:]
+    out = args[args.index("--out") + 1] if "--out" in args else None
+    defs = [a[2:] for a in args if a.startswith("-D")]
+    print(build(force="--force" in args, verbose="--verbose" in args, out=out, defines=defs))

@@ -31,6 +31,13 @@
 
 #include "c2_internal.cuh"
 
+#ifndef C2_EPI
+#define C2_EPI 0  // 1: light rows filtered in the phase-A epilogue (measured slower)
+#endif
+#ifndef C2_RANKMERGE
+#define C2_RANKMERGE 1  // 1: rank-based Alg. 3 step for <= 32 survivors; 0: insertion (<= 16)
+#endif
+
 namespace c2 {
 
 // A cluster processed by the tile kernel: either one big cluster (slot == 0; members in
@@ -53,7 +60,16 @@ __device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
 }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
-constexpr int TILE_T = 512;
+#ifndef C2_TILE_T
+#define C2_TILE_T 512
+#endif
+#ifndef C2_TILE_MINB
+#define C2_TILE_MINB 1
+#endif
+#ifndef C2_SMEM_BUDGET
+#define C2_SMEM_BUDGET 0  // bytes of dynamic shared memory per tile CTA (0: the opt-in maximum)
+#endif
+constexpr int TILE_T = C2_TILE_T;
 constexpr int TILE_WARPS = TILE_T / 32;
 constexpr int MAX_WIN = 16;
 
@@ -743,6 +759,50 @@ __device__ __forceinline__ void merge_kc(KC (&x)[R]) {
   for (int j = 0; j < R; ++j) x[j] = t.e[j];
 }
 
+// One Alg. 3 step for one row, by ranks: the m <= 32 queued survivors Q (distinct ids, unsorted)
+// and the running list S (best first; its real entries are a prefix, pads have id -1) give
+// dst[0..kk) = the first kk distinct ids of S ∪ Q under the order (A13, A16).  A survivor whose id
+// is already in S carries identical (i, U) and is dropped.  Every element's output position is
+// (its rank in S) + (its rank among the kept survivors): O((|S| + m) * m / 32) exact cross-multiplied
+// comparisons per lane, all independent (no sorting network, no 64-bit keys).
+template <int KS>
+__device__ __forceinline__ void rank_merge(const Cand *qr, int m, const c2_cand *S, int kk, c2_cand *dst) {
+  const int lane = threadIdx.x & 31;
+  Cand sv[KS];
+  int nS = 0;
+#pragma unroll
+  for (int j = 0; j < KS; ++j) {
+    sv[j] = (32 * j + lane < kk) ? from_out(S[32 * j + lane]) : sent();
+    nS += __popc(__ballot_sync(0xffffffffu, is_real(sv[j])));
+  }
+  const Cand q = lane < m ? qr[lane] : sent();
+  int rs = 0;
+  bool dup = false;
+  for (int i = 0; i < nS; ++i) {  // rank of q in S (broadcast reads)
+    const Cand si = from_out(S[i]);
+    dup |= si.id == q.id;
+    rs += better_c(si, q) ? 1 : 0;
+  }
+  const unsigned dm = __ballot_sync(0xffffffffu, lane < m && dup);
+  int rq = 0, sh[KS];
+#pragma unroll
+  for (int j = 0; j < KS; ++j) sh[j] = 0;
+  for (int j = 0; j < m; ++j) {
+    const Cand o = shfl_c(q, j);
+    if ((dm >> j) & 1u) continue;  // (uniform)
+    rq += better_c(o, q) ? 1 : 0;
+#pragma unroll
+    for (int jj = 0; jj < KS; ++jj) sh[jj] += better_c(o, sv[jj]) ? 1 : 0;
+  }
+  if (lane < m && !dup && rs + rq < kk) dst[rs + rq] = to_out(q);
+#pragma unroll
+  for (int jj = 0; jj < KS; ++jj) {
+    const int i = 32 * jj + lane;
+    if (i < nS && i + sh[jj] < kk) dst[i + sh[jj]] = to_out(sv[jj]);
+  }
+  for (int p = nS + m - __popc(dm) + lane; p < kk; p += 32) dst[p] = c2_cand{-1, 0, 0};
+}
+
 // ------------------------------------------------------------------ K7 tile kernel
 __device__ __forceinline__ void csa(uint32_t &h, uint32_t &l, uint32_t a, uint32_t b, uint32_t c) {
   uint32_t u = a ^ b;
@@ -751,7 +811,7 @@ __device__ __forceinline__ void csa(uint32_t &h, uint32_t &l, uint32_t a, uint32
 }
 
 // in-register 32x32 bit transpose: A[p] bit r -> A[r] bit p
-__device__ __forceinline__ void transpose32(uint32_t (&A)[32]) {
+__device__ __forceinline__ void transpose32_body(uint32_t (&A)[32]) {
 #pragma unroll
   for (int j = 16, mi = 0; j != 0; j >>= 1, ++mi) {
     const uint32_t m = mi == 0 ? 0x0000FFFFu : mi == 1 ? 0x00FF00FFu : mi == 2 ? 0x0F0F0F0Fu : mi == 3 ? 0x33333333u
@@ -765,6 +825,29 @@ __device__ __forceinline__ void transpose32(uint32_t (&A)[32]) {
       }
     }
   }
+}
+
+#ifndef C2_TRANSPOSE_NI
+#define C2_TRANSPOSE_NI 1  // one out-of-line transpose body instead of VPT inlined copies (i-cache)
+#endif
+struct U32x32 {
+  uint32_t v[32];
+};
+__device__ __noinline__ U32x32 transpose32_ni(U32x32 a) {
+  transpose32_body(a.v);
+  return a;
+}
+__device__ __forceinline__ void transpose32(uint32_t (&A)[32]) {
+#if C2_TRANSPOSE_NI
+  U32x32 t;
+#pragma unroll
+  for (int i = 0; i < 32; ++i) t.v[i] = A[i];
+  t = transpose32_ni(t);
+#pragma unroll
+  for (int i = 0; i < 32; ++i) A[i] = t.v[i];
+#else
+  transpose32_body(A);
+#endif
 }
 
 // Shared-memory layout of the K8 phase (32-bit words), aliased onto the M region once phase A
@@ -877,7 +960,7 @@ __device__ __forceinline__ bool passes(uint32_t i, uint32_t ps, int32_t id, cons
 }
 
 template <int NHI, int VPT, int KS, bool SMEM_CNT>
-__global__ void __launch_bounds__(TILE_T, 1) k_local_tile(TileArgs a) {
+__global__ void __launch_bounds__(TILE_T, C2_TILE_MINB) k_local_tile(TileArgs a) {
   constexpr int R1 = 2 * KS;
   const int qcap = a.qcap;
   extern __shared__ __align__(16) uint32_t dyn[];
@@ -893,6 +976,9 @@ __global__ void __launch_bounds__(TILE_T, 1) k_local_tile(TileArgs a) {
   __shared__ __align__(16) int32_t s_rec[2][REC_W];  // fetched tile records
   __shared__ int s_row;
   __shared__ int s_wq[TILE_WARPS];  // per-warp survivor counters of the K8 scan (0 between scans)
+  __shared__ uint4 s_ref[32];       // light rows: the running k-th best as a Ref (see make_ref)
+  __shared__ int s_qn[32];          // light rows: survivors queued by the phase-A epilogue
+  __shared__ unsigned s_light;      // rows whose running list is full (fused big-cluster tiles)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   if (tid < TILE_WARPS) s_wq[tid] = 0;
   for (int i = tid; i < a.W + 1; i += TILE_T) M[i] = 0;
@@ -968,6 +1054,11 @@ __global__ void __launch_bounds__(TILE_T, 1) k_local_tile(TileArgs a) {
     uint32_t *s_vps = kb + lay.vps;
     Cand *s_q = reinterpret_cast<Cand *>(kb + lay.que);
     if (tid == 0) s_row = 0;
+    if (tid < 32) s_qn[tid] = 0;
+    // light rows: fused mode, big cluster (no slot groups), running list already full.  Their
+    // candidates are filtered against the running k-th best right after the transpose, while
+    // the counts are still in the thread that made them; K8 then skips their scan.
+    const bool epi = C2_EPI && a.seed != nullptr && B.slot == 0;
     // the rows' running lists (fused mode): loaded now, first used in K8 after phase A
     if (a.seed)
       for (int r = warp; r < nr; r += TILE_WARPS) {
@@ -1034,6 +1125,7 @@ __global__ void __launch_bounds__(TILE_T, 1) k_local_tile(TileArgs a) {
           atomicAdd(&a.kstats[64], (unsigned long long)(clock64() - ckpb));
           atomicAdd(&a.kstats[65], (unsigned long long)nsteps);
         }
+        if (epi && w == nwin - 1) cp_async_wait_all();  // the rows' running lists (issued at tile start)
         __syncthreads();
         if (a.kstats) ckp += clock64();
         // ---- clear M
@@ -1044,6 +1136,16 @@ __global__ void __launch_bounds__(TILE_T, 1) k_local_tile(TileArgs a) {
 #pragma unroll
           for (int q = 0; q < 8; ++q)
             if (xs[q] < W) M[xs[q]] = 0;
+        }
+        if (epi && w == nwin - 1 && warp == TILE_WARPS - 1) {
+          const int r = lane;
+          const bool light = r < nr && s_ru[r] >= 0 && s_run[r * kk + kk - 1].id >= 0;
+          if (light) {
+            const Ref R = make_ref(from_out(s_run[r * kk + kk - 1]), s_rp[r], false);
+            s_ref[r] = make_uint4(R.A, R.B, R.iT, R.idlim);
+          }
+          const unsigned lm = __ballot_sync(0xffffffffu, light);
+          if (lane == 0) s_light = lm;
         }
         __syncthreads();
       }
@@ -1067,6 +1169,25 @@ __global__ void __launch_bounds__(TILE_T, 1) k_local_tile(TileArgs a) {
 #pragma unroll
           for (int r = 0; r < 32; ++r)
             if (r < nr) cnt[r * lay.RS + vi] = (uint16_t)A[r];
+          if (epi) {
+            // light rows: candidate (v, i, |P_v|) survives iff strictly better than the row's
+            // running k-th best (passes() with idlim = id_T), i.e. it would enter the list
+            const unsigned lm = s_light;
+            if (lm && vi < s) {
+              const int32_t idv = vp[vi];
+              const uint32_t psv = (uint32_t)a.vsize[B.vp_off + vi];
+              for (unsigned q2 = lm; q2; q2 &= q2 - 1) {
+                const int r = __ffs(q2) - 1;
+                const uint32_t i = cnt[r * lay.RS + vi];
+                const uint4 R = s_ref[r];
+                const uint32_t l = i * R.x, rr = R.z * psv + R.y;
+                if (l >= rr && (l > rr || (uint32_t)idv < R.w) && vi != r0 + r) {
+                  const int p = atomicAdd(&s_qn[r], 1);
+                  if (p < qcap) s_q[r * qcap + p] = Cand{i | ((s_rp[r] + psv - i) << 16), idv};
+                }
+              }
+            }
+          }
         }
       }
     }
@@ -1216,7 +1337,9 @@ __global__ void __launch_bounds__(TILE_T, 1) k_local_tile(TileArgs a) {
         ck_r1 += c - ckr;
         ckr = c;
       }
-      int m = scan(T);
+      const bool light = epi && ((s_light >> r) & 1u);
+      int m = light ? s_qn[r] : 0;
+      if (!light || m > qcap) m = scan(T);  // (a light row whose queue overflowed rescans)
       zq = reinterpret_cast<uint32_t *>(qr);
       zn = 2 * min(m, qcap);
       if (a.kstats && lane == 0) atomicAdd(&a.kstats[16 + min(m, 300) / 20], 1ull);
@@ -1285,7 +1408,12 @@ __global__ void __launch_bounds__(TILE_T, 1) k_local_tile(TileArgs a) {
       }
       if (a.seed && m == 0) continue;
       c2_cand *dst = a.seed ? a.out + (int64_t)u * kk : a.out + ((int64_t)B.f * a.n + u) * kk;
-      if (a.seed && m <= 16) {
+      if (C2_RANKMERGE && a.seed && m <= 32) {
+        // few survivors: Alg. 3 step by ranks (no sorting network, no f64 keys)
+        rank_merge<KS>(qr, m, s_run + r * kk, kk, dst);
+        continue;
+      }
+      if (!C2_RANKMERGE && a.seed && m <= 16) {
         // few survivors (one insertion ~20 instructions, sort-32 + merge-64 ~320): insert them one
         // by one into the running list (duplicates skipped)
         KC S[KS];
@@ -1464,10 +1592,68 @@ __global__ void k_work_steps(const int32_t *__restrict__ offsets, const int32_t 
   if ((threadIdx.x & 31) == 0 && w) atomicAdd(acc, w);
 }
 
-int local_knn(c2_ctx *ctx, const Csr &csr, int t, const Clusters &cl, int k, c2_cand *out, bool fused,
+// ------------------------------------------------------------------ item-id compaction
+// Step 2 streams window-local item ids; ids beyond MAX_WIN windows are first renamed densely in
+// increasing order (rank among the distinct ids present).  An injective renaming leaves every
+// |P_u ∩ P_v| unchanged and keeps rows sorted; |P_u| (psize) is untouched.
+__global__ void k_mark_items(const int32_t *__restrict__ items, int64_t nnz, uint32_t *__restrict__ bm) {
+  int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p < nnz) {
+    const uint32_t x = (uint32_t)items[p];
+    atomicOr(&bm[x >> 5], 1u << (x & 31));
+  }
+}
+__global__ void k_word_pop(const uint32_t *__restrict__ bm, int64_t nw, int32_t *__restrict__ wc) {
+  int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (w < nw) wc[w] = __popc(bm[w]);
+}
+__global__ void k_remap_items(const int32_t *__restrict__ items, int64_t nnz, const uint32_t *__restrict__ bm,
+                              const int32_t *__restrict__ wbase, int32_t *__restrict__ out) {
+  int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p < nnz) {
+    const uint32_t x = (uint32_t)items[p];
+    out[p] = wbase[x >> 5] + __popc(bm[x >> 5] & ((1u << (x & 31)) - 1u));
+  }
+}
+
+static int compact_items(c2_ctx *ctx, Csr *csr) {
+  int rc;
+  cudaStream_t st = ctx->stream;
+  const int64_t nw = ((int64_t)csr->max_item + 32) / 32;
+  uint32_t *bm = (uint32_t *)ws_get(ctx, "cmp_bitmap", (size_t)nw * 4, &rc);
+  if (rc) return rc;
+  int32_t *wc = (int32_t *)ws_get(ctx, "cmp_wc", (size_t)(2 * nw + 2) * 4, &rc);
+  if (rc) return rc;
+  int32_t *wbase = wc + nw + 1;
+  int32_t *out = (int32_t *)ws_get(ctx, "cmp_items", (size_t)csr->nnz * 4, &rc);
+  if (rc) return rc;
+  C2_CUDA(ctx, cudaMemsetAsync(bm, 0, (size_t)nw * 4, st));
+  k_mark_items<<<nblk(csr->nnz), 256, 0, st>>>(csr->items, csr->nnz, bm);
+  C2_LAUNCHED(ctx, "k_mark_items");
+  k_word_pop<<<nblk(nw), 256, 0, st>>>(bm, nw, wc);
+  C2_LAUNCHED(ctx, "k_word_pop");
+  C2_TRY(scan_exclusive(ctx, wc, wbase, nw));
+  k_remap_items<<<nblk(csr->nnz), 256, 0, st>>>(csr->items, csr->nnz, bm, wbase, out);
+  C2_LAUNCHED(ctx, "k_remap_items");
+  int32_t distinct = 0;
+  C2_CUDA(ctx, cudaMemcpyAsync(&distinct, wbase + nw, 4, cudaMemcpyDeviceToHost, st));
+  C2_TRY(stream_sync(ctx, "item compaction"));
+  csr->items = out;
+  csr->max_item = distinct - 1;
+  return C2_OK;
+}
+
+int local_knn(c2_ctx *ctx, const Csr &csr_in, int t, const Clusters &cl, int k, c2_cand *out, bool fused,
               c2_cand **result) {
   int rc;
   cudaStream_t st = ctx->stream;
+  Csr csr = csr_in;
+  if ((int64_t)csr.max_item + 1 > (int64_t)MAX_WIN * 50000) {
+    C2_TRY(compact_items(ctx, &csr));
+    if ((int64_t)csr.max_item + 1 > (int64_t)MAX_WIN * 50000)
+      return set_err(ctx, C2_EDATA, "Step 2 supports at most %d distinct item ids (got %d)", MAX_WIN * 50000,
+                     csr.max_item + 1);
+  }
   const int32_t n = csr.n;
   int32_t hcum[C2_MAX_T + 1];
   hcum[0] = 0;
@@ -1537,7 +1723,7 @@ int local_knn(c2_ctx *ctx, const Csr &csr, int t, const Clusters &cl, int k, c2_
   const int32_t m = csr.max_item + 1;
   int32_t nwin = (int32_t)((m + 50000 - 1) / 50000);
   int32_t W = (int32_t)((m + nwin - 1) / nwin);
-  if (nwin > MAX_WIN) return set_err(ctx, C2_EINVAL, "item ids up to %d need %d windows (max %d)", m, nwin, MAX_WIN);
+
   if (nslices > 0) {
     bcs = (BigC *)ws_get(ctx, "bc", (size_t)ncl * sizeof(BigC), &rc);
     if (rc) return rc;
@@ -1667,7 +1853,8 @@ int local_knn(c2_ctx *ctx, const Csr &csr, int t, const Clusters &cl, int k, c2_
     // survivor queue per row: 256 entries where shared memory allows, at least 64*KS
     const int qmin = k <= 32 ? 64 : 128;
     qcap = 256;
-    const size_t budget = ctx->smem_optin - 4096;  // minus the kernel's static shared memory (~2.1 KB)
+    const size_t budget = (C2_SMEM_BUDGET ? std::min<size_t>(C2_SMEM_BUDGET, ctx->smem_optin) : ctx->smem_optin) -
+                          4096;  // minus the kernel's static shared memory (~2.1 KB)
     const size_t rlw = fused ? (size_t)64 * k : 0;  // the rows' running lists (Cand = 2 words)
     const size_t stgw = 4096;  // staging of the next tile's row blocks: at least 16 KB
     while (qcap > qmin && ((size_t)K8Lay(smax, qcap).words + rlw + stgw) * 4 > budget) qcap -= 64;

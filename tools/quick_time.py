@@ -8,9 +8,13 @@ import paper_2010_11497_b200 as c2
 
 cfgs = sys.argv[1:] or ["c1", "c2", "c3", "c4", "c5"]
 ctx = c2.Context(0, timing=True)
-for name in cfgs:
-    C = synth.config(name)
-    offs, items = synth.generate(name)
+for spec in cfgs:
+    # "c5" or "c5:m=16000:N=256" (overrides of the synthetic config, dev experiments)
+    name, *kv = spec.split(":")
+    over = {k: type(getattr(synth.config(name), k))(v) for k, v in (x.split("=") for x in kv)}
+    C = synth.config(name, **over)
+    offs, items = synth.generate(C)
+    name = spec
     d_o, d_i = torch.from_numpy(offs).cuda(), torch.from_numpy(items).cuda()
     for mode in ([0, 1] if name == "c4" else [0]):
         for rep in range(4):
