@@ -55,6 +55,7 @@ def _load():
         "c2o_frh": (_I, [_I64, _P, _P, _I, _I64, _P, _P]),
         "c2o_sketch": (_I, [_I64, _P, _P, _I, _I64, _P, _I, _P]),
         "c2o_cluster": (_I, [_I64, _P, _P, _I, _I64, _P, _I64, _I, _P, _P, _P, _P, _P]),
+        "c2o_minhash_cluster": (_I, [_I64, _P, _P, _I, _U64, _I64, _P, _P, _P, _P, _P]),
         "c2o_local_knn": (_I, [_I64, _P, _P, _I, _P, _P, _P, _I, _I, _P, _I64, _I, _P]),
         "c2o_merge": (_I, [_I64, _I, _I, _P, _I, _P, _P, _P, _P]),
         "c2o_knn_union": (_I, [_I64, _P, _P, _I, _P, _P, _P, _I, _I, _P, _I64, _I, _P, _P, _P]),
@@ -158,6 +159,19 @@ def cluster(offs, items, htab, N: int, formulation: int = 0) -> dict:
     return out
 
 
+def cluster_minhash(offs, items, seed: int, t: int, N: int) -> dict:
+    """C^2/MinHash variant clustering: one cluster per min-hash item, no split."""
+    offs, items, n = _csr(offs, items)
+    out = dict(offsets=np.zeros((t, n + 1), np.int32), members=np.zeros((t, n), np.int32),
+               cluster_of=np.zeros((t, n), np.int32), n_clusters=np.zeros(t, np.int32))
+    st = np.zeros(8, np.int64)
+    _chk(_load().c2o_minhash_cluster(n, _ptr(offs), _ptr(items), t, seed, N, _ptr(out["offsets"]),
+                                     _ptr(out["members"]), _ptr(out["cluster_of"]), _ptr(out["n_clusters"]),
+                                     _ptr(st)), "minhash_cluster")
+    out["stats"] = dict(zip(STAT_KEYS, (int(x) for x in st)))
+    return out
+
+
 # ------------------------------------------------------------------ steps 2-3
 def local_knn(offs, items, cl: dict, k: int, sim_mode: int = 0, gtab=None, nthreads: int | None = None):
     offs, items, n = _csr(offs, items)
@@ -236,14 +250,17 @@ def pair_counts(offs, items, u, v):
 
 
 def build_graph(offs, items, *, k: int, t: int, b: int, N: int, seed: int, sim_mode: int = 0, htab=None,
-                nthreads: int | None = None, formulation: int = 0) -> dict:
-    """Whole C^2 pipeline on the CPU: FRH clustering -> local brute force -> Alg. 3 merge."""
+                nthreads: int | None = None, formulation: int = 0, clustering: str = "frh") -> dict:
+    """Whole C^2 pipeline on the CPU: FRH (or MinHash) clustering -> local brute force -> Alg. 3."""
     offs, items, n = _csr(offs, items)
     m = int(items.max()) + 1 if len(items) else 1
-    if htab is None:
-        htab = hash_table(seed, t, b, m)
     gtab = gf_table(seed, m) if sim_mode == 1 else None
-    cl = cluster(offs, items, htab, N, formulation)
+    if clustering == "minhash":
+        cl = cluster_minhash(offs, items, seed, t, N)
+    else:
+        if htab is None:
+            htab = hash_table(seed, t, b, m)
+        cl = cluster(offs, items, htab, N, formulation)
     cand = local_knn(offs, items, cl, k, sim_mode, gtab, nthreads)
     nbr, inter, uni, sim = merge(cand, nthreads)
     return dict(clusters=cl, cand=cand, nbr=nbr, inter=inter, uni=uni, sim=sim, htab=htab, gtab=gtab)

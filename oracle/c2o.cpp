@@ -295,6 +295,44 @@ int c2o_sketch(int64_t n, const int32_t *offs, const int32_t *items, int t, int6
   return 0;
 }
 
+// Chunk guard (A9) + canonical form (A25) of one function's clusters; accumulates stats.
+static void emit_canonical(int64_t n, ClusterSet &cs, int64_t N, int f, int32_t *offsets, int32_t *members,
+                           int32_t *cluster_of, int32_t *n_clusters, int64_t *st) {
+  // An emitted cluster larger than N is replaced by ceil(s/N) balanced chunks of its
+  // ascending members.
+  std::vector<std::vector<int32_t>> final_;
+  for (auto &C : cs.clusters) {
+    std::sort(C.begin(), C.end());
+    int64_t s = (int64_t)C.size();
+    if (s <= N) { final_.push_back(C); continue; }
+    int64_t mc = (s + N - 1) / N;
+    st[4]++;
+    for (int64_t j = 0; j < mc; ++j)
+      final_.emplace_back(C.begin() + (j * s) / mc, C.begin() + ((j + 1) * s) / mc);
+  }
+  // Canonical form (A25): clusters ordered by smallest member, members ascending.
+  std::sort(final_.begin(), final_.end(),
+            [](const std::vector<int32_t> &x, const std::vector<int32_t> &y) { return x[0] < y[0]; });
+  int32_t *off = offsets + f * (n + 1);
+  int32_t *mem = members + f * n;
+  int32_t *cof = cluster_of + f * n;
+  int64_t pos = 0;
+  for (size_t c = 0; c < final_.size(); ++c) {
+    off[c] = (int32_t)pos;
+    for (int32_t u : final_[c]) { mem[pos++] = u; cof[u] = (int32_t)c; }
+    int64_t s = (int64_t)final_[c].size();
+    st[5] += s * (s - 1) / 2;  // P counts unordered pairs (A21)
+    st[6] = std::max(st[6], s);
+  }
+  for (size_t c = final_.size(); c <= (size_t)n; ++c) off[c] = (int32_t)pos;
+  n_clusters[f] = (int32_t)final_.size();
+  st[0] += (int64_t)final_.size();
+  st[1] = std::max(st[1], cs.max_depth);
+  st[2] += cs.split_nodes;
+  st[3] += cs.folded;
+  st[7] += cs.residuals;
+}
+
 int c2o_cluster(int64_t n, const int32_t *offs, const int32_t *items, int t, int64_t m, const uint16_t *htab,
                 int64_t N, int formulation, int32_t *offsets, int32_t *members, int32_t *cluster_of,
                 int32_t *n_clusters, int64_t *stats) {
@@ -305,39 +343,37 @@ int c2o_cluster(int64_t n, const int32_t *offs, const int32_t *items, int t, int
     ClusterSet cs;
     if (formulation == 0) cluster_recursive(n, offs, items, htab + f * m, N, cs);
     else cluster_trie(n, offs, items, htab + f * m, N, cs);
-    // Chunk guard (A9): an emitted cluster larger than N (only a residual can be one) is
-    // replaced by ceil(s/N) balanced chunks of its ascending members.
-    std::vector<std::vector<int32_t>> final_;
-    for (auto &C : cs.clusters) {
-      std::sort(C.begin(), C.end());
-      int64_t s = (int64_t)C.size();
-      if (s <= N) { final_.push_back(C); continue; }
-      int64_t mc = (s + N - 1) / N;
-      st[4]++;
-      for (int64_t j = 0; j < mc; ++j)
-        final_.emplace_back(C.begin() + (j * s) / mc, C.begin() + ((j + 1) * s) / mc);
+    emit_canonical(n, cs, N, f, offsets, members, cluster_of, n_clusters, st);
+  }
+  if (stats) std::memcpy(stats, st, sizeof(st));
+  return 0;
+}
+
+int c2o_minhash_cluster(int64_t n, const int32_t *offs, const int32_t *items, int t, uint64_t seed, int64_t N,
+                        int32_t *offsets, int32_t *members, int32_t *cluster_of, int32_t *n_clusters,
+                        int64_t *stats) {
+  if (N < 2 || t < 1) return -1;
+  if (!row_ok(offs, items, n, 0)) return -2;
+  std::vector<uint64_t> a(t), c(t);
+  c2o_hash_params(seed, t, a.data(), c.data());
+  int64_t st[8] = {0};
+  for (int f = 0; f < t; ++f) {
+    // MinHash: the full-range hash z_f(x) = a_f*x + c_f mod 2^64 (the
+    // A1 family before range reduction) simulates a random permutation of the items; u's
+    // cluster is the item of P_u that comes first, i.e. one cluster per item, no splitting.
+    std::map<int32_t, std::vector<int32_t>> byitem;
+    for (int64_t u = 0; u < n; ++u) {
+      uint64_t best = ~0ULL;
+      int32_t arg = -1;
+      for (int32_t p = offs[u]; p < offs[u + 1]; ++p) {
+        uint64_t z = a[f] * (uint64_t)items[p] + c[f];
+        if (arg < 0 || z < best || (z == best && items[p] < arg)) { best = z; arg = items[p]; }
+      }
+      byitem[arg].push_back((int32_t)u);
     }
-    // Canonical form (A25): clusters ordered by smallest member, members ascending.
-    std::sort(final_.begin(), final_.end(),
-              [](const std::vector<int32_t> &x, const std::vector<int32_t> &y) { return x[0] < y[0]; });
-    int32_t *off = offsets + f * (n + 1);
-    int32_t *mem = members + f * n;
-    int32_t *cof = cluster_of + f * n;
-    int64_t pos = 0;
-    for (size_t c = 0; c < final_.size(); ++c) {
-      off[c] = (int32_t)pos;
-      for (int32_t u : final_[c]) { mem[pos++] = u; cof[u] = (int32_t)c; }
-      int64_t s = (int64_t)final_[c].size();
-      st[5] += s * (s - 1) / 2;  // P counts unordered pairs (A21)
-      st[6] = std::max(st[6], s);
-    }
-    for (size_t c = final_.size(); c <= (size_t)n; ++c) off[c] = (int32_t)pos;
-    n_clusters[f] = (int32_t)final_.size();
-    st[0] += (int64_t)final_.size();
-    st[1] = std::max(st[1], cs.max_depth);
-    st[2] += cs.split_nodes;
-    st[3] += cs.folded;
-    st[7] += cs.residuals;
+    ClusterSet cs;
+    for (auto &g : byitem) cs.clusters.push_back(g.second);
+    emit_canonical(n, cs, N, f, offsets, members, cluster_of, n_clusters, st);
   }
   if (stats) std::memcpy(stats, st, sizeof(st));
   return 0;

@@ -62,6 +62,14 @@ int c2o_cluster(int64_t n, const int32_t *offs, const int32_t *items, int t, int
                 int64_t N, int formulation, int32_t *offsets, int32_t *members, int32_t *cluster_of,
                 int32_t *n_clusters, int64_t *stats);
 
+/* C^2/MinHash variant: per function, users grouped by the item of their profile
+ * with the smallest full-range hash z_f(x) = a_f*x + c_f mod 2^64 (ties: lower item id), i.e.
+ * t x m clusters, no splitting.  N >= n keeps them whole (the paper's variant); a smaller N
+ * applies the chunk guard (A9, reading A33).  Outputs and stats as c2o_cluster. */
+int c2o_minhash_cluster(int64_t n, const int32_t *offs, const int32_t *items, int t, uint64_t seed, int64_t N,
+                        int32_t *offsets, int32_t *members, int32_t *cluster_of, int32_t *n_clusters,
+                        int64_t *stats);
+
 /* Step 2, brute-force branch of Alg. 2: per cluster, all s(s-1)/2 similarities
  * (P:555), then per user the first min(k, s-1) candidates under the order (A13/A14), padded.
  * sim_mode 0 = exact sets, 1 = GoldFinger-1024 (gtab != NULL).  cand is [t][n][k]. */

@@ -480,3 +480,75 @@ def test_a7_fold_hand_built():
         assert got == g["expected_clusters"], form
         assert cl["stats"]["split_nodes"] == g["expected_split_nodes"]
         assert cl["stats"]["folded_singletons"] == g["expected_folded_singletons"]
+
+
+# ----------------------------------------------------------------- C^2/MinHash variant (N3)
+def _minhash_py(rows, seed, t, N):
+    """Independent big-int MinHash clustering: z = (a x + c) mod 2^64 with Python integers."""
+    a, c = oracle.hash_params(seed, t)
+    out = []
+    for f in range(t):
+        groups = {}
+        for u, r in enumerate(rows):
+            key = min(r, key=lambda x: (((int(a[f]) * x + int(c[f])) % 2**64), x))
+            groups.setdefault(key, []).append(u)
+        cl = []
+        for g in groups.values():
+            g = sorted(g)
+            s = len(g)
+            if s <= N:
+                cl.append(g)
+            else:
+                mc = -(-s // N)
+                cl += [g[(j * s) // mc:((j + 1) * s) // mc] for j in range(mc)]
+        out.append(sorted(cl))
+    return out
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_minhash_clusters_vs_bigint(seed):
+    rng = np.random.default_rng(50 + seed)
+    n, m = int(rng.integers(2, 300)), int(rng.integers(2, 200))
+    offs, items = synth.random_instance(rng, n, m, 1, 15)
+    rows = [items[offs[u]:offs[u + 1]].tolist() for u in range(n)]
+    t, N = int(rng.integers(1, 6)), int(rng.choice([2, 5, 40, 10**6]))
+    cl = oracle.cluster_minhash(offs, items, 9 + seed, t, N)
+    exp = _minhash_py(rows, 9 + seed, t, N)
+    for f in range(t):
+        got = [cl["members"][f][cl["offsets"][f][c]:cl["offsets"][f][c + 1]].tolist()
+               for c in range(cl["n_clusters"][f])]
+        assert got == exp[f]
+
+
+def test_minhash_invariants():
+    # one cluster per min-hash ITEM: members share that item, so users with disjoint profiles are
+    # never co-clustered; identical profiles always are (P:1204-1212)
+    rows = [[1, 2, 3], [4, 5], [1, 2, 3], [6], [6], [7, 8, 9, 10], [11]]
+    offs, items = csr(rows)
+    cl = oracle.cluster_minhash(offs, items, 3, 64, 10**6)
+    for f in range(64):
+        cof = cl["cluster_of"][f]
+        assert cof[0] == cof[2] and cof[3] == cof[4]
+        for u in range(len(rows)):
+            for v in range(len(rows)):
+                if not set(rows[u]) & set(rows[v]):
+                    assert cof[u] != cof[v]
+    assert cl["stats"]["split_nodes"] == 0
+
+
+@pytest.mark.parametrize("J_target", [0.2, 0.5])
+def test_minhash_collision_probability_is_jaccard(J_target):
+    # Broder's property (S:212 acceptance): P[minhash(u) = minhash(v)] = J for a random
+    # permutation; the multiply-add family on scattered ids must match within MC noise + 0.02.
+    rng = np.random.default_rng(int(J_target * 10))
+    l, T = 100, 4000
+    inter = int(round(2 * J_target * l / (1 + J_target)))  # |A| = |B| = l -> J = i / (2l - i)
+    ids = rng.choice(2**31 - 1, size=2 * l - inter, replace=False)
+    A = np.sort(ids[:l])
+    B = np.sort(np.concatenate([ids[:inter], ids[l:]]))
+    J = inter / (2 * l - inter)
+    offs, items = csr([A.tolist(), B.tolist()])
+    cl = oracle.cluster_minhash(offs, items, 77, T, 10**6)
+    p_hat = float((cl["cluster_of"][:, 0] == cl["cluster_of"][:, 1]).mean())
+    sd = math.sqrt(J * (1 - J) / T)
+    assert abs(p_hat - J) <= 4 * sd + 0.02, (p_hat, J)
