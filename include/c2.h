@@ -95,10 +95,23 @@ enum {
   C2_OPT_TIMING = 3,       /* nonzero: record per-phase CUDA-event times into c2_stats */
   C2_OPT_KSTATS = 4,       /* diagnostics: value = address of a dev uint64[80] the local kernel adds
                               counters to (rows, survivors, sort sizes, overflows; 0 = off) */
-  C2_OPT_RELABEL = 5       /* nonzero (default): when the item range needs >= 3 shared-memory windows,
+  C2_OPT_RELABEL = 5,      /* nonzero (default): when the item range needs >= 3 shared-memory windows,
                               Step 2 renumbers each cluster's shared items densely (one window per
                               tile); 0: always windows over the global item range.  Results are
                               identical either way. */
+  C2_OPT_CLUSTERING = 6,   /* Step 1 of c2_fastrandomhash / c2_build: C2_CLUSTER_FRH (default) or
+                              C2_CLUSTER_MINHASH (the paper's C^2/MinHash ablation) */
+  C2_OPT_FUNC_OFFSET = 7   /* f0 >= 0 (default 0): the t functions used are functions f0 .. f0+t-1 of the
+                              seed's stream (A2), so G processes that each run t/G consecutive functions
+                              together run exactly the functions of one t-function run (multi-GPU by
+                              hash function; their merged lists equal the single run's, A16) */
+};
+enum {
+  C2_CLUSTER_FRH = 0,    /* FastRandomHash + recursive split */
+  C2_CLUSTER_MINHASH = 1 /* per function, u's cluster = the item of P_u with the smallest full-range hash
+                            z_f(x) = a_f*x + c_f mod 2^64 (ties: lower id): t x m clusters, no split; b is
+                            ignored; clusters larger than N are cut into balanced chunks (A9; pass
+                            N >= n_users for the paper's unbounded clusters).  Needs t*(max id+1) < 2^30. */
 };
 C2_API int c2_ctx_set_option(c2_ctx *ctx, int key, int64_t value);
 

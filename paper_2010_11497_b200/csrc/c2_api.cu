@@ -85,10 +85,11 @@ int build_device(c2_ctx *ctx, const int32_t *offs, const int32_t *items, int32_t
   Csr csr{offs, items, n, -1, 0, 0, nullptr};
   C2_TRY(validate_csr(ctx, &csr));
   HashParams hp;
-  make_hash_params(seed, t, &hp);
+  make_hash_params(seed, t, &hp, ctx->func_offset);
   Clusters cl;
   C2_TRY(cluster_buffers(ctx, t, n, &cl));
-  C2_TRY(fastrandomhash(ctx, csr, t, b, N, &hp, nullptr, 0, &cl));
+  if (ctx->clustering == 1) C2_TRY(minhash_clusters(ctx, csr, t, N, &hp, &cl));
+  else C2_TRY(fastrandomhash(ctx, csr, t, b, N, &hp, nullptr, 0, &cl));
   Csr sims = csr;
   if (sim_mode == C2_SIM_GF1024) C2_TRY(gf_encode(ctx, csr, &hp, &sims));
   int rc;
@@ -180,6 +181,14 @@ int c2_ctx_set_option(c2_ctx *ctx, int key, int64_t value) {
     case C2_OPT_TIMING: ctx->timing = value != 0; return C2_OK;
     case C2_OPT_KSTATS: ctx->kstats = (unsigned long long *)(intptr_t)value; return C2_OK;
     case C2_OPT_RELABEL: ctx->relabel = value != 0; return C2_OK;
+    case C2_OPT_FUNC_OFFSET:
+      if (value < 0 || value > (1 << 20)) return set_err(ctx, C2_EINVAL, "bad function offset");
+      ctx->func_offset = (int)value;
+      return C2_OK;
+    case C2_OPT_CLUSTERING:
+      if (value != C2_CLUSTER_FRH && value != C2_CLUSTER_MINHASH) return set_err(ctx, C2_EINVAL, "bad clustering");
+      ctx->clustering = (int)value;
+      return C2_OK;
     default: return set_err(ctx, C2_EINVAL, "unknown option %d", key);
   }
 }
@@ -193,7 +202,7 @@ int c2_sketch(c2_ctx *ctx, const int32_t *csr_offsets, const int32_t *item_ids, 
   Csr csr{csr_offsets, item_ids, n_users, -1, 0, 0, nullptr};
   C2_TRY(validate_csr(ctx, &csr));
   HashParams hp;
-  make_hash_params(seed, t, &hp);
+  make_hash_params(seed, t, &hp, ctx->func_offset);
   return sketch(ctx, csr, t, b, &hp, nullptr, 0, D, sketch_out);
 }
 
@@ -221,12 +230,13 @@ static int frh_common(c2_ctx *ctx, const int32_t *offs, const int32_t *items, in
     if (hmx >= b) return set_err(ctx, C2_EINVAL, "hash table value %d >= b=%d", hmx, b);
   }
   HashParams hp;
-  make_hash_params(seed, t, &hp);
+  make_hash_params(seed, t, &hp, ctx->func_offset);
   Clusters cl;
   cl.offsets = out->offsets;
   cl.members = out->members;
   cl.cluster_of = out->cluster_of;
-  C2_TRY(fastrandomhash(ctx, csr, t, b, N, htab ? nullptr : &hp, htab, m, &cl));
+  if (ctx->clustering == 1 && !htab) C2_TRY(minhash_clusters(ctx, csr, t, N, &hp, &cl));
+  else C2_TRY(fastrandomhash(ctx, csr, t, b, N, htab ? nullptr : &hp, htab, m, &cl));
   for (int f = 0; f < t; ++f) out->n_clusters[f] = cl.n_clusters[f];
   return C2_OK;
 }
@@ -253,7 +263,7 @@ int c2_local_knn(c2_ctx *ctx, const int32_t *csr_offsets, const int32_t *item_id
   Csr csr{csr_offsets, item_ids, n_users, -1, 0, 0, nullptr};
   C2_TRY(validate_csr(ctx, &csr));
   HashParams hp;
-  make_hash_params(seed, t, &hp);
+  make_hash_params(seed, t, &hp, ctx->func_offset);
   Clusters cl;
   cl.offsets = clusters->offsets;
   cl.members = clusters->members;

@@ -28,6 +28,8 @@ struct c2_ctx {
   bool sync_check = false;
   bool timing = false;
   unsigned long long *kstats = nullptr;
+  int clustering = 0;
+  int func_offset = 0;  // C2_OPT_FUNC_OFFSET   // C2_OPT_CLUSTERING: 0 FastRandomHash (Step 1 of C^2), 1 MinHash (N3 variant)
   bool relabel = true;  // C2_OPT_RELABEL  (C2_OPT_KSTATS: kstats = dev [80] K7/K8 counters)
   c2_stats stats{};
   // device workspace: name -> (ptr, bytes); grow-only
@@ -58,7 +60,8 @@ struct HashParams {
   uint64_t c[C2_MAX_T];
   uint64_t ga, gc;
 };
-void make_hash_params(uint64_t seed, int t, HashParams *hp);
+// f0: the first function used is function f0 of the stream (C2_OPT_FUNC_OFFSET)
+void make_hash_params(uint64_t seed, int t, HashParams *hp, int f0 = 0);
 
 // ---------------------------------------------------------------- primitives (prims.cu)
 // out[i] = sum_{j<i} in[j] for i in [0, n]; out has n+1 entries (out[n] = total).
@@ -91,6 +94,9 @@ int sketch(c2_ctx *ctx, const Csr &csr, int t, int b, const HashParams *hp, cons
            int D, uint16_t *out);
 int fastrandomhash(c2_ctx *ctx, const Csr &csr, int t, int b, int64_t N, const HashParams *hp,
                    const uint16_t *htab, int32_t m, Clusters *out);
+// C^2/MinHash variant: one cluster per min-hash item, no splitting (chunk guard
+// for clusters > N).
+int minhash_clusters(c2_ctx *ctx, const Csr &csr, int t, int64_t N, const HashParams *hp, Clusters *out);
 
 // Step 2 (k_local.cu).
 int gf_encode(c2_ctx *ctx, const Csr &csr, const HashParams *hp, Csr *gf);

@@ -272,6 +272,125 @@ int count_gt(c2_ctx *ctx, const int32_t *x, int64_t E, int64_t N, int32_t *out) 
   return C2_OK;
 }
 
+// ------------------------------------------------------------------ K4: chunk guard + canonical form
+// key[f*n+u] = node id in [0, next_id) (at most one node per cluster; a node larger than N is
+// cut into balanced chunks, A9); produces the canonical arrays (A25) and the host statistics.
+static int canonicalize(c2_ctx *ctx, int32_t n, int t, int64_t N, int32_t *key, int64_t next_id,
+                        int64_t split_nodes, int64_t max_depth, Clusters *out) {
+  int rc;
+  const int64_t TN = (int64_t)t * n;
+  cudaStream_t st = ctx->stream;
+  cudaEvent_t *ev = ctx->ev;
+  unsigned long long *acc = (unsigned long long *)ws_get(ctx, "acc", 64, &rc);
+  if (rc) return rc;
+  int32_t *hsmall = (int32_t *)ctx->h_small;
+  int32_t *size = (int32_t *)ws_get(ctx, "nsize", (size_t)(next_id + TN + 1) * 4, &rc);
+  if (rc) return rc;
+  C2_CUDA(ctx, cudaMemsetAsync(size, 0, (size_t)next_id * 4, st));
+  k_count_keys<<<nblk(TN), 256, 0, st>>>(key, TN, size);
+  C2_LAUNCHED(ctx, "k_count_keys");
+  int32_t *mx = (int32_t *)(acc + 2);
+  C2_CUDA(ctx, cudaMemsetAsync(mx, 0, 4, st));
+  k_max<<<nblk(next_id), 256, 0, st>>>(size, next_id, mx);
+  C2_LAUNCHED(ctx, "k_max");
+  C2_CUDA(ctx, cudaMemcpyAsync(hsmall, mx, 4, cudaMemcpyDeviceToHost, st));
+  C2_CUDA(ctx, cudaMemcpyAsync(ctx->h_small + 4, acc + 1, 8, cudaMemcpyDeviceToHost, st));
+  C2_TRY(stream_sync(ctx, "max size"));
+  int64_t chunked = 0;
+  int64_t folded = ctx->h_small[4];
+  uint32_t *skey = (uint32_t *)ws_get(ctx, "skey", (size_t)TN * 4, &rc);
+  if (rc) return rc;
+  uint32_t *sval = (uint32_t *)ws_get(ctx, "sval", (size_t)TN * 4, &rc);
+  if (rc) return rc;
+  uint32_t *skey2 = (uint32_t *)ws_get(ctx, "skey2", (size_t)TN * 4, &rc);
+  if (rc) return rc;
+  uint32_t *sval2 = (uint32_t *)ws_get(ctx, "sval2", (size_t)TN * 4, &rc);
+  if (rc) return rc;
+  if (hsmall[0] > N) {
+    // A9: residuals larger than N -> ceil(s/N) balanced chunks of their ascending members.
+    // Stable sort of (node, f*n+u) by node gives every node's members in ascending order.
+    int32_t *tmp = (int32_t *)ws_get(ctx, "chunk_tmp", (size_t)(next_id + 1) * 4 * 4, &rc);
+    if (rc) return rc;
+    int32_t *start = tmp, *mcnt = tmp + (next_id + 1), *cbase = tmp + 2 * (next_id + 1);
+    C2_TRY(scan_exclusive(ctx, size, start, next_id));
+    k_chunk_count<<<nblk(next_id), 256, 0, st>>>(size, next_id, N, mcnt);
+    C2_LAUNCHED(ctx, "k_chunk_count");
+    C2_TRY(scan_exclusive(ctx, mcnt, cbase, next_id));
+    // flat index -> (key) pairs
+    C2_TRY(fill_key_pairs(ctx, key, TN, skey2, sval2));
+    C2_TRY(radix_sort_pairs(ctx, skey2, sval2, skey, sval, TN, bits_for(next_id)));
+    k_chunk_assign<<<nblk(TN), 256, 0, st>>>(skey, sval, TN, size, start, cbase, N, (int32_t)next_id, key);
+    C2_LAUNCHED(ctx, "k_chunk_assign");
+    C2_CUDA(ctx, cudaMemcpyAsync(hsmall, cbase + next_id, 4, cudaMemcpyDeviceToHost, st));
+    int32_t *nbig = (int32_t *)(acc + 3);
+    C2_CUDA(ctx, cudaMemsetAsync(nbig, 0, 4, st));
+    C2_TRY(count_gt(ctx, size, next_id, N, nbig));
+    C2_CUDA(ctx, cudaMemcpyAsync(hsmall + 1, nbig, 4, cudaMemcpyDeviceToHost, st));
+    C2_TRY(stream_sync(ctx, "chunk guard"));
+    int64_t nchunks = hsmall[0];
+    chunked = hsmall[1];
+    next_id += nchunks;
+    size = (int32_t *)ws_get(ctx, "nsize", (size_t)(next_id + 1) * 4, &rc);
+    if (rc) return rc;
+    C2_CUDA(ctx, cudaMemsetAsync(size, 0, (size_t)next_id * 4, st));
+    k_count_keys<<<nblk(TN), 256, 0, st>>>(key, TN, size);
+    C2_LAUNCHED(ctx, "k_count_keys");
+  }
+  // rep[node] = smallest member; heads; canonical cluster index by scan over users
+  int32_t *rep = (int32_t *)ws_get(ctx, "rep", (size_t)next_id * 4, &rc);
+  if (rc) return rc;
+  C2_CUDA(ctx, cudaMemsetAsync(rep, 0x7F, (size_t)next_id * 4, st));
+  k_rep<<<nblk(TN), 256, 0, st>>>(key, TN, n, rep);
+  C2_LAUNCHED(ctx, "k_rep");
+  int32_t *head = (int32_t *)ws_get(ctx, "head", (size_t)(2 * TN + 2) * 4, &rc);
+  if (rc) return rc;
+  int32_t *hscan = head + TN + 1;
+  k_heads<<<nblk(TN), 256, 0, st>>>(key, rep, TN, n, head);
+  C2_LAUNCHED(ctx, "k_heads");
+  C2_TRY(scan_exclusive(ctx, head, hscan, TN));
+  const int64_t TN1 = (int64_t)t * (n + 1);
+  int32_t *csize = (int32_t *)ws_get(ctx, "csize", (size_t)(2 * TN1 + 2) * 4, &rc);
+  if (rc) return rc;
+  int32_t *craw = csize + TN1 + 1;
+  C2_CUDA(ctx, cudaMemsetAsync(csize, 0, (size_t)TN1 * 4, st));
+  k_cluster_of<<<nblk(TN), 256, 0, st>>>(key, rep, hscan, size, TN, n, out->cluster_of, csize, skey2, sval2);
+  C2_LAUNCHED(ctx, "k_cluster_of");
+  C2_TRY(scan_exclusive(ctx, csize, craw, TN1));
+  k_fix_offsets<<<nblk(TN1), 256, 0, st>>>(craw, TN1, n, out->offsets);
+  C2_LAUNCHED(ctx, "k_fix_offsets");
+  // members: stable sort of (f*n + cluster, u) by key -> ascending members per cluster
+  C2_TRY(radix_sort_pairs(ctx, skey2, sval2, skey, (uint32_t *)out->members, TN, bits_for(TN)));
+  C2_CUDA(ctx, cudaMemsetAsync(acc, 0, 8, st));
+  k_pairs<<<nblk(TN1), 256, 0, st>>>(csize, TN1, acc);
+  C2_LAUNCHED(ctx, "k_pairs");
+  C2_CUDA(ctx, cudaMemsetAsync(mx, 0, 4, st));
+  k_max<<<nblk(TN1), 256, 0, st>>>(csize, TN1, mx);
+  C2_LAUNCHED(ctx, "k_max");
+  // host values: n_clusters[f] = hscan[(f+1)n] - hscan[fn], P, max size
+  int32_t *hh = (int32_t *)ctx->h_small + 16;
+  for (int f = 0; f <= t; ++f)
+    C2_CUDA(ctx, cudaMemcpyAsync(hh + f, hscan + (int64_t)f * n, 4, cudaMemcpyDeviceToHost, st));
+  C2_CUDA(ctx, cudaMemcpyAsync(ctx->h_small, acc, 8, cudaMemcpyDeviceToHost, st));
+  C2_CUDA(ctx, cudaMemcpyAsync(ctx->h_small + 1, mx, 4, cudaMemcpyDeviceToHost, st));
+  C2_TRY(stream_sync(ctx, "canonical"));
+  int64_t total = 0;
+  for (int f = 0; f < t; ++f) {
+    out->n_clusters[f] = hh[f + 1] - hh[f];
+    total += out->n_clusters[f];
+  }
+  out->max_size = (int32_t)(ctx->h_small[1] & 0xffffffff);
+  ctx->stats.pairs = ctx->h_small[0];
+  ctx->stats.clusters = total;
+  ctx->stats.max_cluster_size = out->max_size;
+  ctx->stats.split_nodes = split_nodes;
+  ctx->stats.max_depth = max_depth;
+  ctx->stats.folded_singletons = folded;
+  ctx->stats.chunked_residuals = chunked;
+  if (ctx->timing) cudaEventRecord(ev[3], st);
+  return C2_OK;
+}
+
+
 int fastrandomhash(c2_ctx *ctx, const Csr &csr, int t, int b, int64_t N, const HashParams *hp,
                    const uint16_t *htab, int32_t m, Clusters *out) {
   int rc;
@@ -388,111 +507,61 @@ int fastrandomhash(c2_ctx *ctx, const Csr &csr, int t, int b, int64_t N, const H
   }
   if (ctx->timing) cudaEventRecord(ev[2], st);
 
-  // ---- K4 chunk guard + canonical form
-  int32_t *size = (int32_t *)ws_get(ctx, "nsize", (size_t)(next_id + TN + 1) * 4, &rc);
-  if (rc) return rc;
-  C2_CUDA(ctx, cudaMemsetAsync(size, 0, (size_t)next_id * 4, st));
-  k_count_keys<<<nblk(TN), 256, 0, st>>>(key, TN, size);
-  C2_LAUNCHED(ctx, "k_count_keys");
-  int32_t *mx = (int32_t *)(acc + 2);
-  C2_CUDA(ctx, cudaMemsetAsync(mx, 0, 4, st));
-  k_max<<<nblk(next_id), 256, 0, st>>>(size, next_id, mx);
-  C2_LAUNCHED(ctx, "k_max");
-  C2_CUDA(ctx, cudaMemcpyAsync(hsmall, mx, 4, cudaMemcpyDeviceToHost, st));
-  C2_CUDA(ctx, cudaMemcpyAsync(ctx->h_small + 4, acc + 1, 8, cudaMemcpyDeviceToHost, st));
-  C2_TRY(stream_sync(ctx, "max size"));
-  int64_t chunked = 0;
-  int64_t folded = ctx->h_small[4];
-  uint32_t *skey = (uint32_t *)ws_get(ctx, "skey", (size_t)TN * 4, &rc);
-  if (rc) return rc;
-  uint32_t *sval = (uint32_t *)ws_get(ctx, "sval", (size_t)TN * 4, &rc);
-  if (rc) return rc;
-  uint32_t *skey2 = (uint32_t *)ws_get(ctx, "skey2", (size_t)TN * 4, &rc);
-  if (rc) return rc;
-  uint32_t *sval2 = (uint32_t *)ws_get(ctx, "sval2", (size_t)TN * 4, &rc);
-  if (rc) return rc;
-  if (hsmall[0] > N) {
-    // A9: residuals larger than N -> ceil(s/N) balanced chunks of their ascending members.
-    // Stable sort of (node, f*n+u) by node gives every node's members in ascending order.
-    int32_t *tmp = (int32_t *)ws_get(ctx, "chunk_tmp", (size_t)(next_id + 1) * 4 * 4, &rc);
-    if (rc) return rc;
-    int32_t *start = tmp, *mcnt = tmp + (next_id + 1), *cbase = tmp + 2 * (next_id + 1);
-    C2_TRY(scan_exclusive(ctx, size, start, next_id));
-    k_chunk_count<<<nblk(next_id), 256, 0, st>>>(size, next_id, N, mcnt);
-    C2_LAUNCHED(ctx, "k_chunk_count");
-    C2_TRY(scan_exclusive(ctx, mcnt, cbase, next_id));
-    // flat index -> (key) pairs
-    C2_TRY(fill_key_pairs(ctx, key, TN, skey2, sval2));
-    C2_TRY(radix_sort_pairs(ctx, skey2, sval2, skey, sval, TN, bits_for(next_id)));
-    k_chunk_assign<<<nblk(TN), 256, 0, st>>>(skey, sval, TN, size, start, cbase, N, (int32_t)next_id, key);
-    C2_LAUNCHED(ctx, "k_chunk_assign");
-    C2_CUDA(ctx, cudaMemcpyAsync(hsmall, cbase + next_id, 4, cudaMemcpyDeviceToHost, st));
-    int32_t *nbig = (int32_t *)(acc + 3);
-    C2_CUDA(ctx, cudaMemsetAsync(nbig, 0, 4, st));
-    C2_TRY(count_gt(ctx, size, next_id, N, nbig));
-    C2_CUDA(ctx, cudaMemcpyAsync(hsmall + 1, nbig, 4, cudaMemcpyDeviceToHost, st));
-    C2_TRY(stream_sync(ctx, "chunk guard"));
-    int64_t nchunks = hsmall[0];
-    chunked = hsmall[1];
-    next_id += nchunks;
-    size = (int32_t *)ws_get(ctx, "nsize", (size_t)(next_id + 1) * 4, &rc);
-    if (rc) return rc;
-    C2_CUDA(ctx, cudaMemsetAsync(size, 0, (size_t)next_id * 4, st));
-    k_count_keys<<<nblk(TN), 256, 0, st>>>(key, TN, size);
-    C2_LAUNCHED(ctx, "k_count_keys");
+  return canonicalize(ctx, n, t, N, key, next_id, split_nodes, max_depth, out);
+}
+
+// ------------------------------------------------------------------ C^2/MinHash variant (N3)
+// per function, u's cluster is the item of P_u with the smallest full-range hash
+// z_f(x) = a_f*x + c_f mod 2^64 (ties: lower item id) -- one cluster per item, no splitting.
+// Warp per user; lane f (+32) handles function f; item loads are warp broadcasts.
+__global__ void k_minhash_key(const int32_t *__restrict__ offs, const int32_t *__restrict__ items, int32_t n, int t,
+                              HashArgs2 ha, int64_t m, int32_t *__restrict__ key) {
+  const int lane = threadIdx.x & 31;
+  const int64_t u = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (u >= n) return;
+  const int32_t p0 = offs[u], p1 = offs[u + 1];
+  for (int f = lane; f < t; f += 32) {
+    const uint64_t a = ha.a[f], c = ha.c[f];
+    uint64_t best = ~0ull;
+    int32_t arg = INT32_MAX;
+    for (int32_t p = p0; p < p1; ++p) {
+      const int32_t x = __ldg(items + p);
+      const uint64_t z = a * (uint64_t)(uint32_t)x + c;
+      if (z < best || (z == best && x < arg)) {
+        best = z;
+        arg = x;
+      }
+    }
+    key[(int64_t)f * n + u] = (int32_t)((int64_t)f * m + arg);
   }
-  // rep[node] = smallest member; heads; canonical cluster index by scan over users
-  int32_t *rep = (int32_t *)ws_get(ctx, "rep", (size_t)next_id * 4, &rc);
-  if (rc) return rc;
-  C2_CUDA(ctx, cudaMemsetAsync(rep, 0x7F, (size_t)next_id * 4, st));
-  k_rep<<<nblk(TN), 256, 0, st>>>(key, TN, n, rep);
-  C2_LAUNCHED(ctx, "k_rep");
-  int32_t *head = (int32_t *)ws_get(ctx, "head", (size_t)(2 * TN + 2) * 4, &rc);
-  if (rc) return rc;
-  int32_t *hscan = head + TN + 1;
-  k_heads<<<nblk(TN), 256, 0, st>>>(key, rep, TN, n, head);
-  C2_LAUNCHED(ctx, "k_heads");
-  C2_TRY(scan_exclusive(ctx, head, hscan, TN));
-  const int64_t TN1 = (int64_t)t * (n + 1);
-  int32_t *csize = (int32_t *)ws_get(ctx, "csize", (size_t)(2 * TN1 + 2) * 4, &rc);
-  if (rc) return rc;
-  int32_t *craw = csize + TN1 + 1;
-  C2_CUDA(ctx, cudaMemsetAsync(csize, 0, (size_t)TN1 * 4, st));
-  k_cluster_of<<<nblk(TN), 256, 0, st>>>(key, rep, hscan, size, TN, n, out->cluster_of, csize, skey2, sval2);
-  C2_LAUNCHED(ctx, "k_cluster_of");
-  C2_TRY(scan_exclusive(ctx, csize, craw, TN1));
-  k_fix_offsets<<<nblk(TN1), 256, 0, st>>>(craw, TN1, n, out->offsets);
-  C2_LAUNCHED(ctx, "k_fix_offsets");
-  // members: stable sort of (f*n + cluster, u) by key -> ascending members per cluster
-  C2_TRY(radix_sort_pairs(ctx, skey2, sval2, skey, (uint32_t *)out->members, TN, bits_for(TN)));
-  C2_CUDA(ctx, cudaMemsetAsync(acc, 0, 8, st));
-  k_pairs<<<nblk(TN1), 256, 0, st>>>(csize, TN1, acc);
-  C2_LAUNCHED(ctx, "k_pairs");
-  C2_CUDA(ctx, cudaMemsetAsync(mx, 0, 4, st));
-  k_max<<<nblk(TN1), 256, 0, st>>>(csize, TN1, mx);
-  C2_LAUNCHED(ctx, "k_max");
-  // host values: n_clusters[f] = hscan[(f+1)n] - hscan[fn], P, max size
-  int32_t *hh = (int32_t *)ctx->h_small + 16;
-  for (int f = 0; f <= t; ++f)
-    C2_CUDA(ctx, cudaMemcpyAsync(hh + f, hscan + (int64_t)f * n, 4, cudaMemcpyDeviceToHost, st));
-  C2_CUDA(ctx, cudaMemcpyAsync(ctx->h_small, acc, 8, cudaMemcpyDeviceToHost, st));
-  C2_CUDA(ctx, cudaMemcpyAsync(ctx->h_small + 1, mx, 4, cudaMemcpyDeviceToHost, st));
-  C2_TRY(stream_sync(ctx, "canonical"));
-  int64_t total = 0;
+}
+
+int minhash_clusters(c2_ctx *ctx, const Csr &csr, int t, int64_t N, const HashParams *hp, Clusters *out) {
+  int rc;
+  const int32_t n = csr.n;
+  const int64_t TN = (int64_t)t * n;
+  const int64_t m = (int64_t)csr.max_item + 1;
+  if ((int64_t)t * m + TN + 1 >= (int64_t)INT32_MAX / 2)
+    return set_err(ctx, C2_EINVAL, "MinHash clustering needs t * (max item id + 1) < 2^30");
+  HashArgs2 ha;
   for (int f = 0; f < t; ++f) {
-    out->n_clusters[f] = hh[f + 1] - hh[f];
-    total += out->n_clusters[f];
+    ha.a[f] = hp->a[f];
+    ha.c[f] = hp->c[f];
   }
-  out->max_size = (int32_t)(ctx->h_small[1] & 0xffffffff);
-  ctx->stats.pairs = ctx->h_small[0];
-  ctx->stats.clusters = total;
-  ctx->stats.max_cluster_size = out->max_size;
-  ctx->stats.split_nodes = split_nodes;
-  ctx->stats.max_depth = max_depth;
-  ctx->stats.folded_singletons = folded;
-  ctx->stats.chunked_residuals = chunked;
-  if (ctx->timing) cudaEventRecord(ev[3], st);
-  return C2_OK;
+  cudaStream_t st = ctx->stream;
+  if (ctx->timing) {
+    cudaEventRecord(ctx->ev[0], st);
+    cudaEventRecord(ctx->ev[1], st);
+  }
+  int32_t *key = (int32_t *)ws_get(ctx, "key", (size_t)TN * 4, &rc);
+  if (rc) return rc;
+  unsigned long long *acc = (unsigned long long *)ws_get(ctx, "acc", 64, &rc);
+  if (rc) return rc;
+  C2_CUDA(ctx, cudaMemsetAsync(acc, 0, 64, st));
+  k_minhash_key<<<nblk((int64_t)n * 32), 256, 0, st>>>(csr.offs, csr.items, n, t, ha, m, key);
+  C2_LAUNCHED(ctx, "k_minhash_key");
+  if (ctx->timing) cudaEventRecord(ctx->ev[2], st);
+  return canonicalize(ctx, n, t, N, key, (int64_t)t * m, 0, 0, out);
 }
 
 }  // namespace c2

@@ -59,8 +59,12 @@ static uint64_t splitmix64(uint64_t *s) {
   return z ^ (z >> 31);
 }
 
-void make_hash_params(uint64_t seed, int t, HashParams *hp) {
+void make_hash_params(uint64_t seed, int t, HashParams *hp, int f0) {
   uint64_t s = seed;  // A2: (a_0, c_0, a_1, c_1, ...) from one stream
+  for (int f = 0; f < f0; ++f) {  // functions before the first one used (multi-GPU shards, N2)
+    splitmix64(&s);
+    splitmix64(&s);
+  }
   for (int f = 0; f < t; ++f) {
     hp->a[f] = splitmix64(&s);
     hp->c[f] = splitmix64(&s);
