@@ -34,6 +34,12 @@
 #ifndef C2_EPI
 #define C2_EPI 0  // 1: light rows filtered in the phase-A epilogue (measured slower)
 #endif
+#ifndef C2_SNAKE
+#define C2_SNAKE 1  // 1: warp w probes slices w, 2W-1-w, 2W+w, ... (slices are longest-first: balances warps)
+#endif
+#ifndef C2_BULK
+#define C2_BULK 1  // 1: tile records + staged row blocks by cp.async.bulk on mbarriers (TMA bulk path)
+#endif
 #ifndef C2_RANKMERGE
 #define C2_RANKMERGE 1  // 1: rank-based Alg. 3 step for <= 32 survivors; 0: insertion (<= 16)
 #endif
@@ -59,6 +65,34 @@ __device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((unsigned)__cvta_generic_to_shared(smem)), "l"(gmem));
 }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+// TMA bulk copies (cp.async.bulk, SASS UBLKCP) completing on an mbarrier: any thread can wait for
+// bytes another thread requested (unlike cp.async groups, which only the issuing thread can wait on).
+__device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t *mb, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(mb)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_tx(uint64_t *mb, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(mb)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *mb) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(mb))
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *mb, uint32_t parity) {
+  uint32_t done = 0;
+  for (;;) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}\n"
+        : "=r"(done)
+        : "r"(smem_u32(mb)), "r"(parity)
+        : "memory");
+    if (done) break;
+  }
+}
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
 
 #ifndef C2_TILE_T
 #define C2_TILE_T 512
@@ -988,6 +1022,75 @@ __global__ void __launch_bounds__(TILE_T, C2_TILE_MINB) k_local_tile(TileArgs a)
   const int nwin = a.nwin;
   const int kk = a.k;
   // one warp fetches the descriptors of tile item `it` into slot b
+#if C2_BULK
+  // next-tile descriptors in two halves: fetch_issue (one thread: claim the tile, bulk-copy its
+  // record) right when K8 starts, fetch_finish (the first warp out of K8 rows: wait for the record,
+  // parse it, bulk-copy the rows' packed blocks into the staging buffer) -- so no warp waits on a
+  // global round trip while others still have rows.  Every use of a slot's mbarriers gets exactly
+  // one arrival (0 bytes when there is no tile), so all threads can track the phases.
+  __shared__ __align__(8) uint64_t mb_rec[2], mb_stg[2];
+  __shared__ int s_claim;
+  if (tid == 0) {
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&mb_rec[i], 1);
+      mbar_init(&mb_stg[i], 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  uint32_t ph_rec = 0, ph_stg = 0;  // bit b: parity of the next completion of slot b
+  auto fetch_issue = [&](int b) {    // one thread
+    const int64_t it = a.lo + atomicAdd(a.counter, 1);
+    s_it[b] = it;
+    if (it < a.hi) {
+      fence_proxy_async();
+      mbar_arrive_tx(&mb_rec[b], REC_W * 4);
+      bulk_g2s(s_rec[b], a.rec + it * REC_W, REC_W * 4, &mb_rec[b]);
+    } else {
+      mbar_arrive_tx(&mb_rec[b], 0);
+    }
+  };
+  auto fetch_finish = [&](int b) {  // one warp
+    mbar_wait(&mb_rec[b], (ph_rec >> b) & 1u);
+    const int64_t it = s_it[b];
+    if (it >= a.hi) {
+      if (lane == 0) mbar_arrive_tx(&mb_stg[b], 0);
+      return;
+    }
+    const int32_t *rc = s_rec[b];
+    if (lane == 0) {
+      s_T[b] = Tile{rc[0], rc[1]};
+      s_B[b] = BigC{rc[2], rc[3], rc[4], rc[5], rc[6], rc[7]};
+    }
+    s_ru2[b][lane] = rc[64 + lane];
+    s_rp2[b][lane] = (uint32_t)rc[96 + lane];
+    const int32_t bl = lane < nwin ? rc[8 + lane] : 0;
+    const int32_t bo = lane < nwin ? rc[24 + lane] : 0;
+    int32_t incl = bl * 32;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    const int32_t tot = __shfl_sync(0xffffffffu, incl, 31);
+    const bool staged = tot <= a.stg_cap;
+    if (lane < nwin) {
+      s_bl[b][lane] = bl;
+      s_bo[b][lane] = bo;
+      s_so[b][lane] = incl - bl * 32;
+    }
+    if (lane == 0) {
+      s_stg[b] = staged ? 1 : 0;
+      fence_proxy_async();
+      mbar_arrive_tx(&mb_stg[b], staged ? (uint32_t)tot * 16u : 0u);
+    }
+    __syncwarp();
+    if (staged && lane < nwin && bl > 0)
+      bulk_g2s(stg + (incl - bl * 32), a.packed + (int64_t)bo * 32, (uint32_t)bl * 512u, &mb_stg[b]);
+  };
+  if (tid == 0) fetch_issue(0);
+  if (warp == 0) fetch_finish(0);
+#else
   auto fetch = [&](int b) {
     int64_t it = 0;
     if (lane == 0) it = a.lo + atomicAdd(a.counter, 1);
@@ -1030,10 +1133,20 @@ __global__ void __launch_bounds__(TILE_T, C2_TILE_MINB) k_local_tile(TileArgs a)
         for (int i = lane; i < n4; i += 32) cp_async16(stg + so + i, g + i);
       }
   };
+#endif
+#if !C2_BULK
   if (warp == 0) fetch(0);
+#endif
   int cur = 0;
   for (;;) {
+#if C2_BULK
+    mbar_wait(&mb_stg[cur], (ph_stg >> cur) & 1u);  // this tile's staged row blocks
+    ph_rec ^= 1u << cur;  // (slot cur's record and staging phases were consumed)
+    ph_stg ^= 1u << cur;
+    if (tid == 0) s_claim = 0;
+#else
     cp_async_wait_all();
+#endif
     __syncthreads();
     const int64_t it = s_it[cur];
     if (it >= a.hi) break;
@@ -1097,7 +1210,7 @@ __global__ void __launch_bounds__(TILE_T, C2_TILE_MINB) k_local_tile(TileArgs a)
         int nsteps = 0;
 #pragma unroll
         for (int q = 0; q < VPT; ++q) {
-          const int jj = g0 + q * TILE_WARPS + warp;
+          const int jj = g0 + q * TILE_WARPS + ((C2_SNAKE && (q & 1)) ? TILE_WARPS - 1 - warp : warp);
           if (jj < nsl) {
             const int64_t bi = (int64_t)(B.sl_off + jj) * nwin + w;
             const bool own = stgd && jj == T.j;  // the tile's own slice: staged
@@ -1153,7 +1266,7 @@ __global__ void __launch_bounds__(TILE_T, C2_TILE_MINB) k_local_tile(TileArgs a)
       //      SMEM_CNT: the host guarantees a single g0 group then)
 #pragma unroll
       for (int q = 0; q < VPT; ++q) {
-        const int jj = g0 + q * TILE_WARPS + warp;
+        const int jj = g0 + q * TILE_WARPS + ((C2_SNAKE && (q & 1)) ? TILE_WARPS - 1 - warp : warp);
         const int vi = jj * 32 + lane;
         if (jj < nsl) {
           uint32_t A[32];
@@ -1203,7 +1316,11 @@ __global__ void __launch_bounds__(TILE_T, C2_TILE_MINB) k_local_tile(TileArgs a)
     cp_async_wait_all();  // the running lists
     __syncthreads();
     // ================= K8: exact top-k per row, one warp per row (no CTA barrier inside)
+#if C2_BULK
+    if (tid == 0) fetch_issue(cur ^ 1);  // next tile's record: claimed and requested now
+#else
     if (warp == 0) fetch(cur ^ 1);  // next tile's descriptors, hidden behind this K8
+#endif
     const int slot = B.slot;  // mixed slice: candidates only inside the row's own slot group
     uint32_t *zq = nullptr;  // queue words the warp's previous row wrote (re-zeroed: M alias)
     int zn = 0;
@@ -1223,7 +1340,14 @@ __global__ void __launch_bounds__(TILE_T, C2_TILE_MINB) k_local_tile(TileArgs a)
       int idx = 0;
       if (lane == 0) idx = atomicAdd(&s_row, 1);
       idx = __shfl_sync(0xffffffffu, idx, 0);
-      if (idx >= nr) break;
+      if (idx >= nr) {
+#if C2_BULK
+        int claim = 0;
+        if (lane == 0) claim = atomicExch(&s_claim, 1);
+        if (__shfl_sync(0xffffffffu, claim, 0) == 0) fetch_finish(cur ^ 1);  // first warp out of rows
+#endif
+        break;
+      }
       const int r = idx < nheavy ? (int)__fns(heavy, 0, idx + 1) : (int)__fns(~heavy, 0, idx - nheavy + 1);
       const int32_t u = s_ru[r];
       if (u < 0) continue;
