@@ -57,6 +57,7 @@ def _load():
         "c2o_cluster": (_I, [_I64, _P, _P, _I, _I64, _P, _I64, _I, _P, _P, _P, _P, _P]),
         "c2o_minhash_cluster": (_I, [_I64, _P, _P, _I, _U64, _I64, _P, _P, _P, _P, _P]),
         "c2o_local_knn": (_I, [_I64, _P, _P, _I, _P, _P, _P, _I, _I, _P, _I64, _I, _P]),
+        "c2o_local_knn2": (_I, [_I64, _P, _P, _I, _P, _P, _P, _I, _I, _P, _I64, _I, _I, _U64, _P, _P]),
         "c2o_merge": (_I, [_I64, _I, _I, _P, _I, _P, _P, _P, _P]),
         "c2o_knn_union": (_I, [_I64, _P, _P, _I, _P, _P, _P, _I, _I, _P, _I64, _I, _P, _P, _P]),
         "c2o_knn_union_users": (_I, [_I64, _P, _P, _I, _P, _P, _P, _I, _I, _P, _I64, _I64, _P, _I, _P, _P, _P]),
@@ -173,14 +174,19 @@ def cluster_minhash(offs, items, seed: int, t: int, N: int) -> dict:
 
 
 # ------------------------------------------------------------------ steps 2-3
-def local_knn(offs, items, cl: dict, k: int, sim_mode: int = 0, gtab=None, nthreads: int | None = None):
+def local_knn(offs, items, cl: dict, k: int, sim_mode: int = 0, gtab=None, nthreads: int | None = None,
+              solver: int = 0, seed: int = 0, stats: dict | None = None):
+    """Alg. 2 per cluster: brute force (solver 0), or the hybrid with Hyrec for |C| >= 5k^2 (solver 1)."""
     offs, items, n = _csr(offs, items)
     t = cl["offsets"].shape[0]
     m = 0 if gtab is None else len(gtab)
     cand = np.zeros((t, n, k), CAND)
-    _chk(_load().c2o_local_knn(n, _ptr(offs), _ptr(items), t, _ptr(cl["offsets"]), _ptr(cl["members"]),
-                               _ptr(cl["n_clusters"]), k, sim_mode, _ptr(gtab), m, nthreads or NTHREADS,
-                               _ptr(cand)), "local_knn")
+    its = ctypes.c_int64(0)
+    _chk(_load().c2o_local_knn2(n, _ptr(offs), _ptr(items), t, _ptr(cl["offsets"]), _ptr(cl["members"]),
+                                _ptr(cl["n_clusters"]), k, sim_mode, _ptr(gtab), m, nthreads or NTHREADS, solver,
+                                seed, _ptr(cand), ctypes.byref(its)), "local_knn")
+    if stats is not None:
+        stats["hyrec_iters"] = its.value
     return cand
 
 
@@ -250,7 +256,8 @@ def pair_counts(offs, items, u, v):
 
 
 def build_graph(offs, items, *, k: int, t: int, b: int, N: int, seed: int, sim_mode: int = 0, htab=None,
-                nthreads: int | None = None, formulation: int = 0, clustering: str = "frh") -> dict:
+                nthreads: int | None = None, formulation: int = 0, clustering: str = "frh",
+                solver: int = 0) -> dict:
     """Whole C^2 pipeline on the CPU: FRH (or MinHash) clustering -> local brute force -> Alg. 3."""
     offs, items, n = _csr(offs, items)
     m = int(items.max()) + 1 if len(items) else 1
@@ -261,6 +268,8 @@ def build_graph(offs, items, *, k: int, t: int, b: int, N: int, seed: int, sim_m
         if htab is None:
             htab = hash_table(seed, t, b, m)
         cl = cluster(offs, items, htab, N, formulation)
-    cand = local_knn(offs, items, cl, k, sim_mode, gtab, nthreads)
+    st = {}
+    cand = local_knn(offs, items, cl, k, sim_mode, gtab, nthreads, solver=solver, seed=seed, stats=st)
     nbr, inter, uni, sim = merge(cand, nthreads)
-    return dict(clusters=cl, cand=cand, nbr=nbr, inter=inter, uni=uni, sim=sim, htab=htab, gtab=gtab)
+    return dict(clusters=cl, cand=cand, nbr=nbr, inter=inter, uni=uni, sim=sim, htab=htab, gtab=gtab,
+                hyrec_iters=st.get("hyrec_iters", 0))

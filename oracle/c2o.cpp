@@ -379,9 +379,67 @@ int c2o_minhash_cluster(int64_t n, const int32_t *offs, const int32_t *items, in
   return 0;
 }
 
-int c2o_local_knn(int64_t n, const int32_t *offs, const int32_t *items, int t, const int32_t *offsets,
-                  const int32_t *members, const int32_t *n_clusters, int k, int sim_mode, const uint16_t *gtab,
-                  int64_t m, int nthreads, c2o_cand *cand) {
+// SplitMix64 finalizer (the mixing function of c2o_splitmix64_next) used as a counter-based
+// generator for Hyrec's random initial graph.
+static inline uint64_t mix64(uint64_t z) {
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+  return z ^ (z >> 31);
+}
+
+// Hyrec on one cluster (Alg. 2 else-branch; reading A34 in DESIGN.md):
+// start from a random k-degree graph over C, then repeatedly compare every user with the
+// neighbours of its neighbours and keep the k best (synchronous iterations: all users read the
+// previous iteration's graph); stop when fewer than delta*k*|C| neighbourhood entries changed
+// (delta = 0.001) or after 30 iterations.  Output: k best-first lists.
+static void hyrec_cluster(const Profiles &P, const int32_t *C, int64_t s, int f, int k, uint64_t seed,
+                          c2o_cand *out_base, int64_t n, int64_t *iters_out) {
+  std::map<int32_t, int64_t> local;
+  for (int64_t a = 0; a < s; ++a) local[C[a]] = a;
+  std::vector<std::vector<int32_t>> N(s);  // local indices
+  for (int64_t a = 0; a < s; ++a) {
+    const uint64_t key = mix64(mix64((seed ^ C2O_HYREC_SALT) + (uint64_t)f) + (uint64_t)C[a]);
+    for (uint64_t j = 0; (int)N[a].size() < k; ++j) {
+      const uint64_t r = mix64(key + j + 1);
+      const int64_t b = (int64_t)(((unsigned __int128)r * (unsigned __int128)(uint64_t)s) >> 64);
+      if (b == a || std::find(N[a].begin(), N[a].end(), (int32_t)b) != N[a].end()) continue;
+      N[a].push_back((int32_t)b);
+    }
+  }
+  std::vector<std::vector<c2o_cand>> L(s);
+  int64_t it = 0;
+  for (;;) {
+    int64_t updates = 0;
+    std::vector<std::vector<int32_t>> Nn(s);
+    for (int64_t a = 0; a < s; ++a) {
+      std::vector<int32_t> cand(N[a].begin(), N[a].end());
+      for (int32_t b : N[a]) cand.insert(cand.end(), N[b].begin(), N[b].end());  // neighbours' neighbours
+      std::sort(cand.begin(), cand.end());
+      cand.erase(std::unique(cand.begin(), cand.end()), cand.end());
+      std::vector<c2o_cand> cs;
+      for (int32_t b : cand)
+        if (b != a) cs.push_back(P.cand(C[a], C[b]));
+      std::sort(cs.begin(), cs.end(), better);
+      cs.resize(std::min<size_t>(cs.size(), (size_t)k));
+      for (const c2o_cand &x : cs) {
+        const int32_t b = (int32_t)local[x.id];
+        Nn[a].push_back(b);
+        if (std::find(N[a].begin(), N[a].end(), b) == N[a].end()) ++updates;
+      }
+      L[a] = cs;
+    }
+    N.swap(Nn);
+    ++it;
+    if (updates * C2O_HYREC_DELTA_INV < (int64_t)k * s || it >= C2O_HYREC_MAX_ITERS) break;
+  }
+  for (int64_t a = 0; a < s; ++a)
+    for (int j = 0; j < k; ++j) out_base[(int64_t)C[a] * k + j] = j < (int)L[a].size() ? L[a][j] : PAD;
+  if (iters_out) *iters_out = it;
+}
+
+int c2o_local_knn2(int64_t n, const int32_t *offs, const int32_t *items, int t, const int32_t *offsets,
+                   const int32_t *members, const int32_t *n_clusters, int k, int sim_mode, const uint16_t *gtab,
+                   int64_t m, int nthreads, int solver, uint64_t seed, c2o_cand *cand, int64_t *hyrec_iters) {
   if (k < 1 || t < 1) return -1;
   if (!row_ok(offs, items, n, m)) return -2;
   Profiles P(n, offs, items, sim_mode, gtab);
@@ -393,11 +451,21 @@ int c2o_local_knn(int64_t n, const int32_t *offs, const int32_t *items, int t, c
       work.push_back({-s, {f, c}});
     }
   std::sort(work.begin(), work.end());
+  std::atomic<int64_t> hit(0);
   parallel_for((int64_t)work.size(), nthreads, [&](int64_t w) {
     int f = work[w].second.first;
     int32_t c = work[w].second.second;
     const int32_t *C = members + f * n + offsets[f * (n + 1) + c];
     int64_t s = -work[w].first;
+    // Alg. 2: brute force if |C| < rho k^2, else Hyrec -- with solver = 1 only; the
+    // default (solver = 0) is brute force for every cluster (A12, BASELINE.json north_star).
+    const bool hyrec = (solver == 1 && s >= (int64_t)C2O_HYREC_RHO * k * k) || (solver == 2 && s > k);
+    if (hyrec) {
+      int64_t its = 0;
+      hyrec_cluster(P, C, s, f, k, seed, cand + (int64_t)f * n * k, n, &its);
+      hit += its;
+      return;
+    }
     // Brute force: the s(s-1)/2 similarities of the cluster, each computed once.
     std::vector<c2o_cand> sims((size_t)(s * s));
     for (int64_t a = 0; a < s; ++a)
@@ -414,7 +482,15 @@ int c2o_local_knn(int64_t n, const int32_t *offs, const int32_t *items, int t, c
       write_topk(cands, k, cand + ((int64_t)f * n + C[a]) * k);
     }
   });
+  if (hyrec_iters) *hyrec_iters = hit.load();
   return 0;
+}
+
+int c2o_local_knn(int64_t n, const int32_t *offs, const int32_t *items, int t, const int32_t *offsets,
+                  const int32_t *members, const int32_t *n_clusters, int k, int sim_mode, const uint16_t *gtab,
+                  int64_t m, int nthreads, c2o_cand *cand) {
+  return c2o_local_knn2(n, offs, items, t, offsets, members, n_clusters, k, sim_mode, gtab, m, nthreads, 0, 0,
+                        cand, nullptr);
 }
 
 int c2o_merge(int64_t n, int t, int k, const c2o_cand *cand, int nthreads, int32_t *nbr, uint16_t *inter,

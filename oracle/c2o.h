@@ -31,6 +31,13 @@ typedef struct {
 #define C2O_ABSENT 0xFFFFu
 #define C2O_GF_BITS 1024
 #define C2O_GF_SALT 0x476f6c6446696e67ULL /* "GoldFing" */
+/* Alg. 2 hybrid: Hyrec for clusters with |C| >= rho k^2, rho = 5; delta = 0.001 and at
+ * most 30 iterations; the initial random graph is drawn from SplitMix64-mixed counters
+ * seeded with seed ^ C2O_HYREC_SALT (reading A34). */
+#define C2O_HYREC_RHO 5
+#define C2O_HYREC_DELTA_INV 1000
+#define C2O_HYREC_MAX_ITERS 30
+#define C2O_HYREC_SALT 0x4879726563526e67ULL /* "HyrecRng" */
 
 /* SplitMix64 generator step (A2). */
 uint64_t c2o_splitmix64_next(uint64_t *state);
@@ -76,6 +83,13 @@ int c2o_minhash_cluster(int64_t n, const int32_t *offs, const int32_t *items, in
 int c2o_local_knn(int64_t n, const int32_t *offs, const int32_t *items, int t, const int32_t *offsets,
                   const int32_t *members, const int32_t *n_clusters, int k, int sim_mode, const uint16_t *gtab,
                   int64_t m, int nthreads, c2o_cand *cand);
+/* As c2o_local_knn with the local solver selectable: solver 0 = brute force everywhere (A12),
+ * 1 = Alg. 2 hybrid: brute force if |C| < rho k^2, else Hyrec; 2 = test hook: Hyrec for
+ * every cluster with |C| > k.  hyrec_iters (nullable)
+ * receives the total number of Hyrec iterations run. */
+int c2o_local_knn2(int64_t n, const int32_t *offs, const int32_t *items, int t, const int32_t *offsets,
+                   const int32_t *members, const int32_t *n_clusters, int k, int sim_mode, const uint16_t *gtab,
+                   int64_t m, int nthreads, int solver, uint64_t seed, c2o_cand *cand, int64_t *hyrec_iters);
 
 /* Step 3, Alg. 3: per user, add the t partial neighbourhoods into a set bounded
  * to k keeping the best, reusing similarity values; output sorted best-first, padded.

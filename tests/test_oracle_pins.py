@@ -552,3 +552,99 @@ def test_minhash_collision_probability_is_jaccard(J_target):
     p_hat = float((cl["cluster_of"][:, 0] == cl["cluster_of"][:, 1]).mean())
     sd = math.sqrt(J * (1 - J) / T)
     assert abs(p_hat - J) <= 4 * sd + 0.02, (p_hat, J)
+
+
+# ----------------------------------------------------------------- Hyrec (Alg. 2 else-branch, N4)
+def _mix64(z):
+    z &= 2**64 - 1
+    z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & (2**64 - 1)
+    z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & (2**64 - 1)
+    return z ^ (z >> 31)
+
+
+def _hyrec_py(rows, C, f, k, seed):
+    """Independent pure-Python Hyrec: random k-graph, then synchronous rounds of
+    'compare u with its neighbours' neighbours, keep the k best' until < 0.001 k |C| entries
+    change or 30 rounds."""
+    SALT = 0x4879726563526E67
+    s = len(C)
+    sets = [set(rows[u]) for u in C]
+
+    def key(a, b):  # exact order: J desc (cross products), then id asc
+        i = len(sets[a] & sets[b])
+        U = len(sets[a]) + len(sets[b]) - i
+        return (Fraction(-i, U), C[b]), (C[b], i, U)
+
+    N = []
+    for a in range(s):
+        kk = _mix64(_mix64(((seed ^ SALT) + f) & (2**64 - 1)) + C[a])
+        nb, j = [], 0
+        while len(nb) < k:
+            b = (_mix64(kk + j + 1) * s) >> 64
+            j += 1
+            if b != a and b not in nb:
+                nb.append(b)
+        N.append(nb)
+    it = 0
+    while True:
+        upd, Nn, L = 0, [], []
+        for a in range(s):
+            cand = set(N[a])
+            for b in N[a]:
+                cand |= set(N[b])
+            cand.discard(a)
+            best = sorted(cand, key=lambda b: key(a, b)[0])[:k]
+            upd += sum(1 for b in best if b not in N[a])
+            Nn.append(best)
+            L.append([key(a, b)[1] for b in best])
+        N = Nn
+        it += 1
+        if upd * 1000 < k * s or it >= 30:
+            return L
+
+
+@pytest.mark.parametrize("seed", range(3))
+def test_hyrec_vs_python(seed):
+    rng = np.random.default_rng(70 + seed)
+    offs, items = synth.random_instance(rng, 60, 40, 2, 12)
+    rows = [items[offs[u]:offs[u + 1]].tolist() for u in range(60)]
+    k = 4
+    cl = oracle.cluster(offs, items, oracle.hash_table(1, 1, 1, 40), 10**6)  # b = 1: one cluster of 60
+    cand = oracle.local_knn(offs, items, cl, k, solver=2, seed=seed)
+    C = cl["members"][0][:60].tolist()
+    exp = _hyrec_py(rows, C, 0, k, seed)
+    for a, u in enumerate(C):
+        assert [tuple(int(x) for x in e) for e in cand[0, u]] == exp[a]
+
+
+def test_hyrec_small_cluster_is_exact():
+    # |C| = k + 1: the random initial graph already holds every other member, so Hyrec returns
+    # the exact neighbourhoods (= brute force) after one round
+    rng = np.random.default_rng(5)
+    offs, items = synth.random_instance(rng, 9, 30, 2, 10)
+    cl = oracle.cluster(offs, items, oracle.hash_table(1, 1, 1, 30), 10**6)
+    a = oracle.local_knn(offs, items, cl, 8, solver=2, seed=1)
+    b = oracle.local_knn(offs, items, cl, 8, solver=0)
+    assert np.array_equal(a, b)
+
+
+def test_hyrec_quality_on_planted_clusters():
+    # SPEC greedy_knn example: planted clusters -> Hyrec quality (Eq. 2) >= 0.85 of brute force
+    rng = np.random.default_rng(8)
+    rows = []
+    for g in range(10):
+        base = rng.choice(np.arange(g * 40, g * 40 + 40), 25, replace=False)
+        for _ in range(50):
+            rows.append(sorted(set(rng.choice(base, 12, replace=False).tolist()) | set(rng.choice(400, 2).tolist())))
+    offs, items = csr(rows)
+    k = 10
+    cl = oracle.cluster(offs, items, oracle.hash_table(1, 1, 1, 401), 10**6)
+    st = {}
+    h = oracle.local_knn(offs, items, cl, k, solver=1, seed=2, stats=st)  # 500 >= 5 k^2: Hyrec branch
+    e = oracle.local_knn(offs, items, cl, k, solver=0)
+    assert st["hyrec_iters"] >= 1
+
+    def qsum(c):
+        ok = c["id"] >= 0
+        return float((c["inter"][ok] / c["uni"][ok]).sum())
+    assert qsum(h) >= 0.85 * qsum(e)
