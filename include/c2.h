@@ -101,10 +101,18 @@ enum {
                               identical either way. */
   C2_OPT_CLUSTERING = 6,   /* Step 1 of c2_fastrandomhash / c2_build: C2_CLUSTER_FRH (default) or
                               C2_CLUSTER_MINHASH (the paper's C^2/MinHash ablation) */
-  C2_OPT_FUNC_OFFSET = 7   /* f0 >= 0 (default 0): the t functions used are functions f0 .. f0+t-1 of the
+  C2_OPT_FUNC_OFFSET = 7,  /* f0 >= 0 (default 0): the t functions used are functions f0 .. f0+t-1 of the
                               seed's stream (A2), so G processes that each run t/G consecutive functions
                               together run exactly the functions of one t-function run (multi-GPU by
                               hash function; their merged lists equal the single run's, A16) */
+  C2_OPT_LOCAL_SOLVER = 8  /* Step 2's per-cluster solver: C2_SOLVER_BRUTE (default, every cluster, A12) or
+                              C2_SOLVER_HYBRID (Alg. 2: brute force if |C| < 5k^2, else Hyrec) */
+};
+enum {
+  C2_SOLVER_BRUTE = 0,
+  C2_SOLVER_HYBRID = 1 /* Hyrec: random initial k-graph (SplitMix64-mixed counters from the call's
+                          seed), synchronous neighbours-of-neighbours rounds until fewer than 0.001*k*|C|
+                          entries change or 30 rounds; item ids must fit a shared-memory bitmap */
 };
 enum {
   C2_CLUSTER_FRH = 0,    /* FastRandomHash + recursive split */

@@ -92,6 +92,7 @@ int build_device(c2_ctx *ctx, const int32_t *offs, const int32_t *items, int32_t
   else C2_TRY(fastrandomhash(ctx, csr, t, b, N, &hp, nullptr, 0, &cl));
   Csr sims = csr;
   if (sim_mode == C2_SIM_GF1024) C2_TRY(gf_encode(ctx, csr, &hp, &sims));
+  ctx->hyrec_seed = seed;
   int rc;
   // Steps 2+3 fused: function by function, every local neighbourhood is merged into the
   // running Alg. 3 result; the final lists equal merge(local lists) exactly.
@@ -181,6 +182,10 @@ int c2_ctx_set_option(c2_ctx *ctx, int key, int64_t value) {
     case C2_OPT_TIMING: ctx->timing = value != 0; return C2_OK;
     case C2_OPT_KSTATS: ctx->kstats = (unsigned long long *)(intptr_t)value; return C2_OK;
     case C2_OPT_RELABEL: ctx->relabel = value != 0; return C2_OK;
+    case C2_OPT_LOCAL_SOLVER:
+      if (value != C2_SOLVER_BRUTE && value != C2_SOLVER_HYBRID) return set_err(ctx, C2_EINVAL, "bad local solver");
+      ctx->solver = (int)value;
+      return C2_OK;
     case C2_OPT_FUNC_OFFSET:
       if (value < 0 || value > (1 << 20)) return set_err(ctx, C2_EINVAL, "bad function offset");
       ctx->func_offset = (int)value;
@@ -287,6 +292,7 @@ int c2_local_knn(c2_ctx *ctx, const int32_t *csr_offsets, const int32_t *item_id
   cl.max_size = hmx;
   Csr sims = csr;
   if (sim_mode == C2_SIM_GF1024) C2_TRY(gf_encode(ctx, csr, &hp, &sims));
+  ctx->hyrec_seed = seed;
   return local_knn(ctx, sims, t, cl, k, cand, false, nullptr);
 }
 

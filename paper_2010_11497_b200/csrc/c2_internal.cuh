@@ -29,7 +29,9 @@ struct c2_ctx {
   bool timing = false;
   unsigned long long *kstats = nullptr;
   int clustering = 0;
-  int func_offset = 0;  // C2_OPT_FUNC_OFFSET   // C2_OPT_CLUSTERING: 0 FastRandomHash (Step 1 of C^2), 1 MinHash (N3 variant)
+  int func_offset = 0;  // C2_OPT_FUNC_OFFSET
+  int solver = 0;       // C2_OPT_LOCAL_SOLVER: 0 brute force everywhere (A12), 1 Alg. 2 hybrid (Hyrec)
+  uint64_t hyrec_seed = 0;  // the call's seed (Hyrec's random initial graphs)   // C2_OPT_CLUSTERING: 0 FastRandomHash (Step 1 of C^2), 1 MinHash (N3 variant)
   bool relabel = true;  // C2_OPT_RELABEL  (C2_OPT_KSTATS: kstats = dev [80] K7/K8 counters)
   c2_stats stats{};
   // device workspace: name -> (ptr, bytes); grow-only
@@ -104,6 +106,10 @@ int gf_encode(c2_ctx *ctx, const Csr &csr, const HashParams *hp, Csr *gf);
 // final lists [n][k], updated in place function by function (Alg. 3 fused, c2_build).
 int local_knn(c2_ctx *ctx, const Csr &csr, int t, const Clusters &cl, int k, c2_cand *out, bool fused,
               c2_cand **result);
+// Alg. 2 else-branch (k_hyrec.cu): Hyrec on the nh clusters listed (global cluster ids) in sval_h.
+int hyrec_clusters(c2_ctx *ctx, const Csr &csr, int t, const int32_t *offsets, const int32_t *members,
+                   const int32_t *ccum, const uint32_t *sval_h, int64_t nh, const int32_t *hyrec_f_lo, int k,
+                   uint64_t seed, c2_cand *out, bool fused);
 
 // Step 3 (k_merge.cu).  copyout: c2_build's final format conversion of the fused running lists.
 int copyout(c2_ctx *ctx, int n, int k, const c2_cand *run, int32_t *nbr, uint16_t *inter, uint16_t *uni,

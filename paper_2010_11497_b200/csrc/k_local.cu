@@ -124,6 +124,7 @@ __device__ __forceinline__ int find_f(const int32_t *ccum, int t, int64_t g) {
 // category of every cluster: big (> 32 users), small (2..32), single.  One 32-bit sort key
 // orders them [big: by function, then size descending][small: by function, slot class]
 // [single: by function]; counts per (category, f, class) go to cnt_fc.
+constexpr int WLC = 16;  // counters per function: 0 big tiles, 1..5 small per class, 6 single, 7 big, 8 hyrec
 __device__ __forceinline__ int slot_class(int32_t s) {  // slot = 2^class >= s, s in [2, 32]
   int c = 1;
   while ((1 << c) < s) ++c;
@@ -132,7 +133,7 @@ __device__ __forceinline__ int slot_class(int32_t s) {  // slot = 2^class >= s, 
 
 __global__ void k_wl_classify(const int32_t *__restrict__ offsets, const int32_t *__restrict__ ccum, int t,
                               int32_t n, int64_t C, uint32_t *__restrict__ key, uint32_t *__restrict__ val,
-                              uint32_t maxs, int sized, int32_t *__restrict__ cnt_fc) {
+                              uint32_t maxs, int sized, int32_t *__restrict__ cnt_fc, uint32_t hyrec_min) {
   int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (g >= C) return;
   int f = find_f(ccum, t, g);
@@ -140,17 +141,20 @@ __global__ void k_wl_classify(const int32_t *__restrict__ offsets, const int32_t
   const int32_t *off = offsets + (int64_t)f * (n + 1);
   uint32_t s = (uint32_t)(off[c + 1] - off[c]);
   uint32_t k;
-  if (s > 32) {
+  if (s >= hyrec_min) {  // Alg. 2 else-branch: Hyrec (C2_SOLVER_HYBRID only; hyrec_min = UINT32_MAX otherwise)
+    k = (3u << 30) | ((uint32_t)f << 24);
+    atomicAdd(&cnt_fc[f * WLC + 8], 1);
+  } else if (s > 32) {
     k = ((uint32_t)f << 24) | (sized ? min(maxs - s, 0xFFFFFFu) : 0u);
-    atomicAdd(&cnt_fc[f * 8 + 0], (int32_t)((s + 31) / 32));  // big tiles of f
-    atomicAdd(&cnt_fc[f * 8 + 7], 1);                          // big clusters of f
+    atomicAdd(&cnt_fc[f * WLC + 0], (int32_t)((s + 31) / 32));  // big tiles of f
+    atomicAdd(&cnt_fc[f * WLC + 7], 1);                          // big clusters of f
   } else if (s >= 2) {
     int cl = slot_class((int32_t)s);
     k = (1u << 30) | ((uint32_t)f << 24) | (uint32_t)cl;
-    atomicAdd(&cnt_fc[f * 8 + cl], 1);  // small clusters of (f, class), class 1..5
+    atomicAdd(&cnt_fc[f * WLC + cl], 1);  // small clusters of (f, class), class 1..5
   } else {
     k = (2u << 30) | ((uint32_t)f << 24);
-    atomicAdd(&cnt_fc[f * 8 + 6], 1);  // singletons of f
+    atomicAdd(&cnt_fc[f * WLC + 6], 1);  // singletons of f
   }
   key[g] = k;
   val[g] = (uint32_t)g;
@@ -1783,17 +1787,19 @@ int local_knn(c2_ctx *ctx, const Csr &csr_in, int t, const Clusters &cl, int k, 
   hcum[0] = 0;
   for (int f = 0; f < t; ++f) hcum[f + 1] = hcum[f] + cl.n_clusters[f];
   const int64_t C = hcum[t];
-  int32_t *ccum = (int32_t *)ws_get(ctx, "wl_ccum", (C2_MAX_T + 1) * 4 + 4 * 8 * C2_MAX_T, &rc);
+  int32_t *ccum = (int32_t *)ws_get(ctx, "wl_ccum", (C2_MAX_T + 1) * 4 + 4 * WLC * C2_MAX_T, &rc);
   if (rc) return rc;
-  int32_t *cnt_fc = ccum + C2_MAX_T + 1;  // [f][8]: 0 big tiles, 1..5 small per class, 6 single, 7 big
+  int32_t *cnt_fc = ccum + C2_MAX_T + 1;  // [f][WLC]
   C2_CUDA(ctx, cudaMemcpyAsync(ccum, hcum, (t + 1) * 4, cudaMemcpyHostToDevice, st));
-  C2_CUDA(ctx, cudaMemsetAsync(cnt_fc, 0, 4 * 8 * C2_MAX_T, st));
+  C2_CUDA(ctx, cudaMemsetAsync(cnt_fc, 0, 4 * WLC * C2_MAX_T, st));
   uint32_t *kv = (uint32_t *)ws_get(ctx, "wl_kv", (size_t)C * 4 * 4 + 16, &rc);
   if (rc) return rc;
   uint32_t *key = kv, *val = kv + C, *skey = kv + 2 * C, *sval = kv + 3 * C;
-  const uint32_t maxs = (uint32_t)std::max(cl.max_size, 1);
+  // Alg. 2: with the hybrid solver, clusters of >= rho k^2 users go to Hyrec
+  const uint32_t hyrec_min = ctx->solver == 1 ? (uint32_t)(5 * k * k) : 0xFFFFFFFFu;
+  const uint32_t maxs = (uint32_t)std::max(std::min<int64_t>(cl.max_size, (int64_t)hyrec_min - 1), (int64_t)1);
   const int sized = maxs < (1u << 24) ? 1 : 0;
-  k_wl_classify<<<nblk(C), 256, 0, st>>>(cl.offsets, ccum, t, n, C, key, val, maxs, sized, cnt_fc);
+  k_wl_classify<<<nblk(C), 256, 0, st>>>(cl.offsets, ccum, t, n, C, key, val, maxs, sized, cnt_fc, hyrec_min);
   C2_LAUNCHED(ctx, "k_wl_classify");
   C2_TRY(radix_sort_pairs(ctx, key, val, skey, sval, C, 32));
   unsigned long long *wacc = (unsigned long long *)ws_get(ctx, "work_acc", 16, &rc);
@@ -1801,18 +1807,21 @@ int local_knn(c2_ctx *ctx, const Csr &csr_in, int t, const Clusters &cl, int k, 
   C2_CUDA(ctx, cudaMemsetAsync(wacc, 0, 8, st));
   k_work_steps<<<nblk((int64_t)t * n), 256, 0, st>>>(cl.offsets, cl.cluster_of, csr.psize, (int64_t)t * n, n, wacc);
   C2_LAUNCHED(ctx, "k_work_steps");
-  int32_t hfc[8 * C2_MAX_T];
+  int32_t hfc[WLC * C2_MAX_T];
   unsigned long long hwork = 0;
-  C2_CUDA(ctx, cudaMemcpyAsync(hfc, cnt_fc, 4 * 8 * t, cudaMemcpyDeviceToHost, st));
+  C2_CUDA(ctx, cudaMemcpyAsync(hfc, cnt_fc, 4 * WLC * t, cudaMemcpyDeviceToHost, st));
   C2_CUDA(ctx, cudaMemcpyAsync(&hwork, wacc, 8, cudaMemcpyDeviceToHost, st));
   C2_TRY(stream_sync(ctx, "worklist counts"));
   ctx->stats.work_steps = (int64_t)hwork;
-  int64_t nbig = 0, nsmall = 0, nsingle = 0, nbigtiles = 0;
+  int64_t nbig = 0, nsmall = 0, nsingle = 0, nbigtiles = 0, nhyrec = 0;
+  int32_t hy_lo[C2_MAX_T + 1];
   for (int f = 0; f < t; ++f) {
-    nbig += hfc[f * 8 + 7];
-    nbigtiles += hfc[f * 8 + 0];
-    for (int c = 1; c <= 5; ++c) nsmall += hfc[f * 8 + c];
-    nsingle += hfc[f * 8 + 6];
+    hy_lo[f] = (int32_t)nhyrec;
+    nhyrec += hfc[f * WLC + 8];
+    nbig += hfc[f * WLC + 7];
+    nbigtiles += hfc[f * WLC + 0];
+    for (int c = 1; c <= 5; ++c) nsmall += hfc[f * WLC + c];
+    nsingle += hfc[f * WLC + 6];
   }
   // mixed slices: groups (f, class) in sorted order
   std::vector<MixGroup> groups;
@@ -1821,7 +1830,7 @@ int local_knn(c2_ctx *ctx, const Csr &csr_in, int t, const Clusters &cl, int k, 
   for (int f = 0; f < t; ++f) {
     mix_lo[f] = nmix;
     for (int c = 1; c <= 5; ++c) {
-      int32_t cntc = hfc[f * 8 + c];
+      int32_t cntc = hfc[f * WLC + c];
       if (!cntc) continue;
       int per = 32 >> c;
       groups.push_back(MixGroup{f, c, (int32_t)entry, cntc, (int32_t)nmix});
@@ -1831,10 +1840,15 @@ int local_knn(c2_ctx *ctx, const Csr &csr_in, int t, const Clusters &cl, int k, 
   }
   mix_lo[t] = nmix;
 
+  hy_lo[t] = (int32_t)nhyrec;
   if (fused) {
     k_init_pads<<<nblk((int64_t)n * k), 256, 0, st>>>(out, (int64_t)n * k);
     C2_LAUNCHED(ctx, "k_init_pads");
   }
+  // Hyrec clusters (sorted after the singletons): their lists go straight to cand (local mode) or
+  // are merged into the running lists (fused), before the tiles (the merge is order-independent)
+  C2_TRY(hyrec_clusters(ctx, csr, t, cl.offsets, cl.members, ccum, sval + (C - nhyrec), nhyrec, hy_lo, k,
+                        ctx->hyrec_seed, out, fused));
 
   // ---- tile descriptors: big clusters (length-sorted members) + mixed slices
   const int64_t ncl = nbig + nmix;
@@ -2045,7 +2059,7 @@ int local_knn(c2_ctx *ctx, const Csr &csr_in, int t, const Clusters &cl, int k, 
     // its neighbourhood in that function's cluster (singletons: nothing to merge)
     int64_t blo = 0;
     for (int f = 0; f < t; ++f) {
-      int64_t bhi = blo + hfc[f * 8 + 0];
+      int64_t bhi = blo + hfc[f * WLC + 0];
       C2_TRY(launch_tiles(blo, bhi, 2 * f, out, out));
       C2_TRY(launch_tiles(nbigtiles + mix_lo[f], nbigtiles + mix_lo[f + 1], 2 * f + 1, out, out));
       blo = bhi;
