@@ -3,8 +3,11 @@
 // K1: for every user u and function f, the D smallest DISTINCT values of {h_f(x) : x in P_u}
 // (ascending, C2_ABSENT padded).  Element 0 is H_f(u) = min_{i in P_u} h_f(i); element
 // d+1 is H\eta(u) with eta = element d (reading A5), so the recursive split never has to
-// revisit the CSR while its depth stays below D (A29).  One pass over the item list computes
-// all t functions (TF per pass), keeping a sorted distinct top-8 per function in registers.
+// revisit the CSR while its depth stays below D (A29).  k_sketch_w (hashed, the product path):
+// one warp per user, bitmap windows (below); k_sketch (an injected hash table, the paper's worked
+// examples): G lanes per user, a sorted distinct top-8 per (user, function) in registers.
+#include <algorithm>
+
 #include "c2_internal.cuh"
 
 namespace c2 {
@@ -74,6 +77,162 @@ __global__ void __launch_bounds__(256) k_sketch(const int32_t *__restrict__ offs
   }
 }
 
+// Hashed sketch (no injected table): one warp per user, lanes striding the user's items with
+// coalesced loads; all functions of a group of SK_FG are hashed from each loaded item.  The D
+// smallest distinct values of function f are found with a shared-memory bitmap over a value
+// window [base_f, base_f + Wv): every hash in the window sets its bit (atomicOr, so duplicates
+// merge), then the warp reads the window's words in order (ballot-free: popc + warp scan) and
+// takes the first D set bits.  Wv is sized from |P_u| so ~SK_K values fall in the first window
+// (E = |P_u| * Wv / b); a function that finds fewer than D values there (and has values left
+// above the window) slides its window up and re-reads the items -- exact for every (b, |P_u|).
+// Per item and function: one 64-bit multiply-add, a compare, and for ~SK_K/|P_u| of them one
+// shared atomic; no per-lane sorted inserts (the divergence of the thread-per-(user, f) form).
+constexpr int SK_WARPS = 8;
+constexpr int SK_FG = 8;      // functions per pass over the items
+constexpr int SK_CAPW = 128;  // window words per function (4096 values)
+constexpr int SK_K = 16;      // target number of hashed values inside the first window
+
+template <bool POW2>
+__global__ void __launch_bounds__(SK_WARPS * 32, 3) k_sketch_w(const int32_t *__restrict__ offs,
+                                                            const int32_t *__restrict__ items, int32_t n, int t,
+                                                            uint32_t b, HashArgs ha, int D,
+                                                            uint16_t *__restrict__ out) {
+  __shared__ __align__(16) uint32_t bm[SK_WARPS][SK_FG * SK_CAPW];
+  __shared__ __align__(16) uint16_t sv[SK_WARPS][SK_FG][C2_SKETCH_D];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  // extraction and output: the 4 lanes 4f..4f+3 own function f of the group
+  const int myf = lane >> 2, sub = lane & 3;
+  uint32_t *B = bm[w];
+  for (int i = lane; i < SK_FG * SK_CAPW; i += 32) B[i] = 0;
+  __syncwarp();
+  const int sh = POW2 ? 65 - __ffs(b) : 0;
+  const int64_t nwarps = (int64_t)gridDim.x * SK_WARPS;
+  const float kb = (float)SK_K * (float)b;
+  for (int f0 = 0; f0 < t; f0 += SK_FG) {
+    const int nf = min(SK_FG, t - f0);
+    uint64_t fa[SK_FG], fc[SK_FG];
+#pragma unroll
+    for (int f = 0; f < SK_FG; ++f) {
+      fa[f] = f < nf ? ha.a[f0 + f] : 0;
+      fc[f] = f < nf ? ha.c[f0 + f] : 0;
+    }
+    for (int64_t u = (int64_t)blockIdx.x * SK_WARPS + w; u < n; u += nwarps) {
+      const int32_t p0 = __ldg(offs + u), p1 = __ldg(offs + u + 1);
+      // first window: ~SK_K of the |P_u| hashes (uniform over [0, b)) expected inside; a multiple
+      // of 512 values, so every lane's quarter of the words is a whole number of uint4
+      const float wf = kb / (float)max(p1 - p0, 1);
+      const uint32_t W0 = wf >= (float)(SK_CAPW * 32 - 512) ? SK_CAPW * 32 : ((uint32_t)wf + 512u) & ~511u;
+      uint32_t mybase = 0;  // window start of function myf
+      int mycnt = 0;        // values of function myf found so far
+      unsigned need = (1u << nf) - 1u;
+      uint32_t Wv = W0;
+      while (need) {
+        uint32_t base[SK_FG];
+#pragma unroll
+        for (int f = 0; f < SK_FG; ++f) base[f] = __shfl_sync(0xffffffffu, mybase, 4 * f);
+        // ---- hash pass: set the bits of the values inside each needing function's window
+        auto hset = [&](int f, uint32_t x) {
+          const uint64_t z = fa[f] * (uint64_t)x + fc[f];
+          const uint32_t v = POW2 ? (uint32_t)(z >> sh) : (uint32_t)__umul64hi(z, (uint64_t)b);
+          const uint32_t d = v - base[f];
+          if (d < Wv) atomicOr(&B[f * SK_CAPW + (d >> 5)], 1u << (d & 31));
+        };
+        const bool all = need == (1u << SK_FG) - 1u;  // (every function of a full group: round 1)
+        int32_t p = p0 + lane;
+        for (; p + 96 < p1; p += 128) {  // four items per lane, no bounds checks
+          uint32_t x[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) x[q] = (uint32_t)__ldg(items + p + 32 * q);
+          if (all) {
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+#pragma unroll
+              for (int f = 0; f < SK_FG; ++f) hset(f, x[q]);
+          } else {
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+#pragma unroll
+              for (int f = 0; f < SK_FG; ++f)
+                if ((need >> f) & 1u) hset(f, x[q]);
+          }
+        }
+        for (; p < p1; p += 32) {
+          const uint32_t x = (uint32_t)__ldg(items + p);
+#pragma unroll
+          for (int f = 0; f < SK_FG; ++f)
+            if ((need >> f) & 1u) hset(f, x);
+        }
+        __syncwarp();
+        // ---- extraction, all functions at once: lane sub of function myf reads its quarter of the
+        //      window's words (uint4), a 4-lane prefix places its set bits, the first D - mycnt
+        //      are kept; the words are cleared as they are read
+        const int nq = (int)(Wv >> 9);  // uint4 per lane
+        const bool act = (need >> myf) & 1u;
+        uint4 *Bq = reinterpret_cast<uint4 *>(B + myf * SK_CAPW) + sub * nq;
+        int pc = 0;
+        if (act)
+          for (int j = 0; j < nq; ++j) {
+            const uint4 q = Bq[j];
+            pc += __popc(q.x) + __popc(q.y) + __popc(q.z) + __popc(q.w);
+          }
+        int incl = pc;
+        {
+          const int y1 = __shfl_up_sync(0xffffffffu, incl, 1, 4);
+          if (sub >= 1) incl += y1;
+          const int y2 = __shfl_up_sync(0xffffffffu, incl, 2, 4);
+          if (sub >= 2) incl += y2;
+        }
+        const int tot = __shfl_sync(0xffffffffu, incl, 3, 4);
+        if (act) {
+          int r = mycnt + incl - pc;
+          const uint32_t vb = mybase + (uint32_t)(sub * nq * 128);
+          for (int j = 0; j < nq && r < D; ++j) {
+            const uint4 q = Bq[j];
+            const uint32_t ws[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              uint32_t word = ws[e];
+              while (word && r < D) {
+                const int bp = __ffs(word) - 1;
+                word &= word - 1;
+                sv[w][myf][r++] = (uint16_t)(vb + (uint32_t)(j * 128 + e * 32 + bp));
+              }
+            }
+          }
+          for (int j = 0; j < nq; ++j) Bq[j] = make_uint4(0u, 0u, 0u, 0u);
+          mycnt = min(D, mycnt + tot);
+          mybase += Wv;
+        }
+        const unsigned done = __ballot_sync(0xffffffffu, sub == 0 && (mycnt >= D || mybase >= b));
+        unsigned dn = 0;
+#pragma unroll
+        for (int f = 0; f < SK_FG; ++f) dn |= ((done >> (4 * f)) & 1u) << f;
+        need &= ~dn;
+        __syncwarp();
+        Wv = SK_CAPW * 32;  // later windows (rare): the full capacity
+      }
+      // ---- out[f][u][0..D): lane 4f writes function f0+f's row (ABSENT past the values found)
+      if (sub == 0 && myf < nf) {
+        const uint4 q = *reinterpret_cast<const uint4 *>(sv[w][myf]);
+        uint32_t s[C2_SKETCH_D] = {q.x & 0xFFFFu, q.x >> 16, q.y & 0xFFFFu, q.y >> 16,
+                                   q.z & 0xFFFFu, q.z >> 16, q.w & 0xFFFFu, q.w >> 16};
+#pragma unroll
+        for (int j = 0; j < C2_SKETCH_D; ++j) s[j] = j < mycnt ? s[j] : C2_ABSENT16;
+        uint16_t *o = out + ((int64_t)(f0 + myf) * n + u) * D;
+        if (D == C2_SKETCH_D) {
+          *reinterpret_cast<uint4 *>(o) = make_uint4(s[0] | (s[1] << 16), s[2] | (s[3] << 16), s[4] | (s[5] << 16),
+                                                     s[6] | (s[7] << 16));
+        } else {
+#pragma unroll
+          for (int j = 0; j < C2_SKETCH_D; ++j)
+            if (j < D) o[j] = (uint16_t)s[j];
+        }
+      }
+      __syncwarp();
+    }
+  }
+}
+
 template <int G>
 static int launch_sketch(c2_ctx *ctx, const Csr &csr, int t, int f0, int b, const HashArgs &ha,
                          const uint16_t *htab, int32_t m, int D, uint16_t *out) {
@@ -97,6 +256,18 @@ int sketch(c2_ctx *ctx, const Csr &csr, int t, int b, const HashParams *hp, cons
   for (int f = 0; f < t; ++f) {
     ha.a[f] = hp ? hp->a[f] : 0;
     ha.c[f] = hp ? hp->c[f] : 0;
+  }
+  if (!htab && csr.n > 0) {
+    // persistent grid: every block resident (users are taken in a grid-stride loop)
+    const bool pow2 = b >= 2 && (b & (b - 1)) == 0;
+    auto kern = pow2 ? k_sketch_w<true> : k_sketch_w<false>;
+    static int occ[2] = {0, 0};
+    if (!occ[pow2]) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ[pow2], kern, SK_WARPS * 32, 0);
+    const unsigned grid = (unsigned)std::min<int64_t>((int64_t)ctx->num_sms * std::max(occ[pow2], 1),
+                                                      ((int64_t)csr.n + SK_WARPS - 1) / SK_WARPS);
+    kern<<<grid, SK_WARPS * 32, 0, ctx->stream>>>(csr.offs, csr.items, csr.n, t, (uint32_t)b, ha, D, out);
+    C2_LAUNCHED(ctx, "k_sketch_w");
+    return C2_OK;
   }
   for (int f0 = 0; f0 < t; f0 += 8) {
     int rem = t - f0;

@@ -80,6 +80,20 @@ def test_sketch_random(ctx, seed):
     assert np.array_equal(g3, o[:, :, :3])
 
 
+@pytest.mark.parametrize("t,b,lo,hi", [(13, 4096, 1, 12), (17, 32768, 1, 40), (9, 1000, 100, 3000), (8, 2, 1, 50),
+                                        (3, 64, 2000, 5000)])
+def test_sketch_windows(ctx, t, b, lo, hi):
+    """k_sketch_w edge cases: several function groups (t > 8), short lists at large b (the value
+    window slides up several times), long lists (many item chunks per lane), tiny b."""
+    rng = np.random.default_rng(t * 100 + b)
+    n, m = 300, 20000
+    offs, items = synth.random_instance(rng, n, m, lo, hi, zipf=0.8)
+    o = oracle.sketch(offs, items, oracle.hash_table(77, t, b, mval(items)), 8)
+    for D in (8, 5):
+        g = npy(c2.sketch(dev(offs), dev(items), t, b, 77, D, ctx=ctx))
+        assert np.array_equal(g, o[:, :, :D])
+
+
 @pytest.mark.parametrize("cfg", ["c1", "c2", "c3", "c4"])
 def test_sketch_configs(ctx, cfg):
     C = synth.config(cfg)
