@@ -30,9 +30,11 @@
 #include <vector>
 
 #include "c2_internal.cuh"
+#include "cand.cuh"
+#include "k_rows.cuh"
 
-#ifndef C2_EPI
-#define C2_EPI 0  // 1: light rows filtered in the phase-A epilogue (measured slower)
+#ifndef C2_LIGHT
+#define C2_LIGHT 1  // 1: light rows (full running list) filtered in the phase-A epilogue, merged by k_surv_merge
 #endif
 #ifndef C2_SNAKE
 #define C2_SNAKE 1  // 1: warp w probes slices w, 2W-1-w, 2W+w, ... (slices are longest-first: balances warps)
@@ -600,247 +602,6 @@ __global__ void __launch_bounds__(RL_T) k_relabel(BigC *__restrict__ bcs, int64_
   }
 }
 
-// ------------------------------------------------------------------ candidate lists
-// A candidate (v, i, U) is held as {iu = i | U << 16, id}.  The order (A13): a before b iff
-// a.i * b.U > b.i * a.U, ties by lower id.  SENT is worse than every real candidate.
-struct Cand {
-  uint32_t iu;
-  int32_t id;
-};
-__device__ __forceinline__ Cand sent() { return Cand{1u << 16, INT32_MAX}; }
-__device__ __forceinline__ bool is_real(Cand a) { return a.id != INT32_MAX; }
-__device__ __forceinline__ bool better_c(Cand a, Cand b) {
-  uint32_t l = (a.iu & 0xFFFFu) * (b.iu >> 16), r = (b.iu & 0xFFFFu) * (a.iu >> 16);
-  return l > r || (l == r && a.id < b.id);
-}
-__device__ __forceinline__ Cand shfl_c(Cand a, int src) {
-  return Cand{__shfl_sync(0xffffffffu, a.iu, src), __shfl_sync(0xffffffffu, a.id, src)};
-}
-__device__ __forceinline__ Cand shfl_xor_c(Cand a, int m) {
-  return Cand{__shfl_xor_sync(0xffffffffu, a.iu, m), __shfl_xor_sync(0xffffffffu, a.id, m)};
-}
-__device__ __forceinline__ Cand shfl_up_c(Cand a) {
-  return Cand{__shfl_up_sync(0xffffffffu, a.iu, 1), __shfl_up_sync(0xffffffffu, a.id, 1)};
-}
-__device__ __forceinline__ c2_cand to_out(Cand a) {
-  return is_real(a) ? c2_cand{a.id, (uint16_t)(a.iu & 0xFFFFu), (uint16_t)(a.iu >> 16)} : c2_cand{-1, 0, 0};
-}
-__device__ __forceinline__ Cand from_out(c2_cand e) {
-  return e.id >= 0 ? Cand{(uint32_t)e.inter | ((uint32_t)e.uni << 16), e.id} : sent();
-}
-
-// Sort key of a candidate: K = q32 << 32 | (2^32 - 1 - id), larger = better, where
-// q32 = floor(i/U * 2^32) (U >= 1; 2^32 - 1 for i == U) from the IEEE (correctly rounded) f64
-// quotient.  K orders candidates exactly as the fraction comparison (A13): equal fractions
-// give identical quotients; distinct fractions with U <= 65534 differ by >= 1/65534^2, i.e. by
-// >= 1.00006 after scaling by 2^32, far above the f64 rounding error (< 2^-20), so their
-// floors differ.  The payload iu = i | U << 16 rides along.  Sentinel: K = 0.
-struct KC {
-  uint64_t k;
-  uint32_t iu;
-};
-__device__ __forceinline__ KC to_kc(Cand c) {
-  if (!is_real(c)) return KC{0ull, 1u << 16};
-  const uint32_t i = c.iu & 0xFFFFu, U = c.iu >> 16;
-  const double q = (double)i / (double)U;
-  const uint32_t q32 = i >= U ? 0xFFFFFFFFu : (uint32_t)(q * 4294967296.0);
-  return KC{((uint64_t)q32 << 32) | (uint64_t)(0xFFFFFFFFu - (uint32_t)c.id), c.iu};
-}
-__device__ __forceinline__ int32_t kc_id(KC a) { return (int32_t)(0xFFFFFFFFu - (uint32_t)a.k); }
-__device__ __forceinline__ bool kc_real(KC a) { return a.k != 0ull; }
-__device__ __forceinline__ Cand kc_cand(KC a) { return kc_real(a) ? Cand{a.iu, kc_id(a)} : sent(); }
-__device__ __forceinline__ c2_cand kc_out(KC a) {
-  return kc_real(a) ? c2_cand{kc_id(a), (uint16_t)(a.iu & 0xFFFFu), (uint16_t)(a.iu >> 16)} : c2_cand{-1, 0, 0};
-}
-__device__ __forceinline__ bool better_e(KC a, KC b) { return a.k > b.k; }
-__device__ __forceinline__ bool better_e(Cand a, Cand b) { return better_c(a, b); }
-__device__ __forceinline__ KC shfl_e(KC a, int src) {
-  return KC{__shfl_sync(0xffffffffu, a.k, src), __shfl_sync(0xffffffffu, a.iu, src)};
-}
-__device__ __forceinline__ KC shfl_xor_e(KC a, int m) {
-  return KC{__shfl_xor_sync(0xffffffffu, a.k, m), __shfl_xor_sync(0xffffffffu, a.iu, m)};
-}
-__device__ __forceinline__ KC shfl_up_e(KC a) {
-  return KC{__shfl_up_sync(0xffffffffu, a.k, 1), __shfl_up_sync(0xffffffffu, a.iu, 1)};
-}
-__device__ __forceinline__ Cand shfl_e(Cand a, int src) { return shfl_c(a, src); }
-__device__ __forceinline__ Cand shfl_xor_e(Cand a, int m) { return shfl_xor_c(a, m); }
-__device__ __forceinline__ Cand shfl_up_e(Cand a) { return shfl_up_c(a); }
-
-// Bitonic sort of the 32R warp-held elements a[j] (position 32j + lane), best first.
-template <int R, class E>
-__device__ __forceinline__ void warp_sort(E (&a)[R]) {
-  const int lane = threadIdx.x & 31;
-#pragma unroll
-  for (int size = 2; size <= 32 * R; size <<= 1) {
-#pragma unroll
-    for (int stride = size >> 1; stride > 0; stride >>= 1) {
-      if (stride >= 32) {
-        const int js = stride >> 5;
-#pragma unroll
-        for (int j = 0; j < R; ++j) {
-          if ((j & js) == 0) {
-            const int p = 32 * j + lane;
-            const bool desc = (p & size) == 0;  // lower position takes the better element
-            E x = a[j], y = a[j + js];
-            if (desc ? better_e(y, x) : better_e(x, y)) {
-              a[j] = y;
-              a[j + js] = x;
-            }
-          }
-        }
-      } else {
-#pragma unroll
-        for (int j = 0; j < R; ++j) {
-          const int p = 32 * j + lane;
-          E o = shfl_xor_e(a[j], stride);
-          const bool lower = (lane & stride) == 0;
-          const bool desc = (p & size) == 0;
-          // lower position of a descending block keeps the better one
-          if ((lower == desc) ? better_e(o, a[j]) : better_e(a[j], o)) a[j] = o;
-        }
-      }
-    }
-  }
-}
-
-// Bitonic merge of a bitonic sequence of 32R warp-held elements into best-first order.
-template <int R, class E>
-__device__ __forceinline__ void warp_bitonic_merge(E (&a)[R]) {
-  const int lane = threadIdx.x & 31;
-#pragma unroll
-  for (int stride = 16 * R; stride > 0; stride >>= 1) {
-    if (stride >= 32) {
-      const int js = stride >> 5;
-#pragma unroll
-      for (int j = 0; j < R; ++j)
-        if ((j & js) == 0 && better_e(a[j + js], a[j])) {
-          E x = a[j];
-          a[j] = a[j + js];
-          a[j + js] = x;
-        }
-    } else {
-#pragma unroll
-      for (int j = 0; j < R; ++j) {
-        E o = shfl_xor_e(a[j], stride);
-        const bool lower = (lane & stride) == 0;
-        if (lower ? better_e(o, a[j]) : better_e(a[j], o)) a[j] = o;
-      }
-    }
-  }
-}
-
-// Insert x into the sorted warp list a (32R positions, best first); the worst drops out.
-template <int R, class E>
-__device__ __forceinline__ void warp_insert(E (&a)[R], E x) {
-  const int lane = threadIdx.x & 31;
-  int pos = 0;
-#pragma unroll
-  for (int j = 0; j < R; ++j) pos += __popc(__ballot_sync(0xffffffffu, better_e(a[j], x)));
-  E up[R];
-#pragma unroll
-  for (int j = 0; j < R; ++j) up[j] = shfl_up_e(a[j]);
-#pragma unroll
-  for (int j = 1; j < R; ++j) {
-    E last = shfl_e(a[j - 1], 31);
-    if (lane == 0) up[j] = last;
-  }
-#pragma unroll
-  for (int j = 0; j < R; ++j) {
-    const int p = 32 * j + lane;
-    if (p == pos) a[j] = x;
-    else if (p > pos) a[j] = up[j];
-  }
-}
-
-template <int R, class E>
-__device__ __forceinline__ E warp_get(const E (&a)[R], int p) {
-  E r = a[0];
-#pragma unroll
-  for (int j = 1; j < R; ++j)
-    if ((p >> 5) == j) r = a[j];
-  return shfl_e(r, p & 31);
-}
-
-// Out-of-line copies of the K8 sorting networks: one body per size instead of one per call site
-// (the fully unrolled networks otherwise dominate the kernel's code and its i-cache misses).
-template <int R>
-struct KCA {
-  KC e[R];
-};
-template <int R>
-__device__ __noinline__ KCA<R> sort_kc_ni(KCA<R> a) {
-  warp_sort<R>(a.e);
-  return a;
-}
-template <int R>
-__device__ __noinline__ KCA<R> merge_kc_ni(KCA<R> a) {
-  warp_bitonic_merge<R>(a.e);
-  return a;
-}
-template <int R>
-__device__ __forceinline__ void sort_kc(KC (&x)[R]) {
-  KCA<R> t;
-#pragma unroll
-  for (int j = 0; j < R; ++j) t.e[j] = x[j];
-  t = sort_kc_ni<R>(t);
-#pragma unroll
-  for (int j = 0; j < R; ++j) x[j] = t.e[j];
-}
-template <int R>
-__device__ __forceinline__ void merge_kc(KC (&x)[R]) {
-  KCA<R> t;
-#pragma unroll
-  for (int j = 0; j < R; ++j) t.e[j] = x[j];
-  t = merge_kc_ni<R>(t);
-#pragma unroll
-  for (int j = 0; j < R; ++j) x[j] = t.e[j];
-}
-
-// One Alg. 3 step for one row, by ranks: the m <= 32 queued survivors Q (distinct ids, unsorted)
-// and the running list S (best first; its real entries are a prefix, pads have id -1) give
-// dst[0..kk) = the first kk distinct ids of S ∪ Q under the order (A13, A16).  A survivor whose id
-// is already in S carries identical (i, U) and is dropped.  Every element's output position is
-// (its rank in S) + (its rank among the kept survivors): O((|S| + m) * m / 32) exact cross-multiplied
-// comparisons per lane, all independent (no sorting network, no 64-bit keys).
-template <int KS>
-__device__ __forceinline__ void rank_merge(const Cand *qr, int m, const c2_cand *S, int kk, c2_cand *dst) {
-  const int lane = threadIdx.x & 31;
-  Cand sv[KS];
-  int nS = 0;
-#pragma unroll
-  for (int j = 0; j < KS; ++j) {
-    sv[j] = (32 * j + lane < kk) ? from_out(S[32 * j + lane]) : sent();
-    nS += __popc(__ballot_sync(0xffffffffu, is_real(sv[j])));
-  }
-  const Cand q = lane < m ? qr[lane] : sent();
-  int rs = 0;
-  bool dup = false;
-  for (int i = 0; i < nS; ++i) {  // rank of q in S (broadcast reads)
-    const Cand si = from_out(S[i]);
-    dup |= si.id == q.id;
-    rs += better_c(si, q) ? 1 : 0;
-  }
-  const unsigned dm = __ballot_sync(0xffffffffu, lane < m && dup);
-  int rq = 0, sh[KS];
-#pragma unroll
-  for (int j = 0; j < KS; ++j) sh[j] = 0;
-  for (int j = 0; j < m; ++j) {
-    const Cand o = shfl_c(q, j);
-    if ((dm >> j) & 1u) continue;  // (uniform)
-    rq += better_c(o, q) ? 1 : 0;
-#pragma unroll
-    for (int jj = 0; jj < KS; ++jj) sh[jj] += better_c(o, sv[jj]) ? 1 : 0;
-  }
-  if (lane < m && !dup && rs + rq < kk) dst[rs + rq] = to_out(q);
-#pragma unroll
-  for (int jj = 0; jj < KS; ++jj) {
-    const int i = 32 * jj + lane;
-    if (i < nS && i + sh[jj] < kk) dst[i + sh[jj]] = to_out(sv[jj]);
-  }
-  for (int p = nS + m - __popc(dm) + lane; p < kk; p += 32) dst[p] = c2_cand{-1, 0, 0};
-}
-
 // ------------------------------------------------------------------ K7 tile kernel
 __device__ __forceinline__ void csa(uint32_t &h, uint32_t &l, uint32_t a, uint32_t b, uint32_t c) {
   uint32_t u = a ^ b;
@@ -888,26 +649,6 @@ __device__ __forceinline__ void transpose32(uint32_t (&A)[32]) {
 #endif
 }
 
-// Shared-memory layout of the K8 phase (32-bit words), aliased onto the M region once phase A
-// is done (M is dead then).  Depends on the tile's cluster size s:
-//   cnt  [32 rows][RS] u16   |P_r ∩ P_v| by (row, member position); RS = 64*ceil(s/64)+4, so a
-//                            warp reading 4 consecutive counts per row (LDS.64, lane = row) is
-//                            bank-conflict free
-//   vid  [s4] int32          member ids (positions >= s: INT32_MAX)
-//   vps  [s4] uint32         member |P_v| (positions >= s: 0)
-//   que  [32][qcap] Cand     survivors per row (qcap >= 64*KS, as large as shared memory allows)
-struct K8Lay {
-  int RS, vid, vps, que, words;
-  __host__ __device__ __forceinline__ K8Lay(int s, int qcap) {
-    RS = ((s + 63) / 64) * 64 + 4;
-    const int s4 = (s + 3) & ~3;
-    vid = 16 * RS;
-    vps = vid + s4;
-    que = vps + s4;
-    words = que + 32 * qcap * 2;
-  }
-};
-
 struct TileArgs {
   const Tile *tiles;
   int64_t lo, hi;
@@ -924,14 +665,20 @@ struct TileArgs {
   int32_t W, nwin;
   int k;
   const c2_cand *seed;  // fused: running lists before this function [n][k]; else nullptr
-  c2_cand *out;         // local: cand [t][n][k]; fused: running lists after this function
   unsigned long long *kstats;  // C2_OPT_KSTATS counters or nullptr
-  uint32_t *gscratch;   // !SMEM_CNT only: per CTA K8Lay(smax, qcap).words words
-  int32_t smax;
-  int32_t qcap;         // survivor queue capacity per row
-  int32_t rl_off;       // fused: word offset of the rows' running lists in shared memory
   int32_t stg_off, stg_cap;  // staging buffer (word offset, capacity in 16-byte groups; 0: off)
   int relabel;          // 1: items are unit-local ids, the tile's window is [0, B.kc) (nwin == 1)
+  c2_cand *surv;        // fused light-row path: survivors [n][qmax] (nullptr: no light rows)
+  int32_t *qn;          // survivors per user (read and zeroed by k_surv_merge)
+  int32_t qmax;
+  // rows handed to k_row_topk: count rows (u16) and records, bump-allocated
+  uint16_t *hv_cnt;
+  int64_t hv_cap;
+  unsigned long long *hv_used;
+  RowRec *hv_recs;
+  int64_t hv_rcap;
+  unsigned long long *hv_nrec;
+  int *err;             // set to 1 if a buffer above was too small (the host sizes them exactly)
 };
 
 // 8 masks of one uint4 of packed u16 item ids
@@ -979,31 +726,11 @@ struct Counter {
   }
 };
 
-// A fixed reference candidate of row r (|P_r| = pr) in the form that makes the order test of a
-// candidate (i, |P_v|, id) two multiply-adds: with U = pr + |P_v| - i and the reference (iT, UT),
-//   i*UT > iT*U  <=>  i*(UT + iT) > iT*|P_v| + iT*pr.
-// Both sides fit in 32 bits (i <= 32767, U <= 65534, A28).  Ties are decided by id < idlim
-// (idlim = idT: strictly better; idT + 1: better or the reference itself).  Unsigned id compare:
-// an id of -1 (empty position of a mixed slice) never passes a tie.
-struct Ref {
-  uint32_t A, B, iT, idlim;
-};
-__device__ __forceinline__ Ref make_ref(Cand t, uint32_t pr, bool or_equal) {
-  const uint32_t i = t.iu & 0xFFFFu, U = t.iu >> 16;
-  return Ref{U + i, i * pr, i, (uint32_t)t.id + (or_equal ? 1u : 0u)};
-}
-__device__ __forceinline__ bool passes(uint32_t i, uint32_t ps, int32_t id, const Ref &R) {
-  const uint32_t l = i * R.A, r = R.iT * ps + R.B;
-  return l > r || (l == r && (uint32_t)id < R.idlim);
-}
-
-template <int NHI, int VPT, int KS, bool SMEM_CNT>
+template <int NHI, int VPT>
 __global__ void __launch_bounds__(TILE_T, C2_TILE_MINB) k_local_tile(TileArgs a) {
-  constexpr int R1 = 2 * KS;
-  const int qcap = a.qcap;
   extern __shared__ __align__(16) uint32_t dyn[];
-  uint32_t *M = dyn;  // phase A: W + 1 words, M[W] == 0
-  // tile descriptors, double-buffered: the next tile's are fetched during this tile's K8
+  uint32_t *M = dyn;  // W + 1 words, M[W] == 0 (all zero between tiles)
+  // tile descriptors, double-buffered: the next tile's are fetched during this tile
   __shared__ int64_t s_it[2];
   __shared__ Tile s_T[2];
   __shared__ BigC s_B[2];
@@ -1012,28 +739,22 @@ __global__ void __launch_bounds__(TILE_T, C2_TILE_MINB) k_local_tile(TileArgs a)
   __shared__ int32_t s_bl[2][MAX_WIN], s_bo[2][MAX_WIN], s_so[2][MAX_WIN];  // rows' blocks; staged offsets
   __shared__ int s_stg[2];  // 1: the rows' blocks of every window are staged in stg
   __shared__ __align__(16) int32_t s_rec[2][REC_W];  // fetched tile records
-  __shared__ int s_row;
-  __shared__ int s_wq[TILE_WARPS];  // per-warp survivor counters of the K8 scan (0 between scans)
   __shared__ uint4 s_ref[32];       // light rows: the running k-th best as a Ref (see make_ref)
-  __shared__ int s_qn[32];          // light rows: survivors queued by the phase-A epilogue
-  __shared__ unsigned s_light;      // rows whose running list is full (fused big-cluster tiles)
+  __shared__ int s_qn[32];          // light rows: survivors found by the phase-A epilogue
+  __shared__ unsigned s_light;      // light rows (running list full, k-th best with i >= 1)
+  __shared__ unsigned s_over;       // light rows with more than qmax survivors (handed to k_row_topk)
+  __shared__ int64_t s_cbase, s_rbase;  // this tile's first count entry / record for k_row_topk
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  if (tid < TILE_WARPS) s_wq[tid] = 0;
   for (int i = tid; i < a.W + 1; i += TILE_T) M[i] = 0;
-  uint32_t *kb = SMEM_CNT ? dyn : a.gscratch + (int64_t)blockIdx.x * K8Lay(a.smax, qcap).words;  // K8 region
-  c2_cand *s_run = reinterpret_cast<c2_cand *>(dyn + a.rl_off);  // fused: the rows' running lists [32][k]
-  uint4 *stg = reinterpret_cast<uint4 *>(dyn + a.stg_off);       // staged rows' blocks of the next tile
+  uint4 *stg = reinterpret_cast<uint4 *>(dyn + a.stg_off);  // staged rows' blocks of the next tile
   const int nwin = a.nwin;
   const int kk = a.k;
-  // one warp fetches the descriptors of tile item `it` into slot b
-#if C2_BULK
-  // next-tile descriptors in two halves: fetch_issue (one thread: claim the tile, bulk-copy its
-  // record) right when K8 starts, fetch_finish (the first warp out of K8 rows: wait for the record,
-  // parse it, bulk-copy the rows' packed blocks into the staging buffer) -- so no warp waits on a
-  // global round trip while others still have rows.  Every use of a slot's mbarriers gets exactly
-  // one arrival (0 bytes when there is no tile), so all threads can track the phases.
+  // next-tile descriptors in two halves (TMA bulk copies completing on mbarriers): fetch_issue
+  // (one thread, at tile start: claim the next tile, bulk-copy its record), fetch_finish (one warp,
+  // once this tile's staged blocks are dead: wait for the record, parse it, bulk-copy the rows'
+  // packed blocks into the staging buffer).  Every use of a slot's mbarriers gets exactly one
+  // arrival (0 bytes when there is no tile), so all threads can track the phases.
   __shared__ __align__(8) uint64_t mb_rec[2], mb_stg[2];
-  __shared__ int s_claim;
   if (tid == 0) {
     for (int i = 0; i < 2; ++i) {
       mbar_init(&mb_rec[i], 1);
@@ -1094,95 +815,43 @@ __global__ void __launch_bounds__(TILE_T, C2_TILE_MINB) k_local_tile(TileArgs a)
   };
   if (tid == 0) fetch_issue(0);
   if (warp == 0) fetch_finish(0);
-#else
-  auto fetch = [&](int b) {
-    int64_t it = 0;
-    if (lane == 0) it = a.lo + atomicAdd(a.counter, 1);
-    it = __shfl_sync(0xffffffffu, it, 0);
-    if (lane == 0) s_it[b] = it;
-    if (it >= a.hi) return;
-    cp_async16(&s_rec[b][lane * 4], a.rec + it * REC_W + lane * 4);
-    cp_async_wait_all();
-    __syncwarp();
-    const int32_t *rc = s_rec[b];
-    if (lane == 0) {
-      s_T[b] = Tile{rc[0], rc[1]};
-      s_B[b] = BigC{rc[2], rc[3], rc[4], rc[5], rc[6], rc[7]};
-    }
-    s_ru2[b][lane] = rc[64 + lane];
-    s_rp2[b][lane] = (uint32_t)rc[96 + lane];
-    // the rows' packed blocks: copied to the staging buffer now (async), used by the build and
-    // the probe of the tile's own slice
-    const int32_t bl = lane < nwin ? rc[8 + lane] : 0;
-    const int32_t bo = lane < nwin ? rc[24 + lane] : 0;
-    int32_t incl = bl * 32;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int32_t y = __shfl_up_sync(0xffffffffu, incl, o);
-      if (lane >= o) incl += y;
-    }
-    const int32_t tot = __shfl_sync(0xffffffffu, incl, 31);
-    const bool staged = tot <= a.stg_cap;
-    if (lane < nwin) {
-      s_bl[b][lane] = bl;
-      s_bo[b][lane] = bo;
-      s_so[b][lane] = incl - bl * 32;
-    }
-    if (lane == 0) s_stg[b] = staged ? 1 : 0;
-    if (staged)
-      for (int w = 0; w < nwin; ++w) {
-        const int32_t n4 = __shfl_sync(0xffffffffu, bl, w) * 32;
-        const int32_t so = __shfl_sync(0xffffffffu, incl - bl * 32, w);
-        const uint4 *g = a.packed + (int64_t)__shfl_sync(0xffffffffu, bo, w) * 32;
-        for (int i = lane; i < n4; i += 32) cp_async16(stg + so + i, g + i);
-      }
-  };
-#endif
-#if !C2_BULK
-  if (warp == 0) fetch(0);
-#endif
+  // light rows (c2_build; the row's running list full and its k-th best tau has i >= 1): a
+  // candidate can only enter the list if it is strictly better than tau.  Right after phase A,
+  // while the bit-sliced counts are still in the threads that made them, every light row's
+  // candidates are screened against a per-slice bound with a bit-sliced compare (all 32 rows at
+  // once, ~2 LOP3 per count bit), the few that pass get the exact test, and the survivors go to
+  // global memory for k_surv_merge.  The other rows' counts go to k_row_topk.
+  const bool light_on = C2_LIGHT && a.surv != nullptr;
   int cur = 0;
   for (;;) {
-#if C2_BULK
     mbar_wait(&mb_stg[cur], (ph_stg >> cur) & 1u);  // this tile's staged row blocks
     ph_rec ^= 1u << cur;  // (slot cur's record and staging phases were consumed)
     ph_stg ^= 1u << cur;
-    if (tid == 0) s_claim = 0;
-#else
-    cp_async_wait_all();
-#endif
     __syncthreads();
     const int64_t it = s_it[cur];
     if (it >= a.hi) break;
-    long long ck0 = a.kstats ? clock64() : 0, ck_r1 = 0, ck_scan = 0, ckb = 0, ckp = 0;
+    if (tid == 0) fetch_issue(cur ^ 1);  // next tile's record: claimed and requested now
+    const long long ck0 = a.kstats ? clock64() : 0;
+    long long ckA = 0, ckE = 0;
     const Tile T = s_T[cur];
     const BigC B = s_B[cur];
     const int32_t *s_ru = s_ru2[cur];
     const uint32_t *s_rp = s_rp2[cur];
     const int s = B.s;
+    const int s4 = (s + 3) & ~3;
     const int nsl = (s + 31) >> 5;
     const int r0 = T.j * 32;
     const int nr = min(32, s - r0);
     const int32_t *vp = a.vperm + B.vp_off;
     const uint32_t W = a.relabel ? (uint32_t)B.kc : (uint32_t)a.W;
-    const K8Lay lay(s, qcap);
-    uint16_t *cnt = reinterpret_cast<uint16_t *>(kb);
-    int32_t *s_vid = reinterpret_cast<int32_t *>(kb + lay.vid);
-    uint32_t *s_vps = kb + lay.vps;
-    Cand *s_q = reinterpret_cast<Cand *>(kb + lay.que);
-    if (tid == 0) s_row = 0;
     if (tid < 32) s_qn[tid] = 0;
-    // light rows: fused mode, big cluster (no slot groups), running list already full.  Their
-    // candidates are filtered against the running k-th best right after the transpose, while
-    // the counts are still in the thread that made them; K8 then skips their scan.
-    const bool epi = C2_EPI && a.seed != nullptr && B.slot == 0;
-    // the rows' running lists (fused mode): loaded now, first used in K8 after phase A
-    if (a.seed)
-      for (int r = warp; r < nr; r += TILE_WARPS) {
-        const int32_t u = s_ru[r];
-        if (u < 0) continue;
-        for (int j = lane; j < kk; j += 32) cp_async8(s_run + r * kk + j, a.seed + (int64_t)u * kk + j);
-      }
+    if (tid == 0) {
+      s_light = 0u;
+      s_over = 0u;
+    }
+    const unsigned valid = __ballot_sync(0xffffffffu, lane < nr && s_ru[lane] >= 0);
+    unsigned k8rows = valid;  // rows handed to k_row_topk
+    const bool lt = light_on && nsl <= VPT * TILE_WARPS;  // (one g0 group: counters of all members live)
     // ================= phase A: counts |P_r ∩ P_v| for the 32 rows x all v of the cluster
     for (int g0 = 0; g0 < nsl; g0 += VPT * TILE_WARPS) {
       Counter<NHI> C[VPT];
@@ -1207,7 +876,6 @@ __global__ void __launch_bounds__(TILE_T, C2_TILE_MINB) k_local_tile(TileArgs a)
             if (xs[q] < W) atomicOr(&M[xs[q]], bit);
         }
         __syncthreads();
-        if (a.kstats) ckb += clock64();
         // ---- probe: each warp streams VPT slices of v lists, two 16-byte loads per step with
         //      the next two steps in flight (odd tails padded with the sentinel item W, M[W] = 0)
         const long long ckpb = a.kstats ? clock64() : 0;
@@ -1242,9 +910,7 @@ __global__ void __launch_bounds__(TILE_T, C2_TILE_MINB) k_local_tile(TileArgs a)
           atomicAdd(&a.kstats[64], (unsigned long long)(clock64() - ckpb));
           atomicAdd(&a.kstats[65], (unsigned long long)nsteps);
         }
-        if (epi && w == nwin - 1) cp_async_wait_all();  // the rows' running lists (issued at tile start)
         __syncthreads();
-        if (a.kstats) ckp += clock64();
         // ---- clear M
         for (int gi = tid; gi < n4r; gi += TILE_T) {
           const uint4 d = gi == tid ? dkeep : srcr[gi];
@@ -1254,11 +920,13 @@ __global__ void __launch_bounds__(TILE_T, C2_TILE_MINB) k_local_tile(TileArgs a)
           for (int q = 0; q < 8; ++q)
             if (xs[q] < W) M[xs[q]] = 0;
         }
-        if (epi && w == nwin - 1 && warp == TILE_WARPS - 1) {
+        if (lt && w == nwin - 1 && warp == TILE_WARPS - 1) {
+          // light rows: the running k-th best tau (one global read per row) as a Ref
           const int r = lane;
-          const bool light = r < nr && s_ru[r] >= 0 && s_run[r * kk + kk - 1].id >= 0;
+          const c2_cand tl = ((valid >> r) & 1u) ? a.seed[(int64_t)s_ru[r] * kk + kk - 1] : c2_cand{-1, 0, 0};
+          const bool light = tl.id >= 0 && tl.inter >= 1;
           if (light) {
-            const Ref R = make_ref(from_out(s_run[r * kk + kk - 1]), s_rp[r], false);
+            const Ref R = make_ref(from_out(tl), s_rp[r], false);
             s_ref[r] = make_uint4(R.A, R.B, R.iT, R.idlim);
           }
           const unsigned lm = __ballot_sync(0xffffffffu, light);
@@ -1266,414 +934,152 @@ __global__ void __launch_bounds__(TILE_T, C2_TILE_MINB) k_local_tile(TileArgs a)
         }
         __syncthreads();
       }
-      // ---- planes -> 32 counts per v (transpose) -> cnt[r][v] (M is dead from here on when
-      //      SMEM_CNT: the host guarantees a single g0 group then)
+      // the staging buffer is dead now: the next tile's row blocks may be copied in
+      if (g0 + VPT * TILE_WARPS >= nsl && warp == TILE_WARPS - 1) fetch_finish(cur ^ 1);
+      if (a.kstats) ckA = clock64();
+      // ---- light rows: bit-sliced prefilter on the counters (count >= imin_r for all 32 rows at
+      //      once), the exact test for the few that pass, survivors to global memory (one g0 group)
+      if (lt) {
+        const unsigned lm = s_light;
+        if (lm) {
+          constexpr int NPL = 4 + NHI;
+          // per row (lane r): the light row's reference tau = (iT, UT) and |P_r|
+          const uint4 Rr = s_ref[lane];  // A = UT + iT, B = iT |P_r|, iT
+          const bool lr = (lm >> lane) & 1u;
 #pragma unroll
-      for (int q = 0; q < VPT; ++q) {
-        const int jj = g0 + q * TILE_WARPS + ((C2_SNAKE && (q & 1)) ? TILE_WARPS - 1 - warp : warp);
-        const int vi = jj * 32 + lane;
-        if (jj < nsl) {
-          uint32_t A[32];
-          A[0] = C[q].ones;
-          A[1] = C[q].twos;
-          A[2] = C[q].fours;
-          A[3] = C[q].eights;
+          for (int q = 0; q < VPT; ++q) {
+            const int jj = g0 + q * TILE_WARPS + ((C2_SNAKE && (q & 1)) ? TILE_WARPS - 1 - warp : warp);
+            if (jj >= nsl) continue;  // (warp-uniform: all lanes of a warp share the slice jj)
+            const int vi = jj * 32 + lane;
+            const int32_t idv = vi < s ? vp[vi] : -1;
+            const uint32_t psv = idv >= 0 ? (uint32_t)a.vsize[B.vp_off + vi] : 0xFFFFFFFFu;
+            // slice bound: every member has |P_v| >= psmin, so a member passes row r only if
+            // i (UT + iT) >= iT (|P_r| + psmin), i.e. i >= imin_r; the bit-planes of the 32 imin_r
+            const uint32_t psmin = __reduce_min_sync(0xffffffffu, psv);
+            uint32_t imin = 0xFFFFFFFFu;
+            if (lr && psmin != 0xFFFFFFFFu) imin = (Rr.y + Rr.z * psmin + Rr.x - 1u) / Rr.x;
+            const unsigned pm = __ballot_sync(0xffffffffu, imin < (1u << NPL));
+            if (!pm) continue;
+            uint32_t pl[NPL], gt = 0u, eq = 0xFFFFFFFFu;
+            pl[0] = C[q].ones;
+            pl[1] = C[q].twos;
+            pl[2] = C[q].fours;
+            pl[3] = C[q].eights;
 #pragma unroll
-          for (int i = 0; i < NHI; ++i) A[4 + i] = C[q].H[i];
+            for (int i = 0; i < NHI; ++i) pl[4 + i] = C[q].H[i];
 #pragma unroll
-          for (int i = 4 + NHI; i < 32; ++i) A[i] = 0;
-          transpose32(A);
+            for (int j = NPL - 1; j >= 0; --j) {
+              const uint32_t im = __ballot_sync(0xffffffffu, (imin >> j) & 1u);
+              gt |= eq & pl[j] & ~im;
+              eq &= ~(pl[j] ^ im);
+            }
+            uint32_t hit = (gt | eq) & pm;
+            if (B.slot) {
+              const int lo = lane & ~(B.slot - 1);
+              hit &= (B.slot >= 32 ? 0xFFFFFFFFu : ((1u << B.slot) - 1u)) << lo;
+            }
+            if (jj == T.j) hit &= ~(1u << lane);  // the row itself
+            if (idv < 0) hit = 0u;
+            while (hit) {
+              const int r = __ffs(hit) - 1;
+              hit &= hit - 1u;
+              uint32_t i = 0u;
 #pragma unroll
-          for (int r = 0; r < 32; ++r)
-            if (r < nr) cnt[r * lay.RS + vi] = (uint16_t)A[r];
-          if (epi) {
-            // light rows: candidate (v, i, |P_v|) survives iff strictly better than the row's
-            // running k-th best (passes() with idlim = id_T), i.e. it would enter the list
-            const unsigned lm = s_light;
-            if (lm && vi < s) {
-              const int32_t idv = vp[vi];
-              const uint32_t psv = (uint32_t)a.vsize[B.vp_off + vi];
-              for (unsigned q2 = lm; q2; q2 &= q2 - 1) {
-                const int r = __ffs(q2) - 1;
-                const uint32_t i = cnt[r * lay.RS + vi];
-                const uint4 R = s_ref[r];
-                const uint32_t l = i * R.x, rr = R.z * psv + R.y;
-                if (l >= rr && (l > rr || (uint32_t)idv < R.w) && vi != r0 + r) {
-                  const int p = atomicAdd(&s_qn[r], 1);
-                  if (p < qcap) s_q[r * qcap + p] = Cand{i | ((s_rp[r] + psv - i) << 16), idv};
-                }
+              for (int j = 0; j < NPL; ++j) i |= ((pl[j] >> r) & 1u) << j;
+              const uint4 R4 = s_ref[r];
+              if (passes(i, psv, idv, Ref{R4.x, R4.y, R4.z, R4.w})) {
+                const int pq = atomicAdd(&s_qn[r], 1);
+                if (pq < a.qmax)
+                  a.surv[(int64_t)s_ru[r] * a.qmax + pq] = c2_cand{idv, (uint16_t)i, (uint16_t)(s_rp[r] + psv - i)};
+                else if (pq == a.qmax)
+                  atomicOr(&s_over, 1u << r);
+              }
+            }
+          }
+        }
+        __syncthreads();  // s_qn, s_over complete
+        k8rows = valid & ~(s_light & ~s_over);
+      }
+      if (a.kstats) ckE = clock64();
+      // ---- the other rows: planes -> 32 counts per member (transpose) -> their count rows, and
+      //      one RowRec per row, for k_row_topk
+      if (k8rows) {
+        if (g0 == 0) {
+          const int n8 = __popc(k8rows);
+          if (tid == 0) {
+            const unsigned long long cb = atomicAdd(a.hv_used, (unsigned long long)n8 * s4);
+            const unsigned long long rb = atomicAdd(a.hv_nrec, (unsigned long long)n8);
+            const bool fits = cb + (unsigned long long)n8 * s4 <= (unsigned long long)a.hv_cap &&
+                              rb + (unsigned long long)n8 <= (unsigned long long)a.hv_rcap;
+            if (!fits) atomicExch(a.err, 1);
+            s_cbase = fits ? (int64_t)cb : -1;
+            s_rbase = (int64_t)rb;
+          }
+          __syncthreads();
+          if (warp == 0 && ((k8rows >> lane) & 1u) && s_cbase >= 0) {
+            const int rk = __popc(k8rows & ((1u << lane) - 1u));
+            const int slot = B.slot;
+            a.hv_recs[s_rbase + rk] = RowRec{s_ru[lane], (int32_t)s_rp[lane], s, B.vp_off, slot ? lane : r0 + lane,
+                                             slot ? (lane & ~(slot - 1)) : 0, slot, B.f, s_cbase + (int64_t)rk * s4};
+          }
+        }
+        const int64_t cb = s_cbase;
+        if (cb >= 0) {
+#pragma unroll
+          for (int q = 0; q < VPT; ++q) {
+            const int jj = g0 + q * TILE_WARPS + ((C2_SNAKE && (q & 1)) ? TILE_WARPS - 1 - warp : warp);
+            const int vi = jj * 32 + lane;
+            if (jj < nsl) {
+              uint32_t A[32];
+              A[0] = C[q].ones;
+              A[1] = C[q].twos;
+              A[2] = C[q].fours;
+              A[3] = C[q].eights;
+#pragma unroll
+              for (int i = 0; i < NHI; ++i) A[4 + i] = C[q].H[i];
+#pragma unroll
+              for (int i = 4 + NHI; i < 32; ++i) A[i] = 0;
+              transpose32(A);
+              if (vi < s) {
+                uint16_t *dst = a.hv_cnt + cb + vi;
+                int rk = 0;
+#pragma unroll
+                for (int r = 0; r < 32; ++r)
+                  if ((k8rows >> r) & 1u) dst[(int64_t)(rk++) * s4] = (uint16_t)A[r];
               }
             }
           }
         }
       }
     }
-    const long long ck1 = a.kstats ? clock64() : 0;
-    // member ids and sizes (positions s .. s4-1: never-passing pads)
-    {
-      const int s4 = (s + 3) & ~3;
-      for (int i = tid; i < s4; i += TILE_T) {
-        s_vid[i] = i < s ? vp[i] : INT32_MAX;
-        s_vps[i] = i < s ? (uint32_t)a.vsize[B.vp_off + i] : 0u;
-      }
-    }
-    cp_async_wait_all();  // the running lists
-    __syncthreads();
-    // ================= K8: exact top-k per row, one warp per row (no CTA barrier inside)
-#if C2_BULK
-    if (tid == 0) fetch_issue(cur ^ 1);  // next tile's record: claimed and requested now
-#else
-    if (warp == 0) fetch(cur ^ 1);  // next tile's descriptors, hidden behind this K8
-#endif
-    const int slot = B.slot;  // mixed slice: candidates only inside the row's own slot group
-    uint32_t *zq = nullptr;  // queue words the warp's previous row wrote (re-zeroed: M alias)
-    int zn = 0;
-    long long tfin = 0, acc_sel = 0, acc_fin = 0, nrow_b = 0;  // kstats: big tiles' per-row split
-    // rows are taken dynamically, the expensive ones first: rows without a full running list
-    // (round 1 in big clusters), then the others
-    const unsigned heavy = __ballot_sync(0xffffffffu, lane < nr && s_ru[lane] >= 0 &&
-                                                          !(a.seed && s_run[lane * kk + kk - 1].id >= 0));
-    const int nheavy = __popc(heavy);
-    for (;;) {
-      if (a.kstats && tfin) {
-        acc_fin += clock64() - tfin;
-        tfin = 0;
-      }
-      for (int i = lane; i < zn; i += 32) zq[i] = 0u;
-      zn = 0;
-      int idx = 0;
-      if (lane == 0) idx = atomicAdd(&s_row, 1);
-      idx = __shfl_sync(0xffffffffu, idx, 0);
-      if (idx >= nr) {
-#if C2_BULK
-        int claim = 0;
-        if (lane == 0) claim = atomicExch(&s_claim, 1);
-        if (__shfl_sync(0xffffffffu, claim, 0) == 0) fetch_finish(cur ^ 1);  // first warp out of rows
-#endif
-        break;
-      }
-      const int r = idx < nheavy ? (int)__fns(heavy, 0, idx + 1) : (int)__fns(~heavy, 0, idx - nheavy + 1);
-      const int32_t u = s_ru[r];
-      if (u < 0) continue;
-      const uint32_t prr = s_rp[r];
-      const int selfr = slot ? r : r0 + r;
-      const uint16_t *cr = cnt + r * lay.RS;
-      Cand *qr = s_q + r * qcap;
-      const Cand tau = a.seed ? from_out(s_run[r * kk + kk - 1]) : sent();
-      // survivors of T (strictly better than tau, not worse than a round-1 bound) -> qr by
-      // ballot compaction; returns their number (only the first qcap are stored)
-      auto scan = [&](const Ref &T) -> int {
-        int m = 0;
-        if (slot) {
-          const int lo = r & ~(slot - 1);
-          const int vi = lo + lane;
-          bool ok = false;
-          Cand x = sent();
-          if (lane < slot && vi != selfr) {
-            const uint32_t i = cr[vi], ps = s_vps[vi];
-            const int32_t id = s_vid[vi];
-            ok = passes(i, ps, id, T);
-            x = Cand{i | ((prr + ps - i) << 16), id};
-          }
-          const unsigned bal = __ballot_sync(0xffffffffu, ok);
-          if (ok) qr[__popc(bal & ((1u << lane) - 1))] = x;
-          return __popc(bal);
-        }
-        for (int base = 0; base < s; base += 128) {
-          const int v4 = base + lane * 4;
-          uint32_t iv[4] = {0, 0, 0, 0}, pv[4] = {0, 0, 0, 0};
-          int32_t dv[4] = {INT32_MAX, INT32_MAX, INT32_MAX, INT32_MAX};
-          if (v4 < s) {
-            const uint2 c = *reinterpret_cast<const uint2 *>(cr + v4);
-            const uint4 ps = *reinterpret_cast<const uint4 *>(s_vps + v4);
-            const int4 id = *reinterpret_cast<const int4 *>(s_vid + v4);
-            iv[0] = c.x & 0xFFFFu, iv[1] = c.x >> 16, iv[2] = c.y & 0xFFFFu, iv[3] = c.y >> 16;
-            pv[0] = ps.x, pv[1] = ps.y, pv[2] = ps.z, pv[3] = ps.w;
-            dv[0] = id.x, dv[1] = id.y, dv[2] = id.z, dv[3] = id.w;
-          }
-#pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            // survivors are few: a shared counter bumped by the passing lanes only (queue order
-            // is irrelevant, the survivors are sorted by the exact key afterwards)
-            if (v4 + e != selfr && passes(iv[e], pv[e], dv[e], T)) {
-              const int p = atomicAdd(&s_wq[warp], 1);
-              if (p < qcap) qr[p] = Cand{iv[e] | ((prr + pv[e] - iv[e]) << 16), dv[e]};
-            }
-          }
-        }
-        __syncwarp();
-        m = s_wq[warp];
-        __syncwarp();
-        if (lane == 0) s_wq[warp] = 0;
-        __syncwarp();
-        return m;
-      };
-      // k-th best of the first 64*KS queue entries (all distinct real candidates): a valid
-      // lower bound of the row's k-th best
-      auto kth_of_queue = [&]() -> Ref {
-        if (a.kstats && lane == 0) atomicAdd(&a.kstats[15], 1ull);
-        KC e[2 * KS];
-#pragma unroll
-        for (int j = 0; j < 2 * KS; ++j) e[j] = to_kc(qr[32 * j + lane]);
-        sort_kc<2 * KS>(e);
-        return make_ref(kc_cand(warp_get<2 * KS>(e, kk - 1)), prr, true);
-      };
-      long long ckr = a.kstats ? clock64() : 0;
-      const long long ckr0 = ckr;
-      // round 1: every lane's best R1 candidates of its share; T_r = the k-th best of the
-      // 32*R1 tops (any k distinct candidates bound the row's k-th best from below)
-      auto round1 = [&](Ref &T) {
-        Cand t[R1];
-#pragma unroll
-        for (int j = 0; j < R1; ++j) t[j] = sent();
-        Ref wr = make_ref(sent(), prr, false);
-        for (int v4 = lane * 4; v4 < s; v4 += 128) {
-          const uint2 c = *reinterpret_cast<const uint2 *>(cr + v4);
-          const uint4 ps = *reinterpret_cast<const uint4 *>(s_vps + v4);
-          const int4 id = *reinterpret_cast<const int4 *>(s_vid + v4);
-          const uint32_t iv[4] = {c.x & 0xFFFFu, c.x >> 16, c.y & 0xFFFFu, c.y >> 16};
-          const uint32_t pv[4] = {ps.x, ps.y, ps.z, ps.w};
-          const int32_t dv[4] = {id.x, id.y, id.z, id.w};
-#pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            if (v4 + e != selfr && passes(iv[e], pv[e], dv[e], wr)) {
-              Cand x{iv[e] | ((prr + pv[e] - iv[e]) << 16), dv[e]};
-#pragma unroll
-              for (int j = R1 - 1; j > 0; --j) {
-                if (better_c(x, t[j - 1])) t[j] = t[j - 1];
-                else if (better_c(x, t[j])) t[j] = x;
-              }
-              if (better_c(x, t[0])) t[0] = x;
-              wr = make_ref(t[R1 - 1], prr, false);
-            }
-          }
-        }
-        KC e[R1];
-#pragma unroll
-        for (int j = 0; j < R1; ++j) e[j] = to_kc(t[j]);
-        sort_kc<R1>(e);
-        const KC Tr = warp_get<R1>(e, kk - 1);
-        if (kc_real(Tr) && better_c(kc_cand(Tr), tau)) T = make_ref(kc_cand(Tr), prr, true);
-      };
-      Ref T = make_ref(tau, prr, false);
-      // rows without a running list yet (tau = sentinel) whose candidates cannot all be queued
-      // start with round 1; rows whose tau lets too many through get it after the first scan
-      bool r1 = !slot && !is_real(tau) && s - 1 > 64 * KS;
-      if (r1) round1(T);
-      if (a.kstats) {
-        const long long c = clock64();
-        ck_r1 += c - ckr;
-        ckr = c;
-      }
-      const bool light = epi && ((s_light >> r) & 1u);
-      int m = light ? s_qn[r] : 0;
-      if (!light || m > qcap) m = scan(T);  // (a light row whose queue overflowed rescans)
-      zq = reinterpret_cast<uint32_t *>(qr);
-      zn = 2 * min(m, qcap);
-      if (a.kstats && lane == 0) atomicAdd(&a.kstats[16 + min(m, 300) / 20], 1ull);
-      if (m > 64 * KS && !slot && !r1) {
-        if (a.kstats && lane == 0) atomicAdd(&a.kstats[14], 1ull);
-        r1 = true;
-        round1(T);
-        m = scan(T);
-        zn = max(zn, 2 * min(m, qcap));
-      }
-      int rescans = 0;
-      for (; rescans < 2 && m > qcap; ++rescans) {
-        T = kth_of_queue();
-        __syncwarp();
-        m = scan(T);
-        zn = max(zn, 2 * min(m, qcap));
-      }
-      // shrink a long queue in place: keep the entries not worse than the k-th best of its
-      // first 64*KS (stops when that makes no progress: massive ties)
-      while (m > 64 * KS && m <= qcap) {
-        const Ref T2 = kth_of_queue();
-        __syncwarp();
-        int w = 0;
-        for (int b0 = 0; b0 < m; b0 += 32) {
-          const int j = b0 + lane;
-          Cand x = j < m ? qr[j] : sent();
-          const uint32_t i = x.iu & 0xFFFFu, ps = (x.iu >> 16) + i - prr;
-          const bool ok = j < m && passes(i, ps, x.id, T2);
-          __syncwarp();
-          const unsigned bal = __ballot_sync(0xffffffffu, ok);
-          if (ok) qr[w + __popc(bal & ((1u << lane) - 1))] = x;
-          w += __popc(bal);
-        }
-        __syncwarp();
-        if (w == m) break;
-        m = w;
-      }
-      if (a.kstats) {
-        const long long c = clock64();
-        ck_scan += c - ckr;
-        if (s > 1024) {
-          acc_sel += c - ckr0;
-          tfin = c;
-          ++nrow_b;
-        }
-      }
-      if (a.kstats) {  // pair evaluations of this row: its cluster-mates (debug work accounting)
-        int ev = s - 1;
-        if (slot) {
-          const int lo = r & ~(slot - 1);
-          ev = __popc(__ballot_sync(0xffffffffu, lane < slot && s_vid[lo + lane] >= 0)) - 1;
-        }
-        if (lane == 0) atomicAdd(&a.kstats[70], (unsigned long long)ev);
-      }
+    // light rows' survivor counts (read and reset by k_surv_merge)
+    if (lt && warp == 0) {
+      const unsigned lok = s_light & ~s_over;
+      if (((lok >> lane) & 1u) && s_qn[lane] > 0) a.qn[s_ru[lane]] = s_qn[lane];
       if (a.kstats && lane == 0) {
-        atomicAdd(&a.kstats[0], 1ull);
-        atomicAdd(&a.kstats[1], m == 0 ? 1ull : 0ull);
-        atomicAdd(&a.kstats[2], (unsigned long long)m);
-        atomicAdd(&a.kstats[3], m > 32 * KS ? 1ull : 0ull);
-        atomicAdd(&a.kstats[4], (unsigned long long)rescans);
-        atomicAdd(&a.kstats[6], r1 ? 1ull : 0ull);
-        if (r == 0) {
-          atomicAdd(&a.kstats[5], 1ull);
-          atomicAdd(&a.kstats[7], (unsigned long long)s);
+        atomicAdd(&a.kstats[71], (unsigned long long)__popc(lok));
+        atomicAdd(&a.kstats[73], (unsigned long long)__popc(s_over));
+      }
+      if (a.kstats && ((lok >> lane) & 1u)) {
+        atomicAdd(&a.kstats[72], (unsigned long long)s_qn[lane]);
+        int ev = s - 1;  // pair evaluations of this row: its cluster-mates (debug work accounting)
+        if (B.slot) {
+          const int lo = lane & ~(B.slot - 1);
+          ev = -1;
+          for (int j = 0; j < B.slot; ++j) ev += vp[lo + j] >= 0 ? 1 : 0;
         }
+        atomicAdd(&a.kstats[70], (unsigned long long)ev);
       }
-      if (a.seed && m == 0) continue;
-      c2_cand *dst = a.seed ? a.out + (int64_t)u * kk : a.out + ((int64_t)B.f * a.n + u) * kk;
-      if (C2_RANKMERGE && a.seed && m <= 32) {
-        // few survivors: Alg. 3 step by ranks (no sorting network, no f64 keys)
-        rank_merge<KS>(qr, m, s_run + r * kk, kk, dst);
-        continue;
-      }
-      if (!C2_RANKMERGE && a.seed && m <= 16) {
-        // few survivors (one insertion ~20 instructions, sort-32 + merge-64 ~320): insert them one
-        // by one into the running list (duplicates skipped)
-        KC S[KS];
-#pragma unroll
-        for (int j = 0; j < KS; ++j) S[j] = to_kc((32 * j + lane < kk) ? from_out(s_run[r * kk + 32 * j + lane]) : sent());
-        const KC xk = to_kc(lane < m ? qr[lane] : sent());  // all survivors' keys at once
-        for (int j = 0; j < m; ++j) {
-          const KC x = shfl_e(xk, j);
-          bool dup = false;
-#pragma unroll
-          for (int jj = 0; jj < KS; ++jj) dup |= S[jj].k == x.k;
-          if (__any_sync(0xffffffffu, dup)) continue;
-          warp_insert<KS>(S, x);
-        }
-#pragma unroll
-        for (int j = 0; j < KS; ++j)
-          if (32 * j + lane < kk) dst[32 * j + lane] = kc_out(S[j]);
-        continue;
-      }
-      KC L[KS];  // top-k of this function's survivors (sentinel padded)
-      if (m <= 32 * KS) {
-        KC q[KS];
-#pragma unroll
-        for (int j = 0; j < KS; ++j) q[j] = to_kc((32 * j + lane < m) ? qr[32 * j + lane] : sent());
-        sort_kc<KS>(q);
-#pragma unroll
-        for (int j = 0; j < KS; ++j) L[j] = q[j];
-      } else if (m <= 64 * KS) {
-        KC q[2 * KS];
-#pragma unroll
-        for (int j = 0; j < 2 * KS; ++j) q[j] = to_kc((32 * j + lane < m) ? qr[32 * j + lane] : sent());
-        sort_kc<2 * KS>(q);
-#pragma unroll
-        for (int j = 0; j < KS; ++j) L[j] = q[j];
-      } else {
-        // pathological ties: exact insertion over the row's candidates
-        if (a.kstats && lane == 0) atomicAdd(&a.kstats[8], 1ull);
-        Cand Lc[KS];
-#pragma unroll
-        for (int j = 0; j < KS; ++j) Lc[j] = sent();
-        Cand thr = sent();
-        for (int vb = 0; vb < s; vb += 32) {
-          const int vi = vb + lane;
-          Cand c = sent();
-          if (vi < s) {
-            int32_t v = s_vid[vi];
-            if (v >= 0 && vi != selfr && (slot == 0 || (vi ^ r) < slot)) {
-              uint32_t ci = cr[vi];
-              c = Cand{ci | ((prr + s_vps[vi] - ci) << 16), v};
-            }
-          }
-          bool bt = is_real(c) && better_c(c, tau) && better_c(c, thr);
-          unsigned mask = __ballot_sync(0xffffffffu, bt);
-          while (mask) {
-            int l = __ffs(mask) - 1;
-            mask &= mask - 1;
-            Cand x = shfl_c(c, l);
-            if (!better_c(x, thr)) continue;
-            warp_insert<KS>(Lc, x);
-            thr = warp_get<KS>(Lc, kk - 1);
-          }
-        }
-#pragma unroll
-        for (int j = 0; j < KS; ++j) L[j] = to_kc(Lc[j]);
-      }
-      if (!a.seed) {
-#pragma unroll
-        for (int j = 0; j < KS; ++j)
-          if (32 * j + lane < kk) dst[32 * j + lane] = kc_out(L[j]);
-        continue;
-      }
-      // merge with the running list S (best first): bitonic sequence L(first k) ++ reverse(S)
-      KC S[KS];
-#pragma unroll
-      for (int j = 0; j < KS; ++j) S[j] = to_kc((32 * j + lane < kk) ? from_out(s_run[r * kk + 32 * j + lane]) : sent());
-      KC mm[2 * KS];
-#pragma unroll
-      for (int j = 0; j < KS; ++j) mm[j] = (32 * j + lane < kk) ? L[j] : KC{0ull, 1u << 16};
-#pragma unroll
-      for (int j = 0; j < KS; ++j) mm[KS + j] = shfl_e(S[KS - 1 - j], 31 - lane);
-      merge_kc<2 * KS>(mm);
-      // drop adjacent duplicates (a repeated id carries identical values, A16); keep k
-      int base = 0;
-#pragma unroll
-      for (int j = 0; j < 2 * KS; ++j) {
-        const uint32_t lo = (uint32_t)mm[j].k;
-        uint32_t prev = __shfl_up_sync(0xffffffffu, lo, 1);
-        uint32_t prevj = j > 0 ? __shfl_sync(0xffffffffu, (uint32_t)mm[j - 1].k, 31) : 0u;
-        if (lane == 0) prev = prevj;
-        bool keep = kc_real(mm[j]) && (j + lane == 0 || lo != prev);
-        unsigned bal = __ballot_sync(0xffffffffu, keep);
-        int rank = base + __popc(bal & ((1u << lane) - 1));
-        if (keep && rank < kk) dst[rank] = kc_out(mm[j]);
-        base += __popc(bal);
-      }
-      for (int p = base + lane; p < kk; p += 32) dst[p] = c2_cand{-1, 0, 0};
     }
-    const long long ck2 = a.kstats ? clock64() : 0;
-    __syncthreads();
-    if (a.kstats && lane == 0) {
+    if (a.kstats && tid == 0) {  // tile cycles by cluster size class: mixed, 33-256, 257-1024, >1024
       const long long ck3 = clock64();
-      atomicAdd(&a.kstats[9], (unsigned long long)(ck1 - ck0));    // phase A (+ tile head)
-      atomicAdd(&a.kstats[10], (unsigned long long)ck_r1);         // K8 round 1
-      atomicAdd(&a.kstats[11], (unsigned long long)ck_scan);       // K8 scan + queue shrink
-      atomicAdd(&a.kstats[12], (unsigned long long)(ck2 - ck1 - ck_r1 - ck_scan));  // K8 rest
-      atomicAdd(&a.kstats[13], (unsigned long long)(ck3 - ck2));   // wait at the K8 barrier
-      if (warp == 0) {  // tile wall cycles by cluster size class: mixed, 33-256, 257-1024, >1024
-        const int cls = B.slot ? 0 : s <= 256 ? 1 : s <= 1024 ? 2 : 3;
-        atomicAdd(&a.kstats[32 + cls], (unsigned long long)(ck3 - ck0));
-        atomicAdd(&a.kstats[36 + cls], 1ull);
-        if (nrow_b) {
-          atomicAdd(&a.kstats[60], (unsigned long long)acc_sel);
-          atomicAdd(&a.kstats[61], (unsigned long long)acc_fin);
-          atomicAdd(&a.kstats[62], (unsigned long long)nrow_b);
-        }
-        {  // per class: build (window sum) / probe / rest of phase A / K8 / wait
-          unsigned long long *kc5 = a.kstats + 40 + 5 * cls;
-          atomicAdd(&kc5[0], (unsigned long long)(ckb - ck0 * nwin));
-          atomicAdd(&kc5[1], (unsigned long long)(ckp - ckb));
-          atomicAdd(&kc5[2], (unsigned long long)(ck1 - ck0) - (unsigned long long)(ckp - ckb));
-          atomicAdd(&kc5[3], (unsigned long long)(ck2 - ck1));
-          atomicAdd(&kc5[4], (unsigned long long)(ck3 - ck2));
-        }
-      }
-    }
-    // restore the all-zero M words the K8 region overwrote
-    // (queues were re-zeroed row by row; here the counts and member arrays)
-    if (SMEM_CNT) {
-      const int dw = min(lay.que, a.W + 1);
-      uint4 *z = reinterpret_cast<uint4 *>(dyn);
-      for (int i = tid; i < dw / 4; i += TILE_T) z[i] = make_uint4(0, 0, 0, 0);
-      for (int i = (dw & ~3) + tid; i < dw; i += TILE_T) dyn[i] = 0;
+      const int cls = B.slot ? 0 : s <= 256 ? 1 : s <= 1024 ? 2 : 3;
+      atomicAdd(&a.kstats[32 + cls], (unsigned long long)(ck3 - ck0));
+      atomicAdd(&a.kstats[36 + cls], 1ull);
+      unsigned long long *kc3 = a.kstats + 40 + 3 * cls;  // phase A / light epilogue / count rows
+      atomicAdd(&kc3[0], (unsigned long long)(ckA - ck0));
+      atomicAdd(&kc3[1], (unsigned long long)(ckE - ckA));
+      atomicAdd(&kc3[2], (unsigned long long)(ck3 - ckE));
     }
     cur ^= 1;
   }
@@ -1681,20 +1087,23 @@ __global__ void __launch_bounds__(TILE_T, C2_TILE_MINB) k_local_tile(TileArgs a)
 
 typedef void (*TileKernel)(TileArgs);
 
-template <int NHI, int VPT, bool SM>
-static TileKernel pick_ks(int k) {
-  return k <= 32 ? k_local_tile<NHI, VPT, 1, SM> : k_local_tile<NHI, VPT, 2, SM>;
+template <int NHI>
+static TileKernel pick_vpt(int vpt) {
+  return vpt <= 1 ? k_local_tile<NHI, 1> : vpt <= 2 ? k_local_tile<NHI, 2> : k_local_tile<NHI, 4>;
 }
-template <int NHI, bool SM>
-static TileKernel pick_vpt(int vpt, int k) {
-  return vpt <= 1 ? pick_ks<NHI, 1, SM>(k) : vpt <= 2 ? pick_ks<NHI, 2, SM>(k) : pick_ks<NHI, 4, SM>(k);
+static TileKernel pick_tile(int nhi, int vpt) {
+  return nhi <= 4 ? pick_vpt<4>(vpt) : nhi <= 8 ? pick_vpt<8>(vpt) : pick_vpt<11>(vpt);
 }
-template <bool SM>
-static TileKernel pick_nhi(int nhi, int vpt, int k) {
-  return nhi <= 4 ? pick_vpt<4, SM>(vpt, k) : nhi <= 8 ? pick_vpt<8, SM>(vpt, k) : pick_vpt<11, SM>(vpt, k);
-}
-static TileKernel pick_tile(int nhi, int vpt, int k, bool smem_cnt) {
-  return smem_cnt ? pick_nhi<true>(nhi, vpt, k) : pick_nhi<false>(nhi, vpt, k);
+
+// Per function: count entries (s * s4 per cluster: every member is a row) and rows the tiles of
+// that function can hand to k_row_topk -- the exact sizes of its buffers.
+__global__ void k_cnt_need(const BigC *__restrict__ bcs, int64_t ncl, unsigned long long *__restrict__ need, int t) {
+  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= ncl) return;
+  const BigC B = bcs[c];
+  const unsigned long long s = (unsigned long long)B.s;
+  atomicAdd(&need[B.f], s * ((s + 3) & ~3ull));
+  atomicAdd(&need[t + B.f], s);
 }
 
 __global__ void k_init_pads(c2_cand *__restrict__ R, int64_t E) {
@@ -1862,6 +1271,7 @@ int local_knn(c2_ctx *ctx, const Csr &csr_in, int t, const Clusters &cl, int k, 
   int32_t nwin = (int32_t)((m + 50000 - 1) / 50000);
   int32_t W = (int32_t)((m + nwin - 1) / nwin);
 
+  unsigned long long *hv_need = nullptr;
   if (nslices > 0) {
     bcs = (BigC *)ws_get(ctx, "bc", (size_t)ncl * sizeof(BigC), &rc);
     if (rc) return rc;
@@ -1905,6 +1315,13 @@ int local_knn(c2_ctx *ctx, const Csr &csr_in, int t, const Clusters &cl, int k, 
                                            tiles);
       C2_LAUNCHED(ctx, "k_mix_bc");
     }
+    // exact sizes of the per-function buffers handed to k_row_topk (read at the next sync)
+    hv_need = (unsigned long long *)ws_get(ctx, "hv_need", (size_t)2 * C2_MAX_T * 8, &rc);
+    if (rc) return rc;
+    C2_CUDA(ctx, cudaMemsetAsync(hv_need, 0, (size_t)2 * t * 8, st));
+    k_cnt_need<<<nblk(ncl), 256, 0, st>>>(bcs, ncl, hv_need, t);
+    C2_LAUNCHED(ctx, "k_cnt_need");
+    C2_CUDA(ctx, cudaMemcpyAsync(ctx->h_small + 256, hv_need, (size_t)2 * t * 8, cudaMemcpyDeviceToHost, st));
     // cluster-local relabeling (one window of kc+1 words per tile) when the unit bitmaps fit
     // in shared memory; otherwise windows over the global item range
     const int32_t nwq = (m + 31) / 32;
@@ -1974,56 +1391,70 @@ int local_knn(c2_ctx *ctx, const Csr &csr_in, int t, const Clusters &cl, int k, 
     C2_LAUNCHED(ctx, "k_tile_rec");
   }
 
+  // ---- light-row survivor buffers (fused only): surv [n][qmax], per-user counts zeroed here and
+  //      re-zeroed by k_surv_merge after every function
+  c2_cand *surv = nullptr;
+  int32_t *surv_qn = nullptr;
+  const int surv_qmax = ctx->surv_qmax;
+  if (fused && C2_LIGHT && surv_qmax > 0 && nslices > 0) {
+    surv = (c2_cand *)ws_get(ctx, "surv", (size_t)n * surv_qmax * sizeof(c2_cand), &rc);
+    if (rc) return rc;
+    surv_qn = (int32_t *)ws_get(ctx, "surv_qn", (size_t)n * 4, &rc);
+    if (rc) return rc;
+    C2_CUDA(ctx, cudaMemsetAsync(surv_qn, 0, (size_t)n * 4, st));
+  }
   // ---- tile kernel configuration
   TileKernel tk = nullptr;
   int grid = 0;
-  int qcap = 64;
-  int32_t rl_off = 0, stg_off = 0, stg_cap = 0;
+  int32_t stg_off = 0, stg_cap = 0;
   size_t smem = 0;
-  uint32_t *gscratch = nullptr;
   int *counters = nullptr;
-  const int32_t smax = (int32_t)std::max<uint32_t>(maxs, 32);
+  uint16_t *hv_cnt = nullptr;
+  RowRec *hv_recs = nullptr;
+  unsigned long long *hv_ctr = nullptr;
+  int *hv_err = nullptr;
+  int64_t hv_cap = 0, hv_rcap = 0;
   if (nslices > 0) {
     int nbits = bits_for((int64_t)csr.max_len + 1);
     int nhi = std::max(nbits - 4, 1);
     int max_sl = (int)((maxs + 31) / 32);
     int vpt = max_sl <= TILE_WARPS ? 1 : max_sl <= 2 * TILE_WARPS ? 2 : 4;
-    // survivor queue per row: 256 entries where shared memory allows, at least 64*KS
-    const int qmin = k <= 32 ? 64 : 128;
-    qcap = 256;
     const size_t budget = (C2_SMEM_BUDGET ? std::min<size_t>(C2_SMEM_BUDGET, ctx->smem_optin) : ctx->smem_optin) -
-                          4096;  // minus the kernel's static shared memory (~2.1 KB)
-    const size_t rlw = fused ? (size_t)64 * k : 0;  // the rows' running lists (Cand = 2 words)
-    const size_t stgw = 4096;  // staging of the next tile's row blocks: at least 16 KB
-    while (qcap > qmin && ((size_t)K8Lay(smax, qcap).words + rlw + stgw) * 4 > budget) qcap -= 64;
-    const int k8w = K8Lay(smax, qcap).words;
-    const size_t mw = (size_t)((W + 4) & ~3);
-    // counts in shared memory (aliased onto M) when one g0 group covers the largest cluster
-    // and the K8 region fits; else a per-CTA global scratch region
-    const bool smem_cnt = max_sl <= 4 * TILE_WARPS && ((size_t)k8w + rlw) * 4 <= budget;
-    rl_off = (int32_t)(((smem_cnt ? std::max(mw, (size_t)k8w) : mw) + 3) & ~(size_t)3);
-    stg_off = (int32_t)(((size_t)rl_off + rlw + 3) & ~(size_t)3);
+                          4096;  // minus the kernel's static shared memory (~2.5 KB)
+    const size_t mw = (size_t)((W + 4) & ~3);  // M: W + 1 words
+    stg_off = (int32_t)mw;
     stg_cap = (int32_t)std::min<int64_t>(4096, ((int64_t)budget / 4 - stg_off) / 4);  // 16-byte groups
     if (stg_cap < 64) stg_cap = 0;
     smem = ((size_t)stg_off + (size_t)stg_cap * 4) * 4;
-    tk = pick_tile(nhi, vpt, k, smem_cnt);
+    tk = pick_tile(nhi, vpt);
     C2_CUDA(ctx, cudaFuncSetAttribute(tk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int occ = 0;
     C2_CUDA(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, tk, TILE_T, smem));
     occ = std::max(occ, 1);
     grid = (int)std::min<int64_t>((int64_t)ctx->num_sms * occ, nslices);
-    if (!smem_cnt) {
-      gscratch = (uint32_t *)ws_get(ctx, "tile_scratch", (size_t)grid * k8w * 4, &rc);
-      if (rc) return rc;
-    }
     counters = (int *)ws_get(ctx, "tile_counter", 4 * (2 * C2_MAX_T + 2), &rc);
     if (rc) return rc;
     C2_CUDA(ctx, cudaMemsetAsync(counters, 0, 4 * (2 * C2_MAX_T + 2), st));
+    // rows handed to k_row_topk, per function (the buffers are reused function after function)
+    for (int f = 0; f < t; ++f) {
+      hv_cap = std::max<int64_t>(hv_cap, (int64_t)ctx->h_small[256 + f]);
+      hv_rcap = std::max<int64_t>(hv_rcap, (int64_t)ctx->h_small[256 + t + f]);
+    }
+    hv_cnt = (uint16_t *)ws_get(ctx, "hv_cnt", (size_t)hv_cap * 2 + 16, &rc);
+    if (rc) return rc;
+    hv_recs = (RowRec *)ws_get(ctx, "hv_recs", (size_t)(hv_rcap + 1) * sizeof(RowRec), &rc);
+    if (rc) return rc;
+    hv_ctr = (unsigned long long *)ws_get(ctx, "hv_ctr", (size_t)(2 * C2_MAX_T + 2) * 8, &rc);
+    if (rc) return rc;
+    hv_err = (int *)(hv_ctr + 2 * C2_MAX_T + 1);
+    C2_CUDA(ctx, cudaMemsetAsync(hv_ctr, 0, (size_t)(2 * C2_MAX_T + 2) * 8, st));
   }
-  auto launch_tiles = [&](int64_t lo, int64_t hi, int ci, const c2_cand *seed, c2_cand *dst) -> int {
+  // tiles [lo, hi) of function f: counts -> light rows' survivors (c2_build) + count rows for k_row_topk
+  auto launch_tiles = [&](int64_t lo, int64_t hi, int ci, int f) -> int {
     if (hi <= lo) return C2_OK;
     TileArgs ta{tiles, lo, hi, counters + ci, bcs, vperm, vsize, trec, blk_len8, blk_off8, packed, csr.psize, n, W, nwin, k,
-                seed, dst, ctx->kstats, gscratch, smax, qcap, rl_off, stg_off, stg_cap, relabel ? 1 : 0};
+                fused ? out : nullptr, ctx->kstats, stg_off, stg_cap, relabel ? 1 : 0, fused ? surv : nullptr, surv_qn,
+                surv_qmax, hv_cnt, hv_cap, hv_ctr + f, hv_recs, hv_rcap, hv_ctr + C2_MAX_T + f, hv_err};
     int g = (int)std::min<int64_t>(grid, hi - lo);
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     if (ctx->timing) {
@@ -2041,7 +1472,19 @@ int local_knn(c2_ctx *ctx, const Csr &csr_in, int t, const Clusters &cl, int k, 
     C2_LAUNCHED(ctx, "k_local_tile");
     if (ctx->timing) C2_CUDA(ctx, cudaEventRecord(e1, st));
     ctx->stats.tile_launches++;
+    if (ctx->sync_check) {
+      int herr = 0;
+      C2_CUDA(ctx, cudaMemcpy(&herr, hv_err, 4, cudaMemcpyDeviceToHost));
+      if (herr) return set_err(ctx, C2_ECUDA, "k_local_tile: row buffers too small (internal sizing error)");
+    }
     return C2_OK;
+  };
+  // the per-row top-k of the rows function f's tiles handed over
+  auto launch_rows = [&](int f) -> int {
+    if (nslices == 0) return C2_OK;
+    RowArgs ra{hv_recs, (const int64_t *)(hv_ctr + C2_MAX_T + f), hv_cnt, vperm, vsize, fused ? out : nullptr, out, n, k,
+               ctx->kstats};
+    return launch_row_topk(ctx, ra);
   };
   auto launch_singles = [&](int64_t lo, int64_t hi, const c2_cand *seed, c2_cand *dst) -> int {
     if (hi <= lo) return C2_OK;
@@ -2050,22 +1493,20 @@ int local_knn(c2_ctx *ctx, const Csr &csr_in, int t, const Clusters &cl, int k, 
     C2_LAUNCHED(ctx, "k_singles");
     return C2_OK;
   };
-  if (!fused) {
-    C2_TRY(launch_tiles(0, nslices, 0, nullptr, out));
-    C2_TRY(launch_singles(0, nsingle, nullptr, out));
-    if (result) *result = out;
-  } else {
-    // Alg. 3 order: function by function, every user's running list is merged in place with
-    // its neighbourhood in that function's cluster (singletons: nothing to merge)
-    int64_t blo = 0;
-    for (int f = 0; f < t; ++f) {
-      int64_t bhi = blo + hfc[f * WLC + 0];
-      C2_TRY(launch_tiles(blo, bhi, 2 * f, out, out));
-      C2_TRY(launch_tiles(nbigtiles + mix_lo[f], nbigtiles + mix_lo[f + 1], 2 * f + 1, out, out));
-      blo = bhi;
-    }
-    if (result) *result = out;
+  // Alg. 3 order (c2_build): function by function, every user's running list is merged in place
+  // with its neighbourhood in that function's cluster (singletons: nothing to merge).
+  // c2_local_knn: the same launches write each function's lists cand[f].
+  int64_t blo = 0;
+  for (int f = 0; f < t; ++f) {
+    const int64_t bhi = blo + hfc[f * WLC + 0];
+    C2_TRY(launch_tiles(blo, bhi, 2 * f, f));
+    C2_TRY(launch_tiles(nbigtiles + mix_lo[f], nbigtiles + mix_lo[f + 1], 2 * f + 1, f));
+    C2_TRY(launch_rows(f));
+    if (surv) C2_TRY(launch_surv_merge(ctx, surv, surv_qn, surv_qmax, n, k, out));  // light rows' Alg. 3 step
+    blo = bhi;
   }
+  if (!fused) C2_TRY(launch_singles(0, nsingle, nullptr, out));
+  if (result) *result = out;
   return C2_OK;
 }
 

@@ -1,0 +1,357 @@
+// k_rows.cu -- Step 2's per-row exact top-k (K8) and the light rows' Alg. 3 step, as kernels of
+// their own, run after each k_local_tile launch.
+//
+// k_local_tile computes every tile's intersection counts |P_r ∩ P_v| (phase A) and splits its rows:
+//   light rows (c2_build, running list full): screened in the tile's epilogue; the few cluster-mates
+//       strictly better than the row's running k-th best are left in surv[u][..] -> k_surv_merge;
+//   the other rows: their count row cnt[v] (u16, one entry per cluster member) and a RowRec go to
+//       global memory -> k_row_topk.
+// Both kernels are one warp per row/user with many warps per SM, so the latency-bound selection
+// and merge steps of one row overlap other rows' instead of holding the tile's CTA barrier.
+#include "cand.cuh"
+#include "k_rows.cuh"
+
+namespace c2 {
+
+// ---------------------------------------------------------------- K8: exact top-k of one row
+// Candidates of row u: the members v != u of its cluster (or of its slot group in a mixed slice),
+// with i = cnt[v] = |P_u ∩ P_v| and U = |P_u| + |P_v| - i.  Output: the k best under the
+// order (A13) -- written as the function's list (c2_local_knn) or merged with the row's running
+// Alg. 3 list in place (c2_build).  Exactness: a candidate is queued only if it is not
+// worse than a valid lower bound of the k-th best (the running k-th best, or the k-th best of any
+// k distinct candidates); the queue is then sorted on exact keys (cand.cuh).
+constexpr int RT_WARPS = 8;
+constexpr int RT_QCAP = 256;  // survivor queue per warp (>= 64 * KS)
+
+template <int KS>
+__global__ void __launch_bounds__(RT_WARPS * 32) k_row_topk(RowArgs a) {
+  constexpr int R1 = 2 * KS;
+  __shared__ __align__(16) Cand s_q[RT_WARPS][RT_QCAP];
+  __shared__ __align__(16) c2_cand s_run[RT_WARPS][C2_MAX_K];
+  __shared__ int s_wq[RT_WARPS];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int kk = a.k;
+  const int qcap = RT_QCAP;
+  Cand *qr = s_q[warp];
+  if (lane == 0) s_wq[warp] = 0;
+  __syncwarp();
+  const int64_t nrec = *a.nrec;
+  for (int64_t ri = (int64_t)blockIdx.x * RT_WARPS + warp; ri < nrec; ri += (int64_t)gridDim.x * RT_WARPS) {
+    const RowRec rec = a.recs[ri];
+    const int32_t u = rec.u;
+    const uint32_t prr = (uint32_t)rec.pr;
+    const int s = rec.s;
+    const int slot = rec.slot;
+    const int selfr = rec.selfr;
+    const uint16_t *cr = a.cnt + rec.cnt_off;
+    const int32_t *vid = a.vperm + rec.vp_off;
+    const int32_t *vps = a.vsize + rec.vp_off;
+    // running list (fused): staged in shared memory, the output overwrites it in place
+    if (a.seed) {
+      for (int j = lane; j < kk; j += 32) s_run[warp][j] = a.seed[(int64_t)u * kk + j];
+      __syncwarp();
+    }
+    const c2_cand *run = s_run[warp];
+    const Cand tau = a.seed ? from_out(run[kk - 1]) : sent();
+    // survivors of T (strictly better than tau, not worse than a round-1 bound) -> qr; returns
+    // their number (only the first qcap are stored)
+    auto scan = [&](const Ref &T) -> int {
+      if (slot) {
+        const int vi = rec.slot_lo + lane;
+        bool ok = false;
+        Cand x = sent();
+        if (lane < slot && vi != selfr) {
+          const int32_t id = vid[vi];
+          if (id >= 0) {
+            const uint32_t i = cr[vi], ps = (uint32_t)vps[vi];
+            ok = passes(i, ps, id, T);
+            x = Cand{i | ((prr + ps - i) << 16), id};
+          }
+        }
+        const unsigned bal = __ballot_sync(0xffffffffu, ok);
+        if (ok) qr[__popc(bal & ((1u << lane) - 1))] = x;
+        return __popc(bal);
+      }
+      for (int base = 0; base < s; base += 128) {
+        uint32_t iv[4], pv[4];
+        int32_t dv[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const int v = base + 32 * e + lane;
+          iv[e] = v < s ? cr[v] : 0u;
+          pv[e] = v < s ? (uint32_t)vps[v] : 0u;
+          dv[e] = v < s && v != selfr ? vid[v] : INT32_MAX;
+        }
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          if (dv[e] != INT32_MAX && passes(iv[e], pv[e], dv[e], T)) {
+            const int p = atomicAdd(&s_wq[warp], 1);
+            if (p < qcap) qr[p] = Cand{iv[e] | ((prr + pv[e] - iv[e]) << 16), dv[e]};
+          }
+        }
+      }
+      __syncwarp();
+      const int m = s_wq[warp];
+      __syncwarp();
+      if (lane == 0) s_wq[warp] = 0;
+      __syncwarp();
+      return m;
+    };
+    // k-th best of the first 64*KS queue entries (all distinct real candidates): a valid lower
+    // bound of the row's k-th best
+    auto kth_of_queue = [&]() -> Ref {
+      KC e[2 * KS];
+#pragma unroll
+      for (int j = 0; j < 2 * KS; ++j) e[j] = to_kc(qr[32 * j + lane]);
+      sort_kc<2 * KS>(e);
+      return make_ref(kc_cand(warp_get<2 * KS>(e, kk - 1)), prr, true);
+    };
+    // round 1: every lane's best R1 candidates of its share; T_r = the k-th best of the 32*R1
+    // tops (any k distinct candidates bound the row's k-th best from below)
+    auto round1 = [&](Ref &T) {
+      Cand t[R1];
+#pragma unroll
+      for (int j = 0; j < R1; ++j) t[j] = sent();
+      Ref wr = make_ref(sent(), prr, false);
+      for (int v = lane; v < s; v += 32) {
+        if (v == selfr) continue;
+        const uint32_t iv = cr[v], pv = (uint32_t)vps[v];
+        const int32_t dv = vid[v];
+        if (passes(iv, pv, dv, wr)) {
+          const Cand x{iv | ((prr + pv - iv) << 16), dv};
+#pragma unroll
+          for (int j = R1 - 1; j > 0; --j) {
+            if (better_c(x, t[j - 1])) t[j] = t[j - 1];
+            else if (better_c(x, t[j])) t[j] = x;
+          }
+          if (better_c(x, t[0])) t[0] = x;
+          wr = make_ref(t[R1 - 1], prr, false);
+        }
+      }
+      KC e[R1];
+#pragma unroll
+      for (int j = 0; j < R1; ++j) e[j] = to_kc(t[j]);
+      sort_kc<R1>(e);
+      const KC Tr = warp_get<R1>(e, kk - 1);
+      if (kc_real(Tr) && better_c(kc_cand(Tr), tau)) T = make_ref(kc_cand(Tr), prr, true);
+    };
+    Ref T = make_ref(tau, prr, false);
+    // rows without a running list yet (tau = sentinel) whose candidates cannot all be queued
+    // start with round 1; rows whose tau lets too many through get it after the first scan
+    bool r1 = !slot && !is_real(tau) && s - 1 > 64 * KS;
+    if (r1) round1(T);
+    int m = scan(T);
+    int zn = min(m, qcap);
+    if (a.kstats && lane == 0) atomicAdd(&a.kstats[16 + min(m, 300) / 20], 1ull);
+    if (m > 64 * KS && !slot && !r1) {
+      if (a.kstats && lane == 0) atomicAdd(&a.kstats[14], 1ull);
+      r1 = true;
+      round1(T);
+      m = scan(T);
+    }
+    int rescans = 0;
+    for (; rescans < 2 && m > qcap; ++rescans) {
+      T = kth_of_queue();
+      __syncwarp();
+      m = scan(T);
+    }
+    // shrink a long queue in place: keep the entries not worse than the k-th best of its first
+    // 64*KS (stops when that makes no progress: massive ties)
+    while (m > 64 * KS && m <= qcap) {
+      const Ref T2 = kth_of_queue();
+      __syncwarp();
+      int w = 0;
+      for (int b0 = 0; b0 < m; b0 += 32) {
+        const int j = b0 + lane;
+        Cand x = j < m ? qr[j] : sent();
+        const uint32_t i = x.iu & 0xFFFFu, ps = (x.iu >> 16) + i - prr;
+        const bool ok = j < m && passes(i, ps, x.id, T2);
+        __syncwarp();
+        const unsigned bal = __ballot_sync(0xffffffffu, ok);
+        if (ok) qr[w + __popc(bal & ((1u << lane) - 1))] = x;
+        w += __popc(bal);
+      }
+      __syncwarp();
+      if (w == m) break;
+      m = w;
+    }
+    (void)zn;
+    if (a.kstats && lane == 0) {
+      atomicAdd(&a.kstats[0], 1ull);
+      atomicAdd(&a.kstats[1], m == 0 ? 1ull : 0ull);
+      atomicAdd(&a.kstats[2], (unsigned long long)m);
+      atomicAdd(&a.kstats[3], m > 32 * KS ? 1ull : 0ull);
+      atomicAdd(&a.kstats[4], (unsigned long long)rescans);
+      atomicAdd(&a.kstats[6], r1 ? 1ull : 0ull);
+      int ev = s - 1;  // pair evaluations of this row: its cluster-mates (debug work accounting)
+      if (slot) {
+        ev = -1;
+        for (int j = 0; j < slot; ++j) ev += vid[rec.slot_lo + j] >= 0 ? 1 : 0;
+      }
+      atomicAdd(&a.kstats[70], (unsigned long long)ev);
+    }
+    c2_cand *dst = a.seed ? a.out + (int64_t)u * kk : a.out + ((int64_t)rec.f * a.n + u) * kk;
+    if (a.seed && m == 0) continue;
+    if (a.seed && m <= 32) {
+      // few survivors: Alg. 3 step by ranks (no sorting network, no f64 keys)
+      rank_merge<KS>(qr, m, run, kk, dst);
+      __syncwarp();
+      continue;
+    }
+    KC L[KS];  // top-k of this function's survivors (sentinel padded)
+    if (m <= 32 * KS) {
+      KC q[KS];
+#pragma unroll
+      for (int j = 0; j < KS; ++j) q[j] = to_kc((32 * j + lane < m) ? qr[32 * j + lane] : sent());
+      sort_kc<KS>(q);
+#pragma unroll
+      for (int j = 0; j < KS; ++j) L[j] = q[j];
+    } else if (m <= 64 * KS) {
+      KC q[2 * KS];
+#pragma unroll
+      for (int j = 0; j < 2 * KS; ++j) q[j] = to_kc((32 * j + lane < m) ? qr[32 * j + lane] : sent());
+      sort_kc<2 * KS>(q);
+#pragma unroll
+      for (int j = 0; j < KS; ++j) L[j] = q[j];
+    } else {
+      // pathological ties: exact insertion over the row's candidates
+      if (a.kstats && lane == 0) atomicAdd(&a.kstats[8], 1ull);
+      Cand Lc[KS];
+#pragma unroll
+      for (int j = 0; j < KS; ++j) Lc[j] = sent();
+      Cand thr = sent();
+      for (int vb = 0; vb < s; vb += 32) {
+        const int vi = vb + lane;
+        Cand c = sent();
+        if (vi < s) {
+          const int32_t v = vid[vi];
+          if (v >= 0 && vi != selfr && (slot == 0 || (vi - rec.slot_lo >= 0 && vi - rec.slot_lo < slot))) {
+            const uint32_t ci = cr[vi];
+            c = Cand{ci | ((prr + (uint32_t)vps[vi] - ci) << 16), v};
+          }
+        }
+        const bool bt = is_real(c) && better_c(c, tau) && better_c(c, thr);
+        unsigned mask = __ballot_sync(0xffffffffu, bt);
+        while (mask) {
+          const int l = __ffs(mask) - 1;
+          mask &= mask - 1;
+          const Cand x = shfl_c(c, l);
+          if (!better_c(x, thr)) continue;
+          warp_insert<KS>(Lc, x);
+          thr = warp_get<KS>(Lc, kk - 1);
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < KS; ++j) L[j] = to_kc(Lc[j]);
+    }
+    if (!a.seed) {
+#pragma unroll
+      for (int j = 0; j < KS; ++j)
+        if (32 * j + lane < kk) dst[32 * j + lane] = kc_out(L[j]);
+      continue;
+    }
+    // merge with the running list S (best first): bitonic sequence L(first k) ++ reverse(S)
+    KC S[KS];
+#pragma unroll
+    for (int j = 0; j < KS; ++j) S[j] = to_kc((32 * j + lane < kk) ? from_out(run[32 * j + lane]) : sent());
+    KC mm[2 * KS];
+#pragma unroll
+    for (int j = 0; j < KS; ++j) mm[j] = (32 * j + lane < kk) ? L[j] : KC{0ull, 1u << 16};
+#pragma unroll
+    for (int j = 0; j < KS; ++j) mm[KS + j] = shfl_e(S[KS - 1 - j], 31 - lane);
+    merge_kc<2 * KS>(mm);
+    // drop adjacent duplicates (a repeated id carries identical values, A16); keep k
+    int base = 0;
+#pragma unroll
+    for (int j = 0; j < 2 * KS; ++j) {
+      const uint32_t lo = (uint32_t)mm[j].k;
+      uint32_t prev = __shfl_up_sync(0xffffffffu, lo, 1);
+      const uint32_t prevj = j > 0 ? __shfl_sync(0xffffffffu, (uint32_t)mm[j - 1].k, 31) : 0u;
+      if (lane == 0) prev = prevj;
+      const bool keep = kc_real(mm[j]) && (j + lane == 0 || lo != prev);
+      const unsigned bal = __ballot_sync(0xffffffffu, keep);
+      const int rank = base + __popc(bal & ((1u << lane) - 1));
+      if (keep && rank < kk) dst[rank] = kc_out(mm[j]);
+      base += __popc(bal);
+    }
+    for (int p = base + lane; p < kk; p += 32) dst[p] = c2_cand{-1, 0, 0};
+    __syncwarp();
+  }
+}
+
+// ---------------------------------------------------------------- light rows' Alg. 3 step
+// k_local_tile's phase-A epilogue left each light user's survivors -- its cluster-mates strictly
+// better than its running k-th best -- in surv[u][0..qn[u]).  One warp per user with survivors:
+// the running list S (full, best first) sits in registers (lane j holds S[32*jj + j]); survivors
+// are read 32 at a time, those still strictly better than the current k-th best are inserted one
+// by one (a duplicate id carries the same (i, U) and is skipped, A16), the k-th best refreshed
+// after each insertion.  The result is the first k distinct ids of S ∪ Q under the order (A13),
+// whatever the survivors' order.
+template <int KS>
+__global__ void __launch_bounds__(256) k_surv_merge(const c2_cand *__restrict__ surv, int32_t *__restrict__ qn,
+                                                    int qmax, int32_t n, int k, c2_cand *__restrict__ run) {
+  const int lane = threadIdx.x & 31;
+  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwg = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t ub = gw * 32; ub < n; ub += nwg * 32) {
+    const int64_t uu = ub + lane;
+    const int c = uu < n ? qn[uu] : 0;
+    if (c > 0) qn[uu] = 0;
+    unsigned mask = __ballot_sync(0xffffffffu, c > 0);
+    while (mask) {
+      const int j = __ffs(mask) - 1;
+      mask &= mask - 1u;
+      const int64_t u = ub + j;
+      const int m = __shfl_sync(0xffffffffu, c, j);
+      c2_cand *Rw = run + u * k;
+      Cand S[KS];
+#pragma unroll
+      for (int jj = 0; jj < KS; ++jj) S[jj] = (32 * jj + lane < k) ? from_out(Rw[32 * jj + lane]) : sent();
+      Cand tau = warp_get<KS>(S, k - 1);
+      const c2_cand *Q = surv + u * qmax;
+      bool changed = false;
+      for (int c0 = 0; c0 < m; c0 += 32) {
+        const Cand x = c0 + lane < m ? from_out(Q[c0 + lane]) : sent();
+        unsigned bal = __ballot_sync(0xffffffffu, is_real(x) && better_c(x, tau));
+        while (bal) {
+          const int l = __ffs(bal) - 1;
+          bal &= bal - 1u;
+          const Cand y = shfl_c(x, l);
+          if (!better_c(y, tau)) continue;  // (uniform)
+          bool dup = false;
+#pragma unroll
+          for (int jj = 0; jj < KS; ++jj) dup |= S[jj].id == y.id;
+          if (__any_sync(0xffffffffu, dup)) continue;
+          warp_insert<KS>(S, y);
+          tau = warp_get<KS>(S, k - 1);
+          changed = true;
+        }
+      }
+      if (changed) {
+#pragma unroll
+        for (int jj = 0; jj < KS; ++jj)
+          if (32 * jj + lane < k) Rw[32 * jj + lane] = to_out(S[jj]);
+      }
+    }
+  }
+}
+
+int launch_row_topk(c2_ctx *ctx, const RowArgs &ra) {
+  static int occ[2] = {0, 0};
+  const int ks = ra.k <= 32 ? 0 : 1;
+  auto kern = ks ? k_row_topk<2> : k_row_topk<1>;
+  if (!occ[ks]) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ[ks], kern, RT_WARPS * 32, 0);
+  kern<<<ctx->num_sms * std::max(occ[ks], 1), RT_WARPS * 32, 0, ctx->stream>>>(ra);
+  C2_LAUNCHED(ctx, "k_row_topk");
+  return C2_OK;
+}
+
+int launch_surv_merge(c2_ctx *ctx, const c2_cand *surv, int32_t *qn, int qmax, int32_t n, int k, c2_cand *run) {
+  const int g = ctx->num_sms * 8;
+  if (k <= 32) k_surv_merge<1><<<g, 256, 0, ctx->stream>>>(surv, qn, qmax, n, k, run);
+  else k_surv_merge<2><<<g, 256, 0, ctx->stream>>>(surv, qn, qmax, n, k, run);
+  C2_LAUNCHED(ctx, "k_surv_merge");
+  return C2_OK;
+}
+
+}  // namespace c2

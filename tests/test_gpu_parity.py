@@ -441,6 +441,32 @@ def test_pair_evaluations_equal_2P(ctx, cfg):
     assert ctx.stats()["pairs"] == P
 
 
+@pytest.mark.parametrize("qmax", [0, 1, 3, 4096])
+@pytest.mark.parametrize("cfg", ["c2", "c3", "c4"])
+def test_build_survivor_slots(ctx, cfg, qmax):
+    """Light-row path (C2_OPT_SURVIVORS): rows with a full running list are screened in the local
+    kernel's epilogue and merged by k_surv_merge.  0 = every row merged in-tile; 1 and 3 slots make
+    most light rows overflow into the in-tile fallback; all give the oracle's graph bytewise."""
+    C = synth.config(cfg)
+    offs, items = synth.generate(cfg)
+    ctx.set_option(c2.OPT_SURVIVORS, qmax)
+    try:
+        check_build(ctx, offs, items, C.t, C.b, C.N, C.k, C.hash_seed)
+    finally:
+        ctx.set_option(c2.OPT_SURVIVORS, 128)
+
+
+@pytest.mark.parametrize("seed", range(8))
+@pytest.mark.parametrize("qmax", [1, 2])
+def test_build_random_survivor_slots(ctx, seed, qmax):
+    offs, items, t, b, N, k, hs = random_case(100 + seed)
+    ctx.set_option(c2.OPT_SURVIVORS, qmax)
+    try:
+        check_build(ctx, offs, items, max(t, 3), b, N, k, hs, mode=seed % 2)
+    finally:
+        ctx.set_option(c2.OPT_SURVIVORS, 128)
+
+
 @pytest.mark.parametrize("k,n,N", [(50, 2600, 2600), (64, 3000, 1800), (33, 2300, 2300)])
 def test_build_big_clusters_large_k(ctx, k, n, N):
     """Clusters past 2048 members (count matrix in global scratch) and k > 32 (two-register

@@ -16,21 +16,13 @@ ctx.set_option(c2.OPT_KSTATS, ks.data_ptr())
 c2.build(d_o, d_i, k=C.k, t=C.t, b=C.b, N=C.N, seed=C.hash_seed, ctx=ctx)
 torch.cuda.synchronize()
 k = ks.tolist()
-print(f"{name}: rows {k[0]} nq==0 {k[1]/k[0]:.3f} mean nq {k[2]/k[0]:.2f} nq>32KS {k[3]/k[0]:.4f} overflow {k[4]/k[0]:.5f} "
-      f"tiles {k[5]} round1 rows {k[6]} mean s {k[7]/max(k[5],1):.1f} exact-fallback rows {k[8]}")
-tot = sum(k[9:14])
-print("  warp-cycles: " + " ".join(f"{n} {v / tot * 100:.1f}%" for n, v in
-      zip(["phaseA", "round1", "scan", "k8-rest", "k8-wait"], k[9:14])))
-print(f"  round1-after-overflow rows {k[14]}  kth_of_queue calls {k[15]}")
+print(f"{name}: k_row_topk rows {k[0]} nq==0 {k[1]/max(k[0],1):.3f} mean nq {k[2]/max(k[0],1):.2f} "
+      f"nq>32KS {k[3]/max(k[0],1):.4f} rescans {k[4]} round1 rows {k[6]} exact-fallback rows {k[8]}")
 print("  first-scan m histogram (bins of 20): " + " ".join(str(x) for x in k[16:32]))
+print(f"  light rows {k[71]} survivors {k[72]} (mean {k[72] / max(k[71], 1):.2f}) overflowed to k_row_topk {k[73]}")
 tt = sum(k[32:36]) or 1
-print("  tile cycles by class (share, tiles, mean cycles): " + " ".join(
-    f"{n}: {k[32 + i] / tt * 100:.1f}% {k[36 + i]} {k[32 + i] / max(k[36 + i], 1):.0f}" for i, n in enumerate(["mixed", "33-256", "257-1024", ">1024"])))
 for i, nm in enumerate(["mixed", "33-256", "257-1024", ">1024"]):
     mt = max(k[36 + i], 1)
-    b = 40 + 5 * i
-    print(f"  {nm:9s} tile (warp 0, mean cycles): build-sum {k[b] / mt:.0f}  probe {k[b + 1] / mt:.0f}  "
-          f"phaseA-rest {k[b + 2] / mt:.0f}  K8 {k[b + 3] / mt:.0f}  wait {k[b + 4] / mt:.0f}")
-nb = max(k[62], 1)
-print(f"  rows of >1024 tiles (warp 0 sample): select {k[60] / nb:.0f} cycles/row  final {k[61] / nb:.0f} cycles/row  rows {k[62]}")
+    print(f"  {nm:9s} tiles {k[36 + i]:7d} share {k[32 + i] / tt * 100:5.1f}%  mean cycles {k[32 + i] / mt:8.0f}: "
+          f"phase A {k[40 + 3 * i] / mt:8.0f}  light epilogue {k[41 + 3 * i] / mt:7.0f}  count rows {k[42 + 3 * i] / mt:7.0f}")
 print(f"  probe of >1024 tiles: busy cycles per warp-step {k[64] / max(k[65], 1):.0f}  steps {k[65]}")
