@@ -42,6 +42,9 @@
 #ifndef C2_BULK
 #define C2_BULK 1  // 1: tile records + staged row blocks by cp.async.bulk on mbarriers (TMA bulk path)
 #endif
+#ifndef C2_SPLIT
+#define C2_SPLIT 1  // 1: tiles of <= 8 slices split each member list over several warps
+#endif
 #ifndef C2_RANKMERGE
 #define C2_RANKMERGE 1  // 1: rank-based Alg. 3 step for <= 32 survivors; 0: insertion (<= 16)
 #endif
@@ -667,6 +670,7 @@ struct TileArgs {
   const c2_cand *seed;  // fused: running lists before this function [n][k]; else nullptr
   unsigned long long *kstats;  // C2_OPT_KSTATS counters or nullptr
   int32_t stg_off, stg_cap;  // staging buffer (word offset, capacity in 16-byte groups; 0: off)
+  int32_t scr_off;      // split-probe scratch (word offset; 0: M's own words)
   int relabel;          // 1: items are unit-local ids, the tile's window is [0, B.kc) (nwin == 1)
   c2_cand *surv;        // fused light-row path: survivors [n][qmax] (nullptr: no light rows)
   int32_t *qn;          // survivors per user (read and zeroed by k_surv_merge)
@@ -852,8 +856,27 @@ __global__ void __launch_bounds__(TILE_T, C2_TILE_MINB) k_local_tile(TileArgs a)
     const unsigned valid = __ballot_sync(0xffffffffu, lane < nr && s_ru[lane] >= 0);
     unsigned k8rows = valid;  // rows handed to k_row_topk
     const bool lt = light_on && nsl <= VPT * TILE_WARPS;  // (one g0 group: counters of all members live)
+    // small tiles (<= TILE_WARPS/2 slices): G warps share a slice, each probing a contiguous part
+    // of its member lists; the partial bit-sliced counters are then added (bit-sliced ripple
+    // carry), so no warp idles through the probe of a tile with few slices
+    int G = 1;
+    if (C2_SPLIT && nsl <= TILE_WARPS / 2) {
+      // parts of >= ~4 steps (pairs of 8-item groups; the rows' own lengths stand for the slices')
+      int np = 0;
+      for (int w = 0; w < nwin; ++w) np += (s_bl[cur][w] + 1) >> 1;
+      G = TILE_WARPS;
+      while (G > 1 && (G * nsl > TILE_WARPS || 4 * G > np)) G >>= 1;
+    }
+    const int part = warp % G;
     // ================= phase A: counts |P_r ∩ P_v| for the 32 rows x all v of the cluster
     for (int g0 = 0; g0 < nsl; g0 += VPT * TILE_WARPS) {
+      // the slice of this warp's q-th counter (nsl: none); after the probe (all = false) a split
+      // slice belongs to its part-0 warp only, which holds the added counters
+      auto slice_of = [&](int q, bool all = false) -> int {
+        if (G > 1) return (q == 0 && warp / G < nsl && (all || part == 0)) ? warp / G : nsl;
+        const int jj = g0 + q * TILE_WARPS + ((C2_SNAKE && (q & 1)) ? TILE_WARPS - 1 - warp : warp);
+        return jj < nsl ? jj : nsl;
+      };
       Counter<NHI> C[VPT];
 #pragma unroll
       for (int q = 0; q < VPT; ++q) C[q].zero();
@@ -882,15 +905,21 @@ __global__ void __launch_bounds__(TILE_T, C2_TILE_MINB) k_local_tile(TileArgs a)
         int nsteps = 0;
 #pragma unroll
         for (int q = 0; q < VPT; ++q) {
-          const int jj = g0 + q * TILE_WARPS + ((C2_SNAKE && (q & 1)) ? TILE_WARPS - 1 - warp : warp);
+          const int jj = slice_of(q, true);
           if (jj < nsl) {
             const int64_t bi = (int64_t)(B.sl_off + jj) * nwin + w;
             const bool own = stgd && jj == T.j;  // the tile's own slice: staged
             const int32_t len8 = own ? s_bl[cur][w] : a.blk_len8[bi];
             const uint4 *src = (own ? stg + s_so[cur][w] : a.packed + (int64_t)a.blk_off8[bi] * 32) + lane;
             auto ld = [&](int32_t p) { return p < len8 ? src[(int64_t)p * 32] : padv; };
-            uint4 d0 = ld(0), d1 = ld(1), n0 = ld(2), n1 = ld(3);
-            for (int32_t p8 = 0; p8 < len8; p8 += 2) {
+            int32_t plo = 0, phi = len8;  // this warp's part of the lists (pairs of 8-item groups)
+            if (G > 1) {
+              const int32_t np = (len8 + 1) >> 1;
+              plo = 2 * ((part * np) / G);
+              phi = 2 * (((part + 1) * np) / G);
+            }
+            uint4 d0 = ld(plo), d1 = ld(plo + 1), n0 = ld(plo + 2), n1 = ld(plo + 3);
+            for (int32_t p8 = plo; p8 < phi; p8 += 2) {
               const uint4 f0 = ld(p8 + 4), f1 = ld(p8 + 5);
               uint32_t m[8];
               masks8(M, d0, m);
@@ -934,6 +963,47 @@ __global__ void __launch_bounds__(TILE_T, C2_TILE_MINB) k_local_tile(TileArgs a)
         }
         __syncthreads();
       }
+      if (G > 1) {
+        // add the G partial counters of each slice into its part-0 warp (scratch: [warp][plane][lane]
+        // in M's words when M is big enough -- re-zeroed by the reader -- else a region of its own)
+        constexpr int NPL = 4 + NHI;
+        uint32_t *scr = a.scr_off ? dyn + a.scr_off : M;
+        if (part != 0 && warp / G < nsl) {
+          uint32_t *o = scr + warp * NPL * 32 + lane;
+          o[0] = C[0].ones;
+          o[32] = C[0].twos;
+          o[64] = C[0].fours;
+          o[96] = C[0].eights;
+#pragma unroll
+          for (int i = 0; i < NHI; ++i) o[(4 + i) * 32] = C[0].H[i];
+        }
+        __syncthreads();
+        if (part == 0 && warp / G < nsl) {
+          for (int pw = 1; pw < G; ++pw) {
+            uint32_t *o = scr + (warp + pw) * NPL * 32 + lane;
+            uint32_t b[NPL];
+#pragma unroll
+            for (int j = 0; j < NPL; ++j) {
+              b[j] = o[j * 32];
+              if (!a.scr_off) o[j * 32] = 0u;
+            }
+            uint32_t *pa[NPL];
+            pa[0] = &C[0].ones;
+            pa[1] = &C[0].twos;
+            pa[2] = &C[0].fours;
+            pa[3] = &C[0].eights;
+#pragma unroll
+            for (int i = 0; i < NHI; ++i) pa[4 + i] = &C[0].H[i];
+            uint32_t cy = 0u;
+#pragma unroll
+            for (int j = 0; j < NPL; ++j) {
+              const uint32_t x = *pa[j], y = b[j];
+              *pa[j] = x ^ y ^ cy;
+              cy = (x & y) | (cy & (x ^ y));
+            }
+          }
+        }
+      }
       // the staging buffer is dead now: the next tile's row blocks may be copied in
       if (g0 + VPT * TILE_WARPS >= nsl && warp == TILE_WARPS - 1) fetch_finish(cur ^ 1);
       if (a.kstats) ckA = clock64();
@@ -946,13 +1016,20 @@ __global__ void __launch_bounds__(TILE_T, C2_TILE_MINB) k_local_tile(TileArgs a)
           // per row (lane r): the light row's reference tau = (iT, UT) and |P_r|
           const uint4 Rr = s_ref[lane];  // A = UT + iT, B = iT |P_r|, iT
           const bool lr = (lm >> lane) & 1u;
+          int32_t idq[VPT];
+          uint32_t psq[VPT];  // the members' ids and sizes, all requested at once
 #pragma unroll
           for (int q = 0; q < VPT; ++q) {
-            const int jj = g0 + q * TILE_WARPS + ((C2_SNAKE && (q & 1)) ? TILE_WARPS - 1 - warp : warp);
+            const int vi = slice_of(q) * 32 + lane;
+            idq[q] = vi < s ? __ldg(vp + vi) : -1;
+            psq[q] = vi < s ? (uint32_t)__ldg(a.vsize + B.vp_off + vi) : 0u;
+          }
+#pragma unroll
+          for (int q = 0; q < VPT; ++q) {
+            const int jj = slice_of(q);
             if (jj >= nsl) continue;  // (warp-uniform: all lanes of a warp share the slice jj)
-            const int vi = jj * 32 + lane;
-            const int32_t idv = vi < s ? vp[vi] : -1;
-            const uint32_t psv = idv >= 0 ? (uint32_t)a.vsize[B.vp_off + vi] : 0xFFFFFFFFu;
+            const int32_t idv = idq[q];
+            const uint32_t psv = idv >= 0 ? psq[q] : 0xFFFFFFFFu;
             // slice bound: every member has |P_v| >= psmin, so a member passes row r only if
             // i (UT + iT) >= iT (|P_r| + psmin), i.e. i >= imin_r; the bit-planes of the 32 imin_r
             const uint32_t psmin = __reduce_min_sync(0xffffffffu, psv);
@@ -980,6 +1057,10 @@ __global__ void __launch_bounds__(TILE_T, C2_TILE_MINB) k_local_tile(TileArgs a)
             }
             if (jj == T.j) hit &= ~(1u << lane);  // the row itself
             if (idv < 0) hit = 0u;
+            if (a.kstats) {
+              const int nh = __reduce_add_sync(0xffffffffu, __popc(hit));
+              if (lane == 0) atomicAdd(&a.kstats[74], (unsigned long long)nh);
+            }
             while (hit) {
               const int r = __ffs(hit) - 1;
               hit &= hit - 1u;
@@ -1024,12 +1105,25 @@ __global__ void __launch_bounds__(TILE_T, C2_TILE_MINB) k_local_tile(TileArgs a)
           }
         }
         const int64_t cb = s_cbase;
+        const bool few = __popc(k8rows) <= 4;
         if (cb >= 0) {
 #pragma unroll
           for (int q = 0; q < VPT; ++q) {
-            const int jj = g0 + q * TILE_WARPS + ((C2_SNAKE && (q & 1)) ? TILE_WARPS - 1 - warp : warp);
+            const int jj = slice_of(q);
             const int vi = jj * 32 + lane;
-            if (jj < nsl) {
+            if (jj < nsl && few) {
+              // a few rows: each row's count read off the bit-planes
+              uint16_t *dst = a.hv_cnt + cb + vi;
+              int rk = 0;
+              for (unsigned rm = k8rows; rm; rm &= rm - 1u, ++rk) {
+                const int r = __ffs(rm) - 1;
+                uint32_t i = ((C[q].ones >> r) & 1u) | (((C[q].twos >> r) & 1u) << 1) | (((C[q].fours >> r) & 1u) << 2) |
+                             (((C[q].eights >> r) & 1u) << 3);
+#pragma unroll
+                for (int j = 0; j < NHI; ++j) i |= ((C[q].H[j] >> r) & 1u) << (4 + j);
+                if (vi < s) dst[(int64_t)rk * s4] = (uint16_t)i;
+              }
+            } else if (jj < nsl) {
               uint32_t A[32];
               A[0] = C[q].ones;
               A[1] = C[q].twos;
@@ -1406,7 +1500,7 @@ int local_knn(c2_ctx *ctx, const Csr &csr_in, int t, const Clusters &cl, int k, 
   // ---- tile kernel configuration
   TileKernel tk = nullptr;
   int grid = 0;
-  int32_t stg_off = 0, stg_cap = 0;
+  int32_t stg_off = 0, stg_cap = 0, scr_off = 0;
   size_t smem = 0;
   int *counters = nullptr;
   uint16_t *hv_cnt = nullptr;
@@ -1422,7 +1516,11 @@ int local_knn(c2_ctx *ctx, const Csr &csr_in, int t, const Clusters &cl, int k, 
     const size_t budget = (C2_SMEM_BUDGET ? std::min<size_t>(C2_SMEM_BUDGET, ctx->smem_optin) : ctx->smem_optin) -
                           4096;  // minus the kernel's static shared memory (~2.5 KB)
     const size_t mw = (size_t)((W + 4) & ~3);  // M: W + 1 words
-    stg_off = (int32_t)mw;
+    // split-probe scratch: TILE_WARPS x (4 + nhi) planes x 32 lanes, in M's words when W + 1 allows
+    const size_t scrw = (size_t)TILE_WARPS * (4 + (nhi <= 4 ? 4 : nhi <= 8 ? 8 : 11)) * 32;
+    const size_t scr_own = (size_t)W + 1 >= scrw ? 0 : scrw;
+    scr_off = scr_own ? (int32_t)mw : 0;
+    stg_off = (int32_t)(mw + scr_own);
     stg_cap = (int32_t)std::min<int64_t>(4096, ((int64_t)budget / 4 - stg_off) / 4);  // 16-byte groups
     if (stg_cap < 64) stg_cap = 0;
     smem = ((size_t)stg_off + (size_t)stg_cap * 4) * 4;
@@ -1453,7 +1551,7 @@ int local_knn(c2_ctx *ctx, const Csr &csr_in, int t, const Clusters &cl, int k, 
   auto launch_tiles = [&](int64_t lo, int64_t hi, int ci, int f) -> int {
     if (hi <= lo) return C2_OK;
     TileArgs ta{tiles, lo, hi, counters + ci, bcs, vperm, vsize, trec, blk_len8, blk_off8, packed, csr.psize, n, W, nwin, k,
-                fused ? out : nullptr, ctx->kstats, stg_off, stg_cap, relabel ? 1 : 0, fused ? surv : nullptr, surv_qn,
+                fused ? out : nullptr, ctx->kstats, stg_off, stg_cap, scr_off, relabel ? 1 : 0, fused ? surv : nullptr, surv_qn,
                 surv_qmax, hv_cnt, hv_cap, hv_ctr + f, hv_recs, hv_rcap, hv_ctr + C2_MAX_T + f, hv_err};
     int g = (int)std::min<int64_t>(grid, hi - lo);
     cudaEvent_t e0 = nullptr, e1 = nullptr;

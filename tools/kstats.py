@@ -19,7 +19,7 @@ k = ks.tolist()
 print(f"{name}: k_row_topk rows {k[0]} nq==0 {k[1]/max(k[0],1):.3f} mean nq {k[2]/max(k[0],1):.2f} "
       f"nq>32KS {k[3]/max(k[0],1):.4f} rescans {k[4]} round1 rows {k[6]} exact-fallback rows {k[8]}")
 print("  first-scan m histogram (bins of 20): " + " ".join(str(x) for x in k[16:32]))
-print(f"  light rows {k[71]} survivors {k[72]} (mean {k[72] / max(k[71], 1):.2f}) overflowed to k_row_topk {k[73]}")
+print(f"  light rows {k[71]} survivors {k[72]} (mean {k[72] / max(k[71], 1):.2f}) prefilter hits {k[74]} (per light row {k[74] / max(k[71], 1):.1f}) overflowed to k_row_topk {k[73]}")
 tt = sum(k[32:36]) or 1
 for i, nm in enumerate(["mixed", "33-256", "257-1024", ">1024"]):
     mt = max(k[36 + i], 1)
