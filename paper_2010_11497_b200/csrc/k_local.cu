@@ -445,6 +445,40 @@ __global__ void __launch_bounds__(256) k_sl_fill(int64_t nslices, const int32_t 
   }
 }
 
+// Plain order (multi-window runs): the items of member e in window w are the contiguous range
+// [bd[w], bd[w+1]) of its sorted row, so position p of its list is item bd[w] + p.  One warp per
+// 16-byte row t of a (slice, window) block: lane e gathers positions 8t..8t+7 of member e and the
+// warp writes the block's 512-byte row t with one coalesced uint4 store per lane (the per-list
+// form wrote 2-byte scattered stores, i.e. partial sectors).
+__global__ void __launch_bounds__(256) k_sl_fill_rows(int64_t nb, int nwin, const int32_t *__restrict__ bounds,
+                                                      const int32_t *__restrict__ items, int32_t W,
+                                                      const int32_t *__restrict__ blk_len8,
+                                                      const int32_t *__restrict__ blk_off8, uint4 *__restrict__ packed) {
+  const int lane = threadIdx.x & 31;
+  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwg = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  // warps walk the blocks' rows in order: block b, row t (the row index space is blk_off8's)
+  for (int64_t b = gw >> 3; b < nb; b += nwg >> 3) {
+    const int sub = (int)(gw & 7);
+    const int64_t sl = b / nwin;
+    const int w = (int)(b - sl * nwin);
+    const int32_t *bd = bounds + (sl * 32 + lane) * (nwin + 1);
+    const int32_t pb = bd[w], pe = bd[w + 1];
+    const int32_t lo = w * W;
+    const int32_t len8 = blk_len8[b];
+    uint4 *out = packed + (int64_t)blk_off8[b] * 32 + lane;
+    for (int t = sub; t < len8; t += 8) {
+      uint32_t h[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int32_t p = pb + 8 * t + j;
+        h[j] = p < pe ? (uint32_t)(__ldg(items + p) - lo) : (uint32_t)W;
+      }
+      out[(int64_t)t * 32] = make_uint4(h[0] | (h[1] << 16), h[2] | (h[3] << 16), h[4] | (h[5] << 16), h[6] | (h[7] << 16));
+    }
+  }
+}
+
 // ------------------------------------------------------------------ cluster-local relabeling
 // Only items held by >= 2 members of a cluster can contribute to an intersection, so every
 // cluster unit (a big cluster, or one mixed slice of small clusters) gets its own dense item
@@ -1470,9 +1504,14 @@ int local_knn(c2_ctx *ctx, const Csr &csr_in, int t, const Clusters &cl, int k, 
       packed = (uint4 *)ws_get(ctx, "packed", (size_t)tot8 * 32 * 16 + 16, &rc);
       if (rc) return rc;
       // bank-rotated order pays for its second pass only when lists are long (one window)
-      k_sl_fill<<<nblk(nslices * 32 * 32), 256, 0, st>>>(nslices, bounds, csr.items, W, nwin, blk_len8, blk_off8,
-                                                         reinterpret_cast<uint16_t *>(packed), nwin == 1 ? 1 : 0);
-      C2_LAUNCHED(ctx, "k_sl_fill");
+      if (nwin == 1) {
+        k_sl_fill<<<nblk(nslices * 32 * 32), 256, 0, st>>>(nslices, bounds, csr.items, W, nwin, blk_len8, blk_off8,
+                                                           reinterpret_cast<uint16_t *>(packed), 1);
+        C2_LAUNCHED(ctx, "k_sl_fill");
+      } else {
+        k_sl_fill_rows<<<ctx->num_sms * 16, 256, 0, st>>>(nb, nwin, bounds, csr.items, W, blk_len8, blk_off8, packed);
+        C2_LAUNCHED(ctx, "k_sl_fill_rows");
+      }
     }
   }
 

@@ -279,18 +279,60 @@ __global__ void __launch_bounds__(RT_WARPS * 32) k_row_topk(RowArgs a) {
   }
 }
 
+// One Alg. 3 step on warp-held lists: S (best first, 32*KS positions, sentinel padded) becomes the
+// first k distinct ids of S ∪ X, X = one candidate (or sentinel) per lane, by a bitonic sort of X on
+// exact keys, a bitonic merge with S reversed and an adjacent-duplicate drop (A13, A16).
+template <int KS>
+__device__ __forceinline__ void sort_merge_step(Cand (&S)[KS], Cand x, int k, c2_cand *sbuf) {
+  const int lane = threadIdx.x & 31;
+  KC q[KS];
+  q[0] = to_kc(x);
+#pragma unroll
+  for (int j = 1; j < KS; ++j) q[j] = KC{0ull, 1u << 16};
+  sort_kc<KS>(q);
+  KC mm[2 * KS];
+#pragma unroll
+  for (int j = 0; j < KS; ++j) mm[j] = (32 * j + lane < k) ? q[j] : KC{0ull, 1u << 16};
+#pragma unroll
+  for (int j = 0; j < KS; ++j) mm[KS + j] = shfl_e(to_kc(S[KS - 1 - j]), 31 - lane);
+  merge_kc<2 * KS>(mm);
+  int base = 0;
+#pragma unroll
+  for (int j = 0; j < 2 * KS; ++j) {
+    const uint32_t lo = (uint32_t)mm[j].k;
+    uint32_t prev = __shfl_up_sync(0xffffffffu, lo, 1);
+    const uint32_t prevj = j > 0 ? __shfl_sync(0xffffffffu, (uint32_t)mm[j - 1].k, 31) : 0u;
+    if (lane == 0) prev = prevj;
+    const bool keep = kc_real(mm[j]) && (j + lane == 0 || lo != prev);
+    const unsigned bal = __ballot_sync(0xffffffffu, keep);
+    const int rank = base + __popc(bal & ((1u << lane) - 1));
+    if (keep && rank < k) sbuf[rank] = kc_out(mm[j]);
+    base += __popc(bal);
+  }
+  for (int p = base + lane; p < k; p += 32) sbuf[p] = c2_cand{-1, 0, 0};
+  __syncwarp();
+#pragma unroll
+  for (int j = 0; j < KS; ++j) S[j] = (32 * j + lane < k) ? from_out(sbuf[32 * j + lane]) : sent();
+  __syncwarp();
+}
+
 // ---------------------------------------------------------------- light rows' Alg. 3 step
 // k_local_tile's phase-A epilogue left each light user's survivors -- its cluster-mates strictly
 // better than its running k-th best -- in surv[u][0..qn[u]).  One warp per user with survivors:
 // the running list S (full, best first) sits in registers (lane j holds S[32*jj + j]); survivors
-// are read 32 at a time, those still strictly better than the current k-th best are inserted one
-// by one (a duplicate id carries the same (i, U) and is skipped, A16), the k-th best refreshed
-// after each insertion.  The result is the first k distinct ids of S ∪ Q under the order (A13),
+// are read 32 at a time and those still strictly better than the current k-th best are merged in:
+// a few by insertion (a duplicate id carries the same (i, U) and is skipped, A16), more by one
+// sort-and-merge step.  The result is the first k distinct ids of S ∪ Q under the order (A13),
 // whatever the survivors' order.
+constexpr int SM_INSERT_MAX = 32;  // survivors of a chunk merged by insertion (more: sort + merge; at 6 the
+                                   // sort-and-merge step measured slower at c5: 6.6 vs 5.9 ms over 8 launches)
+
 template <int KS>
 __global__ void __launch_bounds__(256) k_surv_merge(const c2_cand *__restrict__ surv, int32_t *__restrict__ qn,
                                                     int qmax, int32_t n, int k, c2_cand *__restrict__ run) {
+  __shared__ c2_cand s_buf[8][32 * KS];
   const int lane = threadIdx.x & 31;
+  c2_cand *sbuf = s_buf[threadIdx.x >> 5];
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwg = ((int64_t)gridDim.x * blockDim.x) >> 5;
   for (int64_t ub = gw * 32; ub < n; ub += nwg * 32) {
@@ -311,8 +353,16 @@ __global__ void __launch_bounds__(256) k_surv_merge(const c2_cand *__restrict__ 
       const c2_cand *Q = surv + u * qmax;
       bool changed = false;
       for (int c0 = 0; c0 < m; c0 += 32) {
-        const Cand x = c0 + lane < m ? from_out(Q[c0 + lane]) : sent();
-        unsigned bal = __ballot_sync(0xffffffffu, is_real(x) && better_c(x, tau));
+        Cand x = c0 + lane < m ? from_out(Q[c0 + lane]) : sent();
+        const bool ok = is_real(x) && better_c(x, tau);
+        unsigned bal = __ballot_sync(0xffffffffu, ok);
+        if (!bal) continue;
+        changed = true;
+        if (__popc(bal) > SM_INSERT_MAX) {
+          sort_merge_step<KS>(S, ok ? x : sent(), k, sbuf);
+          tau = warp_get<KS>(S, k - 1);
+          continue;
+        }
         while (bal) {
           const int l = __ffs(bal) - 1;
           bal &= bal - 1u;
@@ -324,7 +374,6 @@ __global__ void __launch_bounds__(256) k_surv_merge(const c2_cand *__restrict__ 
           if (__any_sync(0xffffffffu, dup)) continue;
           warp_insert<KS>(S, y);
           tau = warp_get<KS>(S, k - 1);
-          changed = true;
         }
       }
       if (changed) {
