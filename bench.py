@@ -144,7 +144,7 @@ def roofline(C, st, tile_ms_step, n_tile, clock, ms_step):
         note = f"ALU-pipe warp instructions per step from {ncu['source']}"
         if ncu.get("dram_bytes_per_launch") is not None:
             traffic = ncu["dram_bytes_per_launch"]
-    out = {"kernel": "k_local_tile (K7 local Jaccard + K8 top-k)", "bound": "alu",
+    out = {"kernel": "k_local_tile (K7 local Jaccard: phase A + light-row epilogue)", "bound": "alu",
            "achieved": achieved, "peak": peak, "unit": "T lane-ops/s (ALU pipe)",
            "frac": (achieved / peak) if achieved else None, "traffic": traffic,
            "peak_source": f"{src} x 148 SMs x {mhz:.0f} MHz (median SM clock during the timed region)",
