@@ -1058,31 +1058,28 @@ __global__ void __launch_bounds__(TILE_T, C2_TILE_MINB) k_local_tile(TileArgs a)
             idq[q] = vi < s ? __ldg(vp + vi) : -1;
             psq[q] = vi < s ? (uint32_t)__ldg(a.vsize + B.vp_off + vi) : 0u;
           }
+          // pass 1 (all slices of the warp, independent chains): the prefilter hit masks
+          uint32_t hitq[VPT];
 #pragma unroll
           for (int q = 0; q < VPT; ++q) {
+            hitq[q] = 0u;
             const int jj = slice_of(q);
             if (jj >= nsl) continue;  // (warp-uniform: all lanes of a warp share the slice jj)
-            const int32_t idv = idq[q];
-            const uint32_t psv = idv >= 0 ? psq[q] : 0xFFFFFFFFu;
+            const uint32_t psv = idq[q] >= 0 ? psq[q] : 0xFFFFFFFFu;
             // slice bound: every member has |P_v| >= psmin, so a member passes row r only if
             // i (UT + iT) >= iT (|P_r| + psmin), i.e. i >= imin_r; the bit-planes of the 32 imin_r
             const uint32_t psmin = __reduce_min_sync(0xffffffffu, psv);
             uint32_t imin = 0xFFFFFFFFu;
             if (lr && psmin != 0xFFFFFFFFu) imin = (Rr.y + Rr.z * psmin + Rr.x - 1u) / Rr.x;
             const unsigned pm = __ballot_sync(0xffffffffu, imin < (1u << NPL));
-            if (!pm) continue;
-            uint32_t pl[NPL], gt = 0u, eq = 0xFFFFFFFFu;
-            pl[0] = C[q].ones;
-            pl[1] = C[q].twos;
-            pl[2] = C[q].fours;
-            pl[3] = C[q].eights;
-#pragma unroll
-            for (int i = 0; i < NHI; ++i) pl[4 + i] = C[q].H[i];
+            uint32_t gt = 0u, eq = 0xFFFFFFFFu;
 #pragma unroll
             for (int j = NPL - 1; j >= 0; --j) {
+              const uint32_t plj = j == 0 ? C[q].ones : j == 1 ? C[q].twos : j == 2 ? C[q].fours
+                                                         : j == 3 ? C[q].eights : C[q].H[j > 3 ? j - 4 : 0];
               const uint32_t im = __ballot_sync(0xffffffffu, (imin >> j) & 1u);
-              gt |= eq & pl[j] & ~im;
-              eq &= ~(pl[j] ^ im);
+              gt |= eq & plj & ~im;
+              eq &= ~(plj ^ im);
             }
             uint32_t hit = (gt | eq) & pm;
             if (B.slot) {
@@ -1090,17 +1087,26 @@ __global__ void __launch_bounds__(TILE_T, C2_TILE_MINB) k_local_tile(TileArgs a)
               hit &= (B.slot >= 32 ? 0xFFFFFFFFu : ((1u << B.slot) - 1u)) << lo;
             }
             if (jj == T.j) hit &= ~(1u << lane);  // the row itself
-            if (idv < 0) hit = 0u;
+            if (idq[q] < 0) hit = 0u;
+            hitq[q] = hit;
             if (a.kstats) {
               const int nh = __reduce_add_sync(0xffffffffu, __popc(hit));
               if (lane == 0) atomicAdd(&a.kstats[74], (unsigned long long)nh);
             }
+          }
+          // pass 2: the exact test for every hit, survivors to global memory
+#pragma unroll
+          for (int q = 0; q < VPT; ++q) {
+            uint32_t hit = hitq[q];
+            const int32_t idv = idq[q];
+            const uint32_t psv = psq[q];
             while (hit) {
               const int r = __ffs(hit) - 1;
               hit &= hit - 1u;
-              uint32_t i = 0u;
+              uint32_t i = ((C[q].ones >> r) & 1u) | (((C[q].twos >> r) & 1u) << 1) | (((C[q].fours >> r) & 1u) << 2) |
+                           (((C[q].eights >> r) & 1u) << 3);
 #pragma unroll
-              for (int j = 0; j < NPL; ++j) i |= ((pl[j] >> r) & 1u) << j;
+              for (int j = 0; j < NHI; ++j) i |= ((C[q].H[j] >> r) & 1u) << (4 + j);
               const uint4 R4 = s_ref[r];
               if (passes(i, psv, idv, Ref{R4.x, R4.y, R4.z, R4.w})) {
                 const int pq = atomicAdd(&s_qn[r], 1);

@@ -113,19 +113,28 @@ __global__ void __launch_bounds__(RT_WARPS * 32) k_row_topk(RowArgs a) {
 #pragma unroll
       for (int j = 0; j < R1; ++j) t[j] = sent();
       Ref wr = make_ref(sent(), prr, false);
-      for (int v = lane; v < s; v += 32) {
-        if (v == selfr) continue;
-        const uint32_t iv = cr[v], pv = (uint32_t)vps[v];
-        const int32_t dv = vid[v];
-        if (passes(iv, pv, dv, wr)) {
-          const Cand x{iv | ((prr + pv - iv) << 16), dv};
+      for (int base = 0; base < s; base += 128) {  // four candidates per lane in flight
+        uint32_t iv[4], pv[4];
+        int32_t dv[4];
 #pragma unroll
-          for (int j = R1 - 1; j > 0; --j) {
-            if (better_c(x, t[j - 1])) t[j] = t[j - 1];
-            else if (better_c(x, t[j])) t[j] = x;
+        for (int e = 0; e < 4; ++e) {
+          const int v = base + 32 * e + lane;
+          iv[e] = v < s ? cr[v] : 0u;
+          pv[e] = v < s ? (uint32_t)vps[v] : 0u;
+          dv[e] = v < s && v != selfr ? vid[v] : INT32_MAX;
+        }
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          if (dv[e] != INT32_MAX && passes(iv[e], pv[e], dv[e], wr)) {
+            const Cand x{iv[e] | ((prr + pv[e] - iv[e]) << 16), dv[e]};
+#pragma unroll
+            for (int j = R1 - 1; j > 0; --j) {
+              if (better_c(x, t[j - 1])) t[j] = t[j - 1];
+              else if (better_c(x, t[j])) t[j] = x;
+            }
+            if (better_c(x, t[0])) t[0] = x;
+            wr = make_ref(t[R1 - 1], prr, false);
           }
-          if (better_c(x, t[0])) t[0] = x;
-          wr = make_ref(t[R1 - 1], prr, false);
         }
       }
       KC e[R1];
