@@ -703,7 +703,7 @@ struct TileArgs {
   int k;
   const c2_cand *seed;  // fused: running lists before this function [n][k]; else nullptr
   unsigned long long *kstats;  // C2_OPT_KSTATS counters or nullptr
-  int32_t stg_off, stg_cap;  // staging buffer (word offset, capacity in 16-byte groups; 0: off)
+  int32_t stg_off, stg_cap;  // two staging buffers (word offset, capacity of each in 16-byte groups; 0: off)
   int32_t scr_off;      // split-probe scratch (word offset; 0: M's own words)
   int relabel;          // 1: items are unit-local ids, the tile's window is [0, B.kc) (nwin == 1)
   c2_cand *surv;        // fused light-row path: survivors [n][qmax] (nullptr: no light rows)
@@ -784,7 +784,7 @@ __global__ void __launch_bounds__(TILE_T, C2_TILE_MINB) k_local_tile(TileArgs a)
   __shared__ int64_t s_cbase, s_rbase;  // this tile's first count entry / record for k_row_topk
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   for (int i = tid; i < a.W + 1; i += TILE_T) M[i] = 0;
-  uint4 *stg = reinterpret_cast<uint4 *>(dyn + a.stg_off);  // staged rows' blocks of the next tile
+  uint4 *stg0 = reinterpret_cast<uint4 *>(dyn + a.stg_off);  // staged rows' blocks, one buffer per slot
   const int nwin = a.nwin;
   const int kk = a.k;
   // next-tile descriptors in two halves (TMA bulk copies completing on mbarriers): fetch_issue
@@ -849,7 +849,7 @@ __global__ void __launch_bounds__(TILE_T, C2_TILE_MINB) k_local_tile(TileArgs a)
     }
     __syncwarp();
     if (staged && lane < nwin && bl > 0)
-      bulk_g2s(stg + (incl - bl * 32), a.packed + (int64_t)bo * 32, (uint32_t)bl * 512u, &mb_stg[b]);
+      bulk_g2s(stg0 + b * a.stg_cap + (incl - bl * 32), a.packed + (int64_t)bo * 32, (uint32_t)bl * 512u, &mb_stg[b]);
   };
   if (tid == 0) fetch_issue(0);
   if (warp == 0) fetch_finish(0);
@@ -868,6 +868,7 @@ __global__ void __launch_bounds__(TILE_T, C2_TILE_MINB) k_local_tile(TileArgs a)
     __syncthreads();
     const int64_t it = s_it[cur];
     if (it >= a.hi) break;
+    uint4 *stg = stg0 + cur * a.stg_cap;
     if (tid == 0) fetch_issue(cur ^ 1);  // next tile's record: claimed and requested now
     const long long ck0 = a.kstats ? clock64() : 0;
     long long ckA = 0, ckE = 0;
@@ -933,6 +934,8 @@ __global__ void __launch_bounds__(TILE_T, C2_TILE_MINB) k_local_tile(TileArgs a)
             if (xs[q] < W) atomicOr(&M[xs[q]], bit);
         }
         __syncthreads();
+        // the next tile's row blocks go to the other staging buffer as soon as its record is in
+        if (g0 == 0 && w == 0 && warp == TILE_WARPS - 1) fetch_finish(cur ^ 1);
         // ---- probe: each warp streams VPT slices of v lists, two 16-byte loads per step with
         //      the next two steps in flight (odd tails padded with the sentinel item W, M[W] = 0)
         const long long ckpb = a.kstats ? clock64() : 0;
@@ -1038,8 +1041,6 @@ __global__ void __launch_bounds__(TILE_T, C2_TILE_MINB) k_local_tile(TileArgs a)
           }
         }
       }
-      // the staging buffer is dead now: the next tile's row blocks may be copied in
-      if (g0 + VPT * TILE_WARPS >= nsl && warp == TILE_WARPS - 1) fetch_finish(cur ^ 1);
       if (a.kstats) ckA = clock64();
       // ---- light rows: bit-sliced prefilter on the counters (count >= imin_r for all 32 rows at
       //      once), the exact test for the few that pass, survivors to global memory (one g0 group)
@@ -1566,9 +1567,9 @@ int local_knn(c2_ctx *ctx, const Csr &csr_in, int t, const Clusters &cl, int k, 
     const size_t scr_own = (size_t)W + 1 >= scrw ? 0 : scrw;
     scr_off = scr_own ? (int32_t)mw : 0;
     stg_off = (int32_t)(mw + scr_own);
-    stg_cap = (int32_t)std::min<int64_t>(4096, ((int64_t)budget / 4 - stg_off) / 4);  // 16-byte groups
+    stg_cap = (int32_t)std::min<int64_t>(2048, ((int64_t)budget / 4 - stg_off) / 8);  // 16-byte groups, each
     if (stg_cap < 64) stg_cap = 0;
-    smem = ((size_t)stg_off + (size_t)stg_cap * 4) * 4;
+    smem = ((size_t)stg_off + (size_t)stg_cap * 8) * 4;
     tk = pick_tile(nhi, vpt);
     C2_CUDA(ctx, cudaFuncSetAttribute(tk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int occ = 0;
