@@ -107,6 +107,10 @@ enum {
                               hash function; their merged lists equal the single run's, A16) */
   C2_OPT_LOCAL_SOLVER = 8, /* Step 2's per-cluster solver: C2_SOLVER_BRUTE (default, every cluster, A12) or
                               C2_SOLVER_HYBRID (Alg. 2: brute force if |C| < 5k^2, else Hyrec) */
+  C2_OPT_GF_TENSOR = 10,   /* nonzero: in GoldFinger mode the intersections of clusters of more than 32
+                              users are 0/1 contractions of the 1024-bit fingerprints on the tensor
+                              cores (tcgen05.mma kind::i8, k_gf_mma); 0 (default, measured faster at c4):
+                              the bit-sliced list kernel.  Results are identical either way. */
   C2_OPT_SURVIVORS = 9     /* c2_build only, 0..4096 (default 256): candidate slots per user of the
                               light-row path (a row whose running list is full is screened in the
                               local kernel's epilogue and merged by a separate kernel; a row with more

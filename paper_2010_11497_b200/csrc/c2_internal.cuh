@@ -33,6 +33,7 @@ struct c2_ctx {
   int solver = 0;       // C2_OPT_LOCAL_SOLVER: 0 brute force everywhere (A12), 1 Alg. 2 hybrid (Hyrec)
   uint64_t hyrec_seed = 0;  // the call's seed (Hyrec's random initial graphs)   // C2_OPT_CLUSTERING: 0 FastRandomHash (Step 1 of C^2), 1 MinHash (N3 variant)
   int surv_qmax = 256;  // C2_OPT_SURVIVORS: light-row survivor slots per user (0: off)
+  bool gf_tensor = false;  // C2_OPT_GF_TENSOR: GoldFinger big clusters on the tensor cores (k_gf_mma; measured slower, off)
   bool relabel = true;  // C2_OPT_RELABEL  (C2_OPT_KSTATS: kstats = dev [80] K7/K8 counters)
   c2_stats stats{};
   // device workspace: name -> (ptr, bytes); grow-only
@@ -83,6 +84,7 @@ struct Csr {
   int32_t max_item;     // filled by validate()
   int32_t max_len;
   const int32_t *psize; // dev [n], |P_u|
+  const uint32_t *gf_words = nullptr;  // GoldFinger mode: fingerprints [n][32] (psize = popcounts)
 };
 // K0: CSR rules + |P_u| + max item / max row length (one host sync).
 int validate_csr(c2_ctx *ctx, Csr *csr);

@@ -32,6 +32,7 @@
 #include "c2_internal.cuh"
 #include "cand.cuh"
 #include "k_rows.cuh"
+#include "k_gf_mma.cuh"
 
 #ifndef C2_LIGHT
 #define C2_LIGHT 1  // 1: light rows (full running list) filtered in the phase-A epilogue, merged by k_surv_merge
@@ -51,16 +52,6 @@
 
 namespace c2 {
 
-// A cluster processed by the tile kernel: either one big cluster (slot == 0; members in
-// vperm[vp_off .. vp_off + s)) or one "mixed" 32-row slice packing 32/slot small clusters of
-// 2..32 users, each in its own aligned group of `slot` positions (empty positions are -1).
-struct BigC {
-  int32_t f, s, vp_off, sl_off, slot;
-  int32_t kc;  // relabeled units: size of the unit's local item universe
-};
-struct Tile {
-  int32_t bc, j;
-};
 
 // cp.async (sm_80+ async global->shared copies; completion by cp.async.wait_all)
 __device__ __forceinline__ void cp_async8(void *smem, const void *gmem) {
@@ -1407,6 +1398,7 @@ int local_knn(c2_ctx *ctx, const Csr &csr_in, int t, const Clusters &cl, int k, 
   int32_t W = (int32_t)((m + nwin - 1) / nwin);
 
   unsigned long long *hv_need = nullptr;
+  int64_t nv_big_all = 0;  // members of all big clusters (all functions)
   if (nslices > 0) {
     bcs = (BigC *)ws_get(ctx, "bc", (size_t)ncl * sizeof(BigC), &rc);
     if (rc) return rc;
@@ -1426,6 +1418,7 @@ int local_knn(c2_ctx *ctx, const Csr &csr_in, int t, const Clusters &cl, int k, 
       C2_CUDA(ctx, cudaMemcpyAsync(&h1, vp_scan + nbig, 4, cudaMemcpyDeviceToHost, st));
       C2_TRY(stream_sync(ctx, "big cluster sizes"));
       nv_big = h1;
+      nv_big_all = nv_big;
     }
     vperm = (int32_t *)ws_get(ctx, "vperm", (size_t)(nv_big + nmix * 32 + 1) * 4 * 2, &rc);
     if (rc) return rc;
@@ -1554,6 +1547,12 @@ int local_knn(c2_ctx *ctx, const Csr &csr_in, int t, const Clusters &cl, int k, 
   unsigned long long *hv_ctr = nullptr;
   int *hv_err = nullptr;
   int64_t hv_cap = 0, hv_rcap = 0;
+  bool gfm = false;
+  int64_t *gf_wl = nullptr, *gf_cb = nullptr, *gf_sum = nullptr, *gf_rng = nullptr;
+  uint8_t *gf_bytes = nullptr;
+  int32_t *gf_witem = nullptr;
+  int64_t gf_icap = 0;
+  int64_t gf_bc[C2_MAX_T + 1] = {0};
   if (nslices > 0) {
     int nbits = bits_for((int64_t)csr.max_len + 1);
     int nhi = std::max(nbits - 4, 1);
@@ -1584,7 +1583,9 @@ int local_knn(c2_ctx *ctx, const Csr &csr_in, int t, const Clusters &cl, int k, 
       hv_cap = std::max<int64_t>(hv_cap, (int64_t)ctx->h_small[256 + f]);
       hv_rcap = std::max<int64_t>(hv_rcap, (int64_t)ctx->h_small[256 + t + f]);
     }
-    hv_cnt = (uint16_t *)ws_get(ctx, "hv_cnt", (size_t)hv_cap * 2 + 16, &rc);
+    // GoldFinger on the tensor cores: the big clusters' count rows get a region of their own
+    gfm = csr.gf_words != nullptr && ctx->gf_tensor && nbig > 0;
+    hv_cnt = (uint16_t *)ws_get(ctx, "hv_cnt", (size_t)hv_cap * (gfm ? 4 : 2) + 16, &rc);
     if (rc) return rc;
     hv_recs = (RowRec *)ws_get(ctx, "hv_recs", (size_t)(hv_rcap + 1) * sizeof(RowRec), &rc);
     if (rc) return rc;
@@ -1592,6 +1593,26 @@ int local_knn(c2_ctx *ctx, const Csr &csr_in, int t, const Clusters &cl, int k, 
     if (rc) return rc;
     hv_err = (int *)(hv_ctr + 2 * C2_MAX_T + 1);
     C2_CUDA(ctx, cudaMemsetAsync(hv_ctr, 0, (size_t)(2 * C2_MAX_T + 2) * 8, st));
+    if (gfm) {
+      // per function: its big clusters [gf_bc[f], gf_bc[f+1]) (bcs is ordered by function), work-item and
+      // count-row prefixes over them
+      for (int f = 0; f < t; ++f) gf_bc[f + 1] = gf_bc[f] + hfc[f * WLC + 7];
+      gf_wl = (int64_t *)ws_get(ctx, "gf_wl", (size_t)(2 * nbig + 2 * C2_MAX_T + 2 + C2_MAX_T + 1) * 8, &rc);
+      if (rc) return rc;
+      gf_cb = gf_wl + nbig;
+      gf_sum = gf_cb + nbig;
+      gf_rng = gf_sum + 2 * C2_MAX_T + 2;
+      for (int f = 0; f <= t; ++f) ctx->h_small[400 + f] = gf_bc[f];
+      C2_CUDA(ctx, cudaMemcpyAsync(gf_rng, ctx->h_small + 400, (size_t)(t + 1) * 8, cudaMemcpyHostToDevice, st));
+      // work items per function <= sum over its clusters of (s/128 + 1)^2 <= nbig + 2 rows/128 + maxs rows/128^2
+      gf_icap = nbig + 2 * (nv_big_all / 128 + 1) + (int64_t)maxs * (nv_big_all / 16384 + 1) + 16;
+      gf_witem = (int32_t *)ws_get(ctx, "gf_witem", (size_t)t * gf_icap * 4, &rc);
+      if (rc) return rc;
+      C2_TRY(gf_prefix(ctx, bcs, gf_rng, t, nbig, gf_wl, gf_cb, gf_sum, gf_witem, gf_icap));
+      gf_bytes = (uint8_t *)ws_get(ctx, "gf_bytes", (size_t)n * 1024, &rc);
+      if (rc) return rc;
+      C2_TRY(gf_expand(ctx, csr.gf_words, n, gf_bytes));
+    }
   }
   // tiles [lo, hi) of function f: counts -> light rows' survivors (c2_build) + count rows for k_row_topk
   auto launch_tiles = [&](int64_t lo, int64_t hi, int ci, int f) -> int {
@@ -1643,7 +1664,14 @@ int local_knn(c2_ctx *ctx, const Csr &csr_in, int t, const Clusters &cl, int k, 
   int64_t blo = 0;
   for (int f = 0; f < t; ++f) {
     const int64_t bhi = blo + hfc[f * WLC + 0];
-    C2_TRY(launch_tiles(blo, bhi, 2 * f, f));
+    if (gfm) {
+      GfArgs ga{bcs, gf_bc[f], gf_bc[f + 1], gf_wl, gf_cb, gf_sum + 2 * f, gf_witem + (int64_t)f * gf_icap, vperm, vsize, gf_bytes, n, k,
+                fused ? out : nullptr, fused ? surv : nullptr, surv_qn, surv_qmax, hv_cnt, hv_cap, hv_recs,
+                hv_ctr + C2_MAX_T + f, hv_rcap, hv_err};
+      C2_TRY(launch_gf_mma(ctx, ga));
+    } else {
+      C2_TRY(launch_tiles(blo, bhi, 2 * f, f));
+    }
     C2_TRY(launch_tiles(nbigtiles + mix_lo[f], nbigtiles + mix_lo[f + 1], 2 * f + 1, f));
     C2_TRY(launch_rows(f));
     if (surv) C2_TRY(launch_surv_merge(ctx, surv, surv_qn, surv_qmax, n, k, out));  // light rows' Alg. 3 step

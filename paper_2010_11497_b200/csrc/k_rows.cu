@@ -348,7 +348,8 @@ __global__ void __launch_bounds__(256) k_surv_merge(const c2_cand *__restrict__ 
     const int64_t uu = ub + lane;
     const int c = uu < n ? qn[uu] : 0;
     if (c > 0) qn[uu] = 0;
-    unsigned mask = __ballot_sync(0xffffffffu, c > 0);
+    // (more than qmax: the row was handed to k_row_topk by its producer)
+    unsigned mask = __ballot_sync(0xffffffffu, c > 0 && c <= qmax);
     while (mask) {
       const int j = __ffs(mask) - 1;
       mask &= mask - 1u;

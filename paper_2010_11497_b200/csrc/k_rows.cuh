@@ -4,6 +4,17 @@
 
 namespace c2 {
 
+// A cluster processed by the tile kernel: either one big cluster (slot == 0; members in
+// vperm[vp_off .. vp_off + s)) or one "mixed" 32-row slice packing 32/slot small clusters of
+// 2..32 users, each in its own aligned group of `slot` positions (empty positions are -1).
+struct BigC {
+  int32_t f, s, vp_off, sl_off, slot;
+  int32_t kc;  // relabeled units: size of the unit's local item universe
+};
+struct Tile {
+  int32_t bc, j;
+};
+
 // One row handed from a tile to k_row_topk: user u (|P_u| = pr) of a cluster whose s members are
 // vperm[vp_off ..) (sizes vsize[vp_off ..)); its counts |P_u ∩ P_v| are cnt[cnt_off + v].  selfr:
 // u's own member position.  Mixed slices: candidates are the members of positions

@@ -347,6 +347,7 @@ int gf_encode(c2_ctx *ctx, const Csr &csr, const HashParams *hp, Csr *gf) {
   gf->nnz = total;
   gf->psize = pc;
   gf->max_item = 1023;
+  gf->gf_words = words;
   gf->max_len = csr.max_len < 1024 ? csr.max_len : 1024;
   return C2_OK;
 }

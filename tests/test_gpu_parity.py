@@ -262,10 +262,16 @@ def test_build_configs(ctx, cfg):
     check_build(ctx, offs, items, C.t, C.b, C.N, C.k, C.hash_seed)
 
 
-def test_build_c4_goldfinger(ctx):
+@pytest.mark.parametrize("tensor", [0, 1])
+def test_build_c4_goldfinger(ctx, tensor):
+    """c4 in GoldFinger mode, big clusters on the bit-sliced list kernel or the tensor cores."""
     C = synth.config("c4")
     offs, items = synth.generate("c4")
-    check_build(ctx, offs, items, C.t, C.b, C.N, C.k, C.hash_seed, mode=1)
+    ctx.set_option(c2.OPT_GF_TENSOR, tensor)
+    try:
+        check_build(ctx, offs, items, C.t, C.b, C.N, C.k, C.hash_seed, mode=1)
+    finally:
+        ctx.set_option(c2.OPT_GF_TENSOR, 0)
 
 
 def test_build_b1_exact_knn(ctx):
@@ -465,6 +471,27 @@ def test_build_random_survivor_slots(ctx, seed, qmax):
         check_build(ctx, offs, items, max(t, 3), b, N, k, hs, mode=seed % 2)
     finally:
         ctx.set_option(c2.OPT_SURVIVORS, 256)
+
+
+@pytest.mark.parametrize("tensor", [1, 0])
+@pytest.mark.parametrize("n,N,k,lo,hi", [(3000, 700, 30, 20, 300), (1500, 1500, 64, 5, 120), (600, 150, 7, 1, 40)])
+def test_goldfinger_tensor_cores(ctx, tensor, n, N, k, lo, hi):
+    """GoldFinger mode: big clusters' intersections as 0/1 fingerprint contractions on the tensor
+    cores (k_gf_mma: 128 x 128 blocks, clusters spanning several row and member blocks) or the
+    bit-sliced list kernel -- both bytewise equal to the oracle (c2_build and c2_local_knn)."""
+    rng = np.random.default_rng(n + N + k)
+    offs, items = synth.random_instance(rng, n, 5000, lo, hi, zipf=0.9)
+    ctx.set_option(c2.OPT_GF_TENSOR, tensor)
+    try:
+        check_build(ctx, offs, items, 3, 2, N, k, 11, mode=1)
+        o_cl = oracle.cluster(offs, items, oracle.hash_table(11, 3, 2, mval(items)), N)
+        cl = {key: dev(o_cl[key]) for key in ("offsets", "members", "cluster_of")}
+        cl["n_clusters"] = o_cl["n_clusters"].tolist()
+        g = cand_np(c2.local_knn(dev(offs), dev(items), cl, k, 1, 11, ctx=ctx))
+        o = oracle.local_knn(offs, items, o_cl, k, 1, oracle.gf_table(11, mval(items)))
+        assert np.array_equal(g, o)
+    finally:
+        ctx.set_option(c2.OPT_GF_TENSOR, 0)
 
 
 @pytest.mark.parametrize("k,n,N", [(50, 2600, 2600), (64, 3000, 1800), (33, 2300, 2300)])

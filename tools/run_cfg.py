@@ -12,6 +12,8 @@ C = synth.config(name)
 offs, items = synth.generate(name)
 d_o, d_i = torch.from_numpy(offs).cuda(), torch.from_numpy(items).cuda()
 ctx = c2.Context(0)
+if os.environ.get("C2_GF_TENSOR"):  # GoldFinger big clusters on the tensor cores (k_gf_mma)
+    ctx.set_option(c2.OPT_GF_TENSOR, int(os.environ["C2_GF_TENSOR"]))
 for _ in range(reps):
     c2.build(d_o, d_i, k=C.k, t=C.t, b=C.b, N=C.N, seed=C.hash_seed, sim_mode=mode, ctx=ctx)
 torch.cuda.synchronize()
