@@ -344,17 +344,14 @@ __global__ void __launch_bounds__(256) k_surv_merge(const c2_cand *__restrict__ 
   c2_cand *sbuf = s_buf[threadIdx.x >> 5];
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwg = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t ub = gw * 32; ub < n; ub += nwg * 32) {
-    const int64_t uu = ub + lane;
-    const int c = uu < n ? qn[uu] : 0;
-    if (c > 0) qn[uu] = 0;
-    // (more than qmax: the row was handed to k_row_topk by its producer)
-    unsigned mask = __ballot_sync(0xffffffffu, c > 0 && c <= qmax);
-    while (mask) {
-      const int j = __ffs(mask) - 1;
-      mask &= mask - 1u;
-      const int64_t u = ub + j;
-      const int m = __shfl_sync(0xffffffffu, c, j);
+  // one user per warp and iteration (small configs: every user with survivors gets its own warp)
+  for (int64_t u = gw; u < n; u += nwg) {
+    const int m = qn[u];
+    if (m <= 0) continue;
+    __syncwarp();
+    if (lane == 0) qn[u] = 0;
+    if (m > qmax) continue;  // the row was handed to k_row_topk by its producer
+    {
       c2_cand *Rw = run + u * k;
       Cand S[KS];
 #pragma unroll
