@@ -60,7 +60,7 @@ def build(force: bool = False, verbose: bool = False, out: str | None = None, de
         for _, err in res:
             sys.stderr.write(err)
     tmp = lib + f".tmp{os.getpid()}"
-    cmd = [NVCC, *ARCH, "-shared", "-o", tmp] + [o for o, _ in res] + ["-Xcompiler", "-fPIC"]
+    cmd = [NVCC, *ARCH, "-shared", "-o", tmp] + [o for o, _ in res] + ["-Xcompiler", "-fPIC", "-ldl"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stderr}")

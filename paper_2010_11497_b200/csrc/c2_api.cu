@@ -81,15 +81,22 @@ int build_device(c2_ctx *ctx, const int32_t *offs, const int32_t *items, int32_t
                  int32_t k, int32_t sim_mode, uint64_t seed, int32_t *nbr, uint16_t *inter, uint16_t *uni,
                  float *sim) {
   cudaStream_t st = ctx->stream;
+  C2Range r_build("c2_build");
   if (ctx->timing) cudaEventRecord(ctx->ev[6], st);
   Csr csr{offs, items, n, -1, 0, 0, nullptr};
-  C2_TRY(validate_csr(ctx, &csr));
+  {
+    C2Range r("validate");
+    C2_TRY(validate_csr(ctx, &csr));
+  }
   HashParams hp;
   make_hash_params(seed, t, &hp, ctx->func_offset);
   Clusters cl;
   C2_TRY(cluster_buffers(ctx, t, n, &cl));
-  if (ctx->clustering == 1) C2_TRY(minhash_clusters(ctx, csr, t, N, &hp, &cl));
-  else C2_TRY(fastrandomhash(ctx, csr, t, b, N, &hp, nullptr, 0, &cl));
+  {
+    C2Range r("step1 clustering (FastRandomHash / MinHash)");
+    if (ctx->clustering == 1) C2_TRY(minhash_clusters(ctx, csr, t, N, &hp, &cl));
+    else C2_TRY(fastrandomhash(ctx, csr, t, b, N, &hp, nullptr, 0, &cl));
+  }
   Csr sims = csr;
   if (sim_mode == C2_SIM_GF1024) C2_TRY(gf_encode(ctx, csr, &hp, &sims));
   ctx->hyrec_seed = seed;
@@ -99,8 +106,12 @@ int build_device(c2_ctx *ctx, const int32_t *offs, const int32_t *items, int32_t
   c2_cand *run = (c2_cand *)ws_get(ctx, "runlist", (size_t)n * k * sizeof(c2_cand), &rc);
   if (rc) return rc;
   c2_cand *fin = nullptr;
-  C2_TRY(local_knn(ctx, sims, t, cl, k, run, true, &fin));
+  {
+    C2Range r("step2+3 local top-k and Alg. 3 merge");
+    C2_TRY(local_knn(ctx, sims, t, cl, k, run, true, &fin));
+  }
   if (ctx->timing) cudaEventRecord(ctx->ev[4], st);
+  C2Range r_out("copy-out");
   C2_TRY(copyout(ctx, n, k, fin, nbr, inter, uni, sim));
   if (ctx->timing) cudaEventRecord(ctx->ev[5], st);
   return C2_OK;

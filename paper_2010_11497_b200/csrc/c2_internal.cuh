@@ -9,7 +9,15 @@
 #include <vector>
 #include <string>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "../../include/c2.h"
+
+// NVTX range for the lifetime of a scope (phases of a build, for nsys/ncu timelines)
+struct C2Range {
+  explicit C2Range(const char *name) { nvtxRangePushA(name); }
+  ~C2Range() { nvtxRangePop(); }
+};
 
 #define C2_MAX_T 64
 #define C2_MAX_K 64

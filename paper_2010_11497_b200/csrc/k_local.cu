@@ -1663,6 +1663,7 @@ int local_knn(c2_ctx *ctx, const Csr &csr_in, int t, const Clusters &cl, int k, 
   // c2_local_knn: the same launches write each function's lists cand[f].
   int64_t blo = 0;
   for (int f = 0; f < t; ++f) {
+    C2Range rf("hash function (tiles, row top-k, light-row merge)");
     const int64_t bhi = blo + hfc[f * WLC + 0];
     if (gfm) {
       GfArgs ga{bcs, gf_bc[f], gf_bc[f + 1], gf_wl, gf_cb, gf_sum + 2 * f, gf_witem + (int64_t)f * gf_icap, vperm, vsize, gf_bytes, n, k,
