@@ -20,12 +20,15 @@ namespace c2 {
 // Alg. 3 list in place (c2_build).  Exactness: a candidate is queued only if it is not
 // worse than a valid lower bound of the k-th best (the running k-th best, or the k-th best of any
 // k distinct candidates); the queue is then sorted on exact keys (cand.cuh).
+#ifndef C2_R1MUL
+#define C2_R1MUL 2  // round 1 keeps C2_R1MUL * KS best candidates per lane
+#endif
 constexpr int RT_WARPS = 8;
 constexpr int RT_QCAP = 256;  // survivor queue per warp (>= 64 * KS)
 
 template <int KS>
 __global__ void __launch_bounds__(RT_WARPS * 32) k_row_topk(RowArgs a) {
-  constexpr int R1 = 2 * KS;
+  constexpr int R1 = C2_R1MUL * KS;
   __shared__ __align__(16) Cand s_q[RT_WARPS][RT_QCAP];
   __shared__ __align__(16) c2_cand s_run[RT_WARPS][C2_MAX_K];
   __shared__ int s_wq[RT_WARPS];
@@ -253,10 +256,11 @@ __global__ void __launch_bounds__(RT_WARPS * 32) k_row_topk(RowArgs a) {
 #pragma unroll
       for (int j = 0; j < KS; ++j) L[j] = to_kc(Lc[j]);
     }
-    if (!a.seed) {
+    if (!a.seed || run[0].id < 0) {  // no running list (c2_local_knn, or a row's first cluster): L is the result
 #pragma unroll
       for (int j = 0; j < KS; ++j)
         if (32 * j + lane < kk) dst[32 * j + lane] = kc_out(L[j]);
+      __syncwarp();
       continue;
     }
     // merge with the running list S (best first): bitonic sequence L(first k) ++ reverse(S)
