@@ -111,6 +111,10 @@ enum {
                               users are 0/1 contractions of the 1024-bit fingerprints on the tensor
                               cores (tcgen05.mma kind::i8, k_gf_mma); 0 (default, measured faster at c4):
                               the bit-sliced list kernel.  Results are identical either way. */
+  C2_OPT_SPLIT_DEVICE = 11, /* nonzero (default): the recursive split runs as ONE cooperative
+                              kernel looping over the levels on the device (no host synchronisation
+                              per level) whenever its histogram bound (t*n/(N+1) * b bins) is at most
+                              2^25; 0: one host-driven pass per level.  Results are identical. */
   C2_OPT_SURVIVORS = 9     /* c2_build only, 0..4096 (default 256): candidate slots per user of the
                               light-row path (a row whose running list is full is screened in the
                               local kernel's epilogue and merged by a separate kernel; a row with more

@@ -27,7 +27,7 @@ HEADER = os.path.join(os.path.dirname(HERE), "include", "c2.h")
 C2_OK, C2_EINVAL, C2_EDATA, C2_ENOMEM, C2_ECUDA = 0, -1, -2, -3, -4
 SIM_EXACT, SIM_GF1024 = 0, 1
 OPT_SKETCH_DEPTH, OPT_SYNC_CHECK, OPT_TIMING, OPT_KSTATS, OPT_RELABEL, OPT_CLUSTERING, OPT_FUNC_OFFSET, \
-    OPT_LOCAL_SOLVER, OPT_SURVIVORS, OPT_GF_TENSOR = 1, 2, 3, 4, 5, 6, 7, 8, 9, 10
+    OPT_LOCAL_SOLVER, OPT_SURVIVORS, OPT_GF_TENSOR, OPT_SPLIT_DEVICE = 1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11
 SOLVER_BRUTE, SOLVER_HYBRID = 0, 1
 CLUSTER_FRH, CLUSTER_MINHASH = 0, 1
 ABSENT = 0xFFFF

@@ -193,6 +193,7 @@ int c2_ctx_set_option(c2_ctx *ctx, int key, int64_t value) {
     case C2_OPT_TIMING: ctx->timing = value != 0; return C2_OK;
     case C2_OPT_KSTATS: ctx->kstats = (unsigned long long *)(intptr_t)value; return C2_OK;
     case C2_OPT_RELABEL: ctx->relabel = value != 0; return C2_OK;
+    case C2_OPT_SPLIT_DEVICE: ctx->split_dev = value != 0; return C2_OK;
     case C2_OPT_GF_TENSOR: ctx->gf_tensor = value != 0; return C2_OK;
     case C2_OPT_SURVIVORS:
       if (value < 0 || value > 4096) return set_err(ctx, C2_EINVAL, "survivor slots must be in [0, 4096]");

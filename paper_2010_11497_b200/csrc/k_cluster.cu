@@ -14,7 +14,11 @@
 // The host reads two counters per level (children, next-level active nodes).
 #include <algorithm>
 
+#include <cooperative_groups.h>
+
 #include "c2_internal.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace c2 {
 
@@ -156,6 +160,237 @@ __global__ void k_split_apply(int32_t *__restrict__ slot, int32_t *__restrict__ 
   slot_next[q] = ns;  // -1: stays in the parent's residual (terminal) or child <= N
 }
 
+// ------------------------------------------------------------------ device-side split loop (N1)
+// The whole recursive split in ONE cooperative kernel: no host round trip per level.
+// Same rules and the same node numbering as the host-driven loop above (children numbered by an
+// exclusive scan over (active node, next value), active children by a scan over the same order),
+// but each level touches only its active users, held in a compact list (q, slot):
+//   count  : nv = next distinct value of every active user; hist[slot*b + nv]++          | grid sync
+//   scan   : over E = n_active*b bins, children (c >= 2) and active children (c > N),
+//            two counts packed in one u64 grid-wide exclusive scan (block partials)      | grid sync
+//   apply  : users of a child move to it; users of an active child join the next list;
+//            the next level's histogram region is zeroed                                 | grid sync
+// Every block computes the level totals from the same partials, so all blocks agree on when
+// the loop ends.  Level 0's active nodes come from the same scan over the t*b level-0 bins.
+struct SplitDev {
+  int32_t *hist;        // [hcap]
+  int32_t *child_id;    // [hcap]
+  int32_t *child_slot;  // [hcap]
+  int32_t *act_q[2];    // [TN] active (f,u) indices, ping-pong
+  int32_t *act_s[2];    // [TN] their node's slot among the level's active nodes
+  uint16_t *nvb;        // [TN] next value per active-list entry
+  unsigned long long *part;  // [grid] block partials of the packed scan
+  int32_t *act_n;       // [2] list lengths (atomic append)
+  long long *out;       // [8]: next_id, split_nodes, max_depth, folded, levels
+  int64_t hcap;
+};
+
+__device__ __forceinline__ unsigned long long block_excl_scan_u64(unsigned long long v, unsigned long long *sh,
+                                                                  unsigned long long *total) {
+  // exclusive scan over the block (blockDim.x <= 1024); sh: 32 entries
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+  unsigned long long x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    unsigned long long y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) sh[w] = x;
+  __syncthreads();
+  if (w == 0) {
+    unsigned long long s = lane < nw ? sh[lane] : 0ull;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      unsigned long long y = __shfl_up_sync(0xffffffffu, s, o);
+      if (lane >= o) s += y;
+    }
+    if (lane < nw) sh[lane] = s;  // inclusive prefix of warp totals
+  }
+  __syncthreads();
+  const unsigned long long before = (w ? sh[w - 1] : 0ull) + x - v;
+  *total = sh[nw - 1];
+  __syncthreads();
+  return before;
+}
+
+template <bool TABLE>
+__global__ void __launch_bounds__(256) k_split_dev(SplitDev sd, const uint16_t *__restrict__ sk, int32_t *__restrict__ key,
+                                                  uint16_t *__restrict__ curval, const int32_t *__restrict__ size0,
+                                                  int64_t TB, int64_t TN, int32_t n, int Deff, int32_t b, int64_t N,
+                                                  const int32_t *__restrict__ offs, const int32_t *__restrict__ items,
+                                                  HashArgs2 ha, const uint16_t *__restrict__ htab, int32_t m) {
+  cg::grid_group grid = cg::this_grid();
+  __shared__ unsigned long long sh[32];
+  __shared__ unsigned long long s_pre, s_tot;
+  const int64_t G = gridDim.x;
+  const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, gstride = G * blockDim.x;
+  const unsigned long long LO = 0xffffffffull;
+
+  // ---- packed grid scan over E bins: value(e) -> (lo, hi) counts; returns the totals.  The
+  //      callback emit(e, pre_lo, pre_hi) sees every bin's exclusive prefix.
+  auto grid_scan = [&](int64_t E, auto value, auto emit) -> unsigned long long {
+    const int64_t lo = E * blockIdx.x / G, hi = E * (blockIdx.x + 1) / G;
+    unsigned long long acc = 0;
+    for (int64_t e = lo + threadIdx.x; e < hi; e += blockDim.x) acc += value(e);
+#pragma unroll
+    for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      unsigned long long s = 0;
+      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += sh[w];
+      sd.part[blockIdx.x] = s;
+    }
+    __syncthreads();
+    grid.sync();
+    // this block's prefix and the grid total from the partials
+    unsigned long long pre = 0, tot = 0;
+    for (int64_t g = threadIdx.x; g < G; g += blockDim.x) {
+      const unsigned long long p = __ldcg(sd.part + g);
+      tot += p;
+      if (g < blockIdx.x) pre += p;
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      pre += __shfl_xor_sync(0xffffffffu, pre, o);
+      tot += __shfl_xor_sync(0xffffffffu, tot, o);
+    }
+    __syncthreads();
+    if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = pre;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      unsigned long long s = 0;
+      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += sh[w];
+      s_pre = s;
+    }
+    __syncthreads();
+    if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = tot;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      unsigned long long s = 0;
+      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += sh[w];
+      s_tot = s;
+    }
+    __syncthreads();
+    unsigned long long carry = s_pre;
+    const unsigned long long total = s_tot;
+    for (int64_t e0 = lo; e0 < hi; e0 += blockDim.x) {
+      const int64_t e = e0 + threadIdx.x;
+      const unsigned long long v = e < hi ? value(e) : 0ull;
+      unsigned long long tsum;
+      const unsigned long long ex = block_excl_scan_u64(v, sh, &tsum) + carry;
+      if (e < hi) emit(e, (int64_t)(ex & LO), (int64_t)(ex >> 32));
+      carry += tsum;
+    }
+    return total;
+  };
+
+  // ---- level 0: active nodes = level-0 bins larger than N, numbered in bin order
+  int64_t n_active = (int64_t)grid_scan(
+      TB, [&](int64_t e) -> unsigned long long { return size0[e] > N ? 1ull : 0ull; },
+      [&](int64_t e, int64_t pre, int64_t) { sd.child_slot[e] = size0[e] > N ? (int32_t)pre : -1; });
+  grid.sync();
+  for (int64_t q = gtid; q < TN; q += gstride) {
+    const int32_t s = sd.child_slot[key[q]];
+    const bool a = s >= 0;
+    const unsigned bal = __ballot_sync(__activemask(), a);
+    if (a) {
+      const int lane = threadIdx.x & 31, leader = __ffs(bal) - 1;
+      int base = 0;
+      if (lane == leader) base = atomicAdd(&sd.act_n[0], __popc(bal));
+      base = __shfl_sync(bal, base, leader);
+      const int i = base + __popc(bal & ((1u << lane) - 1u));
+      sd.act_q[0][i] = (int32_t)q;
+      sd.act_s[0][i] = s;
+    }
+  }
+  // zero the level-0 histogram region
+  for (int64_t e = gtid; e < n_active * b; e += gstride) sd.hist[e] = 0;
+  grid.sync();
+
+  int64_t next_id = TB, split_nodes = 0, max_depth = 0, folded = 0;
+  int cur = 0;
+  int d = 0;
+  for (; n_active > 0; ++d) {
+    if (d > b + 1) break;  // cannot happen (each level consumes one distinct value)
+    const int64_t na = __ldcg(sd.act_n + cur);
+    const int32_t *aq = sd.act_q[cur], *as = sd.act_s[cur];
+    // count
+    for (int64_t i = gtid; i < na; i += gstride) {
+      const int32_t q = aq[i];
+      uint16_t nv;
+      if (d + 1 < Deff) nv = sk[(int64_t)q * C2_SKETCH_D + d + 1];
+      else nv = next_above<TABLE>(offs, items, (int32_t)(q % n), (int)(q / n), curval[q], (uint32_t)b, ha, htab, m);
+      sd.nvb[i] = nv;
+      if (nv != C2_ABSENT16) atomicAdd(&sd.hist[(int64_t)as[i] * b + nv], 1);
+    }
+    if (gtid == 0) sd.act_n[cur ^ 1] = 0;
+    grid.sync();
+    // scan: children (c >= 2, low half) and active children (c > N, high half); singletons folded
+    const int64_t E = n_active * b;
+    const int32_t idb = (int32_t)next_id;
+    unsigned long long ones = 0;
+    const unsigned long long tot = grid_scan(
+        E,
+        [&](int64_t e) -> unsigned long long {
+          const int32_t c = __ldcg(sd.hist + e);
+          return (unsigned long long)(c >= 2) | ((unsigned long long)(c > N) << 32);
+        },
+        [&](int64_t e, int64_t pc, int64_t pa) {
+          const int32_t c = __ldcg(sd.hist + e);
+          sd.child_id[e] = c >= 2 ? idb + (int32_t)pc : -1;
+          sd.child_slot[e] = c > N ? (int32_t)pa : -1;
+          ones += c == 1;
+        });
+    // folded singletons (statistics): block sums into out[3]
+#pragma unroll
+    for (int o = 16; o; o >>= 1) ones += __shfl_xor_sync(0xffffffffu, ones, o);
+    if ((threadIdx.x & 31) == 0 && ones) atomicAdd((unsigned long long *)&sd.out[3], ones);
+    const int64_t n_child = (int64_t)(tot & LO), n_next = (int64_t)(tot >> 32);
+    grid.sync();
+    // apply
+    for (int64_t i = gtid; i < na; i += gstride) {
+      const int32_t q = aq[i];
+      const uint16_t nv = sd.nvb[i];
+      int32_t ns = -1;
+      if (nv != C2_ABSENT16) {
+        const int64_t e = (int64_t)as[i] * b + nv;
+        const int32_t c = sd.child_id[e];
+        if (c >= 0) {
+          key[q] = c;
+          curval[q] = nv;
+          ns = sd.child_slot[e];
+        }
+      }
+      const bool a = ns >= 0;
+      const unsigned bal = __ballot_sync(__activemask(), a);
+      if (a) {
+        const int lane = threadIdx.x & 31, leader = __ffs(bal) - 1;
+        int base = 0;
+        if (lane == leader) base = atomicAdd(&sd.act_n[cur ^ 1], __popc(bal));
+        base = __shfl_sync(bal, base, leader);
+        const int j = base + __popc(bal & ((1u << lane) - 1u));
+        sd.act_q[cur ^ 1][j] = q;
+        sd.act_s[cur ^ 1][j] = ns;
+      }
+    }
+    for (int64_t e = gtid; e < n_next * b; e += gstride) sd.hist[e] = 0;
+    grid.sync();
+    next_id += n_child;
+    split_nodes += n_active;
+    if (n_child > 0) max_depth = d + 1;
+    n_active = n_next;
+    cur ^= 1;
+  }
+  if (gtid == 0) {
+    sd.out[0] = next_id;
+    sd.out[1] = split_nodes;
+    sd.out[2] = max_depth;
+    sd.out[4] = d;
+    sd.out[5] = n_active;  // nonzero only if the level guard tripped
+  }
+}
+
 // ------------------------------------------------------------------ canonical form
 __global__ void k_count_keys(const int32_t *__restrict__ key, int64_t TN, int32_t *__restrict__ size) {
   int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -166,17 +401,35 @@ __global__ void k_count_keys(const int32_t *__restrict__ key, int64_t TN, int32_
   c2d::agg_inc(mask, &size[k], k);
 }
 
-__global__ void k_max(const int32_t *__restrict__ x, int64_t E, int32_t *__restrict__ out) {
-  int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  int v = e < E ? x[e] : 0;
+__global__ void __launch_bounds__(256) k_max(const int32_t *__restrict__ x, int64_t E, int32_t *__restrict__ out,
+                                             const long long *__restrict__ dE = nullptr) {
+  // grid-stride, one atomic per block.  dE (device-side split loop): the actual number of
+  // entries, E is only its bound
+  __shared__ int sh[8];
+  if (dE) E = min(E, (int64_t)*dE);
+  int v = 0;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < E; e += (int64_t)gridDim.x * blockDim.x)
+    v = max(v, x[e]);
 #pragma unroll
   for (int o = 16; o; o >>= 1) v = max(v, __shfl_xor_sync(0xffffffffu, v, o));
-  if ((threadIdx.x & 31) == 0) atomicMax(out, v);
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = v;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < 8; ++w) v = max(v, sh[w]);
+    if (v) atomicMax(out, v);
+  }
 }
 
 __global__ void k_rep(const int32_t *__restrict__ key, int64_t TN, int32_t n, int32_t *__restrict__ rep) {
+  // rep[node] = smallest member; lanes hold ascending q, so among the lanes of one node the lowest
+  // lane carries the smallest user (within one function) and alone does the atomicMin
   int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (q < TN) atomicMin(&rep[key[q]], (int32_t)(q % n));
+  const bool valid = q < TN;
+  const unsigned mask = __ballot_sync(0xffffffffu, valid);
+  if (!valid) return;
+  const int32_t k = key[q];
+  const unsigned peers = __match_any_sync(mask, k);
+  if ((int)(threadIdx.x & 31) == __ffs(peers) - 1) atomicMin(&rep[k], (int32_t)(q % n));
 }
 
 __global__ void k_heads(const int32_t *__restrict__ key, const int32_t *__restrict__ rep, int64_t TN, int32_t n,
@@ -209,13 +462,23 @@ __global__ void k_fix_offsets(const int32_t *__restrict__ raw, int64_t E, int32_
   offsets[e] = raw[e] - (int32_t)(f * n);
 }
 
-__global__ void k_pairs(const int32_t *__restrict__ csize, int64_t E, unsigned long long *__restrict__ acc) {
-  int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  unsigned long long s = e < E ? (unsigned long long)csize[e] : 0ull;
-  unsigned long long p = s * (s - (s > 0)) / 2;
+__global__ void __launch_bounds__(256) k_pairs(const int32_t *__restrict__ csize, int64_t E,
+                                               unsigned long long *__restrict__ acc) {
+  // P = sum of s(s-1)/2 over the clusters (A21); grid-stride, one atomic per block
+  __shared__ unsigned long long sh[8];
+  unsigned long long p = 0;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < E; e += (int64_t)gridDim.x * blockDim.x) {
+    const unsigned long long s = (unsigned long long)csize[e];
+    p += s * (s - (s > 0)) / 2;
+  }
 #pragma unroll
   for (int o = 16; o; o >>= 1) p += __shfl_xor_sync(0xffffffffu, p, o);
-  if ((threadIdx.x & 31) == 0 && p) atomicAdd(acc, p);
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = p;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < 8; ++w) p += sh[w];
+    if (p) atomicAdd(acc, p);
+  }
 }
 
 // chunk guard: sorted (key, f*n+u) pairs; node_start = exclusive scan of sizes
@@ -276,7 +539,7 @@ int count_gt(c2_ctx *ctx, const int32_t *x, int64_t E, int64_t N, int32_t *out) 
 // key[f*n+u] = node id in [0, next_id) (at most one node per cluster; a node larger than N is
 // cut into balanced chunks, A9); produces the canonical arrays (A25) and the host statistics.
 static int canonicalize(c2_ctx *ctx, int32_t n, int t, int64_t N, int32_t *key, int64_t next_id,
-                        int64_t split_nodes, int64_t max_depth, Clusters *out) {
+                        int64_t split_nodes, int64_t max_depth, Clusters *out, const long long *dev_split = nullptr) {
   int rc;
   const int64_t TN = (int64_t)t * n;
   cudaStream_t st = ctx->stream;
@@ -284,6 +547,8 @@ static int canonicalize(c2_ctx *ctx, int32_t n, int t, int64_t N, int32_t *key, 
   unsigned long long *acc = (unsigned long long *)ws_get(ctx, "acc", 64, &rc);
   if (rc) return rc;
   int32_t *hsmall = (int32_t *)ctx->h_small;
+  // dev_split: the node count is still on the device (device-side split loop); size the node
+  // arrays by the bound t*b + t*n (passed as next_id) and read the count at the first sync
   int32_t *size = (int32_t *)ws_get(ctx, "nsize", (size_t)(next_id + TN + 1) * 4, &rc);
   if (rc) return rc;
   C2_CUDA(ctx, cudaMemsetAsync(size, 0, (size_t)next_id * 4, st));
@@ -291,13 +556,25 @@ static int canonicalize(c2_ctx *ctx, int32_t n, int t, int64_t N, int32_t *key, 
   C2_LAUNCHED(ctx, "k_count_keys");
   int32_t *mx = (int32_t *)(acc + 2);
   C2_CUDA(ctx, cudaMemsetAsync(mx, 0, 4, st));
-  k_max<<<nblk(next_id), 256, 0, st>>>(size, next_id, mx);
+  k_max<<<std::min<unsigned>(nblk(next_id), ctx->num_sms * 8), 256, 0, st>>>(size, next_id, mx, dev_split);
   C2_LAUNCHED(ctx, "k_max");
   C2_CUDA(ctx, cudaMemcpyAsync(hsmall, mx, 4, cudaMemcpyDeviceToHost, st));
-  C2_CUDA(ctx, cudaMemcpyAsync(ctx->h_small + 4, acc + 1, 8, cudaMemcpyDeviceToHost, st));
+  if (dev_split) {
+    C2_CUDA(ctx, cudaMemcpyAsync(ctx->h_small + 8, dev_split, 8 * 6, cudaMemcpyDeviceToHost, st));
+  } else {
+    C2_CUDA(ctx, cudaMemcpyAsync(ctx->h_small + 4, acc + 1, 8, cudaMemcpyDeviceToHost, st));
+  }
   C2_TRY(stream_sync(ctx, "max size"));
   int64_t chunked = 0;
   int64_t folded = ctx->h_small[4];
+  if (dev_split) {
+    const long long *o = (const long long *)(ctx->h_small + 8);
+    if (o[5] != 0) return set_err(ctx, C2_ECUDA, "split did not terminate");
+    next_id = o[0];
+    split_nodes = o[1];
+    max_depth = o[2];
+    folded = o[3];
+  }
   uint32_t *skey = (uint32_t *)ws_get(ctx, "skey", (size_t)TN * 4, &rc);
   if (rc) return rc;
   uint32_t *sval = (uint32_t *)ws_get(ctx, "sval", (size_t)TN * 4, &rc);
@@ -361,10 +638,10 @@ static int canonicalize(c2_ctx *ctx, int32_t n, int t, int64_t N, int32_t *key, 
   // members: stable sort of (f*n + cluster, u) by key -> ascending members per cluster
   C2_TRY(radix_sort_pairs(ctx, skey2, sval2, skey, (uint32_t *)out->members, TN, bits_for(TN)));
   C2_CUDA(ctx, cudaMemsetAsync(acc, 0, 8, st));
-  k_pairs<<<nblk(TN1), 256, 0, st>>>(csize, TN1, acc);
+  k_pairs<<<std::min<unsigned>(nblk(TN1), ctx->num_sms * 8), 256, 0, st>>>(csize, TN1, acc);
   C2_LAUNCHED(ctx, "k_pairs");
   C2_CUDA(ctx, cudaMemsetAsync(mx, 0, 4, st));
-  k_max<<<nblk(TN1), 256, 0, st>>>(csize, TN1, mx);
+  k_max<<<std::min<unsigned>(nblk(TN1), ctx->num_sms * 8), 256, 0, st>>>(csize, TN1, mx);
   C2_LAUNCHED(ctx, "k_max");
   // host values: n_clusters[f] = hscan[(f+1)n] - hscan[fn], P, max size
   int32_t *hh = (int32_t *)ctx->h_small + 16;
@@ -444,6 +721,40 @@ int fastrandomhash(c2_ctx *ctx, const Csr &csr, int t, int b, int64_t N, const H
   } else {
     k_level0<<<nblk(TN), 256, 0, st>>>(sk, TN, n, b, key, curval, size0);
     C2_LAUNCHED(ctx, "k_level0");
+  }
+  // ---- K3 on the device (N1): the whole split loop in one cooperative kernel when its histogram
+  //      bound (at most t*n/(N+1) nodes larger than N at any level, b bins each) is moderate
+  const int64_t hcap = std::max<int64_t>(TB, (TN / (N + 1)) * (int64_t)b);
+  if (ctx->split_dev && hcap <= ((int64_t)1 << 25)) {
+    SplitDev sd;
+    char *base = (char *)ws_get(ctx, "split_dev", (size_t)hcap * 12 + (size_t)TN * 18 + 4096 * 8 + 256, &rc);
+    if (rc) return rc;
+    sd.hist = (int32_t *)base;
+    sd.child_id = sd.hist + hcap;
+    sd.child_slot = sd.child_id + hcap;
+    sd.act_q[0] = sd.child_slot + hcap;
+    sd.act_q[1] = sd.act_q[0] + TN;
+    sd.act_s[0] = sd.act_q[1] + TN;
+    sd.act_s[1] = sd.act_s[0] + TN;
+    sd.part = (unsigned long long *)(((uintptr_t)(sd.act_s[1] + TN) + 15) & ~(uintptr_t)15);
+    sd.act_n = (int32_t *)(sd.part + 4096);
+    sd.out = (long long *)(sd.part + 4097);
+    sd.nvb = (uint16_t *)(sd.part + 4106);
+    sd.hcap = hcap;
+    C2_CUDA(ctx, cudaMemsetAsync(sd.act_n, 0, 8 + 9 * 8, st));
+    auto kfn = htab ? k_split_dev<true> : k_split_dev<false>;
+    int occ = 0;
+    C2_CUDA(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kfn, 256, 0));
+    const int grid = std::min(ctx->num_sms * std::max(occ, 1), 4096);
+    int64_t TBa = TB, TNa = TN, Na = N;
+    int32_t na = n, ba = b, ma = m;
+    int Da = Deff;
+    const int32_t *oa = csr.offs, *ia = csr.items;
+    void *args[] = {&sd, &sk, &key, &curval, &size0, &TBa, &TNa, &na, &Da, &ba, &Na, &oa, &ia, &ha, &htab, &ma};
+    C2_CUDA(ctx, cudaLaunchCooperativeKernel((const void *)kfn, grid, 256, args, 0, st));
+    C2_LAUNCHED(ctx, "k_split_dev");
+    if (ctx->timing) cudaEventRecord(ev[2], st);
+    return canonicalize(ctx, n, t, N, key, TB + TN, 0, 0, out, sd.out);
   }
   k_flag_gt<<<nblk(TB), 256, 0, st>>>(size0, TB, N, aflag0);
   C2_LAUNCHED(ctx, "k_flag_gt");

@@ -120,7 +120,8 @@ __device__ __forceinline__ int find_f(const int32_t *ccum, int t, int64_t g) {
 // category of every cluster: big (> 32 users), small (2..32), single.  One 32-bit sort key
 // orders them [big: by function, then size descending][small: by function, slot class]
 // [single: by function]; counts per (category, f, class) go to cnt_fc.
-constexpr int WLC = 16;  // counters per function: 0 big tiles, 1..5 small per class, 6 single, 7 big, 8 hyrec
+constexpr int WLC = 16;  // counters per function: 0 big tiles, 1..5 small per class, 6 single, 7 big, 8 hyrec,
+                         // 9 members of big clusters
 __device__ __forceinline__ int slot_class(int32_t s) {  // slot = 2^class >= s, s in [2, 32]
   int c = 1;
   while ((1 << c) < s) ++c;
@@ -144,6 +145,7 @@ __global__ void k_wl_classify(const int32_t *__restrict__ offsets, const int32_t
     k = ((uint32_t)f << 24) | (sized ? min(maxs - s, 0xFFFFFFu) : 0u);
     atomicAdd(&cnt_fc[f * WLC + 0], (int32_t)((s + 31) / 32));  // big tiles of f
     atomicAdd(&cnt_fc[f * WLC + 7], 1);                          // big clusters of f
+    atomicAdd(&cnt_fc[f * WLC + 9], (int32_t)s);                 // their members
   } else if (s >= 2) {
     int cl = slot_class((int32_t)s);
     k = (1u << 30) | ((uint32_t)f << 24) | (uint32_t)cl;
@@ -1238,21 +1240,28 @@ __global__ void k_init_pads(c2_cand *__restrict__ R, int64_t E) {
 }
 
 // sum over unordered pairs of (|P_u| + |P_v|) = sum over (f,u) of (s_c - 1) * |P_u|
-__global__ void k_work_steps(const int32_t *__restrict__ offsets, const int32_t *__restrict__ cof,
-                             const int32_t *__restrict__ psize, int64_t TN, int32_t n,
-                             unsigned long long *__restrict__ acc) {
-  int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+__global__ void __launch_bounds__(256) k_work_steps(const int32_t *__restrict__ offsets, const int32_t *__restrict__ cof,
+                                                    const int32_t *__restrict__ psize, int64_t TN, int32_t n,
+                                                    unsigned long long *__restrict__ acc) {
+  // sum over (f, u) of (s - 1) |P_u| = sum over unordered local pairs of |P_u| + |P_v|; grid-stride,
+  // one atomic per block
+  __shared__ unsigned long long sh[8];
   unsigned long long w = 0;
-  if (q < TN) {
-    int64_t f = q / n;
-    int32_t u = (int32_t)(q % n);
-    int32_t c = cof[q];
+  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < TN; q += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t f = q / n;
+    const int32_t u = (int32_t)(q % n);
+    const int32_t c = cof[q];
     const int32_t *off = offsets + f * (n + 1);
-    w = (unsigned long long)(off[c + 1] - off[c] - 1) * (unsigned long long)psize[u];
+    w += (unsigned long long)(off[c + 1] - off[c] - 1) * (unsigned long long)psize[u];
   }
 #pragma unroll
   for (int o = 16; o; o >>= 1) w += __shfl_xor_sync(0xffffffffu, w, o);
-  if ((threadIdx.x & 31) == 0 && w) atomicAdd(acc, w);
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = w;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int i = 1; i < 8; ++i) w += sh[i];
+    if (w) atomicAdd(acc, w);
+  }
 }
 
 // ------------------------------------------------------------------ item-id compaction
@@ -1340,7 +1349,7 @@ int local_knn(c2_ctx *ctx, const Csr &csr_in, int t, const Clusters &cl, int k, 
   unsigned long long *wacc = (unsigned long long *)ws_get(ctx, "work_acc", 16, &rc);
   if (rc) return rc;
   C2_CUDA(ctx, cudaMemsetAsync(wacc, 0, 8, st));
-  k_work_steps<<<nblk((int64_t)t * n), 256, 0, st>>>(cl.offsets, cl.cluster_of, csr.psize, (int64_t)t * n, n, wacc);
+  k_work_steps<<<std::min<unsigned>(nblk((int64_t)t * n), ctx->num_sms * 8), 256, 0, st>>>(cl.offsets, cl.cluster_of, csr.psize, (int64_t)t * n, n, wacc);
   C2_LAUNCHED(ctx, "k_work_steps");
   int32_t hfc[WLC * C2_MAX_T];
   unsigned long long hwork = 0;
@@ -1348,12 +1357,13 @@ int local_knn(c2_ctx *ctx, const Csr &csr_in, int t, const Clusters &cl, int k, 
   C2_CUDA(ctx, cudaMemcpyAsync(&hwork, wacc, 8, cudaMemcpyDeviceToHost, st));
   C2_TRY(stream_sync(ctx, "worklist counts"));
   ctx->stats.work_steps = (int64_t)hwork;
-  int64_t nbig = 0, nsmall = 0, nsingle = 0, nbigtiles = 0, nhyrec = 0;
+  int64_t nbig = 0, nsmall = 0, nsingle = 0, nbigtiles = 0, nhyrec = 0, nv_big_cnt = 0;
   int32_t hy_lo[C2_MAX_T + 1];
   for (int f = 0; f < t; ++f) {
     hy_lo[f] = (int32_t)nhyrec;
     nhyrec += hfc[f * WLC + 8];
     nbig += hfc[f * WLC + 7];
+    nv_big_cnt += hfc[f * WLC + 9];
     nbigtiles += hfc[f * WLC + 0];
     for (int c = 1; c <= 5; ++c) nsmall += hfc[f * WLC + c];
     nsingle += hfc[f * WLC + 6];
@@ -1414,10 +1424,7 @@ int local_knn(c2_ctx *ctx, const Csr &csr_in, int t, const Clusters &cl, int k, 
       C2_LAUNCHED(ctx, "k_bc_sizes");
       C2_TRY(scan_exclusive(ctx, bsz, vp_scan, nbig));
       C2_TRY(scan_exclusive(ctx, bns, sl_scan, nbig));
-      int32_t h1;
-      C2_CUDA(ctx, cudaMemcpyAsync(&h1, vp_scan + nbig, 4, cudaMemcpyDeviceToHost, st));
-      C2_TRY(stream_sync(ctx, "big cluster sizes"));
-      nv_big = h1;
+      nv_big = nv_big_cnt;  // (= vp_scan[nbig]; counted by k_wl_classify, read at the worklist sync)
       nv_big_all = nv_big;
     }
     vperm = (int32_t *)ws_get(ctx, "vperm", (size_t)(nv_big + nmix * 32 + 1) * 4 * 2, &rc);

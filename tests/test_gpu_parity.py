@@ -501,3 +501,55 @@ def test_build_big_clusters_large_k(ctx, k, n, N):
     rng = np.random.default_rng(k * 7 + n)
     offs, items = synth.random_instance(rng, n, 400, 3, 60, zipf=0.8)
     check_build(ctx, offs, items, 2, 1, N, k, 5)
+
+
+# ------------------------------------------------------------------ N1: device-side split loop
+@pytest.mark.parametrize("split_dev", [0, 1])
+@pytest.mark.parametrize("case", ["random", "c1", "c3", "c4", "depth"])
+def test_split_device_loop(ctx, split_dev, case):
+    """The cooperative split kernel (C2_OPT_SPLIT_DEVICE=1) and the host-driven level loop (0)
+    both reproduce the oracle's clusters and statistics."""
+    ctx.set_option(c2.OPT_SPLIT_DEVICE, split_dev)
+    try:
+        if case == "random":
+            runs = []
+            for s in range(12):
+                offs, items, t, b, N, _, hs = random_case(s)
+                runs.append((offs, items, t, b, N, hs, 8))
+        elif case == "depth":
+            C = synth.config("c1")
+            offs, items = synth.generate("c1")
+            runs = [(offs, items, C.t, C.b, 60, C.hash_seed, d) for d in (1, 2, 8)]
+        else:
+            C = synth.config(case)
+            offs, items = synth.generate(case)
+            runs = [(offs, items, C.t, C.b, N, C.hash_seed, 8) for N in (C.N, max(C.N // 4, 2))]
+        for offs, items, t, b, N, hs, depth in runs:
+            ctx.set_option(c2.OPT_SKETCH_DEPTH, depth)
+            g = gpu_clusters(c2.fastrandomhash(dev(offs), dev(items), t, b, N, hs, ctx=ctx))
+            o = oracle.cluster(offs, items, oracle.hash_table(hs, t, b, mval(items)), N)
+            assert_clusters_equal(g, o)
+            st = ctx.stats()
+            for key in ("pairs", "split_nodes", "max_depth", "folded_singletons", "chunked_residuals"):
+                assert st[key] == o["stats"][key], key
+    finally:
+        ctx.set_option(c2.OPT_SPLIT_DEVICE, 1)
+        ctx.set_option(c2.OPT_SKETCH_DEPTH, 8)
+
+
+def test_split_device_loop_fewer_syncs():
+    """N1: with the device-side loop Step 1 synchronises with the host a fixed number of times,
+    independent of the split depth (c4 splits 3 levels deep)."""
+    C = synth.config("c4")
+    offs, items = synth.generate("c4")
+    d_o, d_i = dev(offs), dev(items)
+    syncs = {}
+    for sd in (0, 1):
+        c = c2.Context(0)
+        c.set_option(c2.OPT_SPLIT_DEVICE, sd)
+        c2.fastrandomhash(d_o, d_i, C.t, C.b, C.N, C.hash_seed, ctx=c)
+        syncs[sd] = c.stats()["host_syncs"]
+        assert c.stats()["max_depth"] >= 2
+        c.close()
+    assert syncs[1] < syncs[0]
+    assert syncs[1] <= 3, syncs
