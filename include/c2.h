@@ -115,11 +115,11 @@ enum {
                               kernel looping over the levels on the device (no host synchronisation
                               per level) whenever its histogram bound (t*n/(N+1) * b bins) is at most
                               2^25; 0: one host-driven pass per level.  Results are identical. */
-  C2_OPT_SURVIVORS = 9     /* c2_build only, 0..4096 (default 256): candidate slots per user of the
+  C2_OPT_SURVIVORS = 9     /* c2_build only, 0..4096 (default 1024; halved while n*slots*8 B > 8 GiB): slots per user of the
                               light-row path (a row whose running list is full is screened in the
                               local kernel's epilogue and merged by a separate kernel; a row with more
-                              survivors than slots is merged in-tile instead).  0: every row merged
-                              in-tile.  Results are identical for every value. */
+                              survivors than slots gets its full count row and k_row_topk instead).  0: no
+                              light rows.  Results are identical for every value. */
 };
 enum {
   C2_SOLVER_BRUTE = 0,

@@ -290,19 +290,25 @@ __global__ void __launch_bounds__(256) k_split_dev(SplitDev sd, const uint16_t *
       TB, [&](int64_t e) -> unsigned long long { return size0[e] > N ? 1ull : 0ull; },
       [&](int64_t e, int64_t pre, int64_t) { sd.child_slot[e] = size0[e] > N ? (int32_t)pre : -1; });
   grid.sync();
-  for (int64_t q = gtid; q < TN; q += gstride) {
-    const int32_t s = sd.child_slot[key[q]];
-    const bool a = s >= 0;
-    const unsigned bal = __ballot_sync(__activemask(), a);
+  // active lists are appended block-chunk by block-chunk in order (one atomic per block and
+  // chunk), so they stay in ascending runs of blockDim.x entries and the gathers of the next
+  // level (sketch, curval, key by q) stay mostly coalesced
+  __shared__ int s_base;
+  auto block_append = [&](bool a, int32_t q, int32_t s, int32_t *ctr, int32_t *lq, int32_t *ls) {
+    unsigned long long tot;
+    const unsigned long long pre = block_excl_scan_u64(a ? 1ull : 0ull, sh, &tot);
+    if (threadIdx.x == 0 && tot) s_base = atomicAdd(ctr, (int)tot);
+    __syncthreads();
     if (a) {
-      const int lane = threadIdx.x & 31, leader = __ffs(bal) - 1;
-      int base = 0;
-      if (lane == leader) base = atomicAdd(&sd.act_n[0], __popc(bal));
-      base = __shfl_sync(bal, base, leader);
-      const int i = base + __popc(bal & ((1u << lane) - 1u));
-      sd.act_q[0][i] = (int32_t)q;
-      sd.act_s[0][i] = s;
+      lq[s_base + (int)pre] = q;
+      ls[s_base + (int)pre] = s;
     }
+    __syncthreads();
+  };
+  for (int64_t q0 = (int64_t)blockIdx.x * blockDim.x; q0 < TN; q0 += gstride) {
+    const int64_t q = q0 + threadIdx.x;
+    const int32_t s = q < TN ? sd.child_slot[key[q]] : -1;
+    block_append(s >= 0, (int32_t)q, s, &sd.act_n[0], sd.act_q[0], sd.act_s[0]);
   }
   // zero the level-0 histogram region
   for (int64_t e = gtid; e < n_active * b; e += gstride) sd.hist[e] = 0;
@@ -349,30 +355,23 @@ __global__ void __launch_bounds__(256) k_split_dev(SplitDev sd, const uint16_t *
     const int64_t n_child = (int64_t)(tot & LO), n_next = (int64_t)(tot >> 32);
     grid.sync();
     // apply
-    for (int64_t i = gtid; i < na; i += gstride) {
-      const int32_t q = aq[i];
-      const uint16_t nv = sd.nvb[i];
-      int32_t ns = -1;
-      if (nv != C2_ABSENT16) {
-        const int64_t e = (int64_t)as[i] * b + nv;
-        const int32_t c = sd.child_id[e];
-        if (c >= 0) {
-          key[q] = c;
-          curval[q] = nv;
-          ns = sd.child_slot[e];
+    for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x; i0 < na; i0 += gstride) {
+      const int64_t i = i0 + threadIdx.x;
+      int32_t q = -1, ns = -1;
+      if (i < na) {
+        q = aq[i];
+        const uint16_t nv = sd.nvb[i];
+        if (nv != C2_ABSENT16) {
+          const int64_t e = (int64_t)as[i] * b + nv;
+          const int32_t c = sd.child_id[e];
+          if (c >= 0) {
+            key[q] = c;
+            curval[q] = nv;
+            ns = sd.child_slot[e];
+          }
         }
       }
-      const bool a = ns >= 0;
-      const unsigned bal = __ballot_sync(__activemask(), a);
-      if (a) {
-        const int lane = threadIdx.x & 31, leader = __ffs(bal) - 1;
-        int base = 0;
-        if (lane == leader) base = atomicAdd(&sd.act_n[cur ^ 1], __popc(bal));
-        base = __shfl_sync(bal, base, leader);
-        const int j = base + __popc(bal & ((1u << lane) - 1u));
-        sd.act_q[cur ^ 1][j] = q;
-        sd.act_s[cur ^ 1][j] = ns;
-      }
+      block_append(ns >= 0, q, ns, &sd.act_n[cur ^ 1], sd.act_q[cur ^ 1], sd.act_s[cur ^ 1]);
     }
     for (int64_t e = gtid; e < n_next * b; e += gstride) sd.hist[e] = 0;
     grid.sync();

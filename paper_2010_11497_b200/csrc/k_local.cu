@@ -446,7 +446,8 @@ __global__ void __launch_bounds__(256) k_sl_fill(int64_t nslices, const int32_t 
 __global__ void __launch_bounds__(256) k_sl_fill_rows(int64_t nb, int nwin, const int32_t *__restrict__ bounds,
                                                       const int32_t *__restrict__ items, int32_t W,
                                                       const int32_t *__restrict__ blk_len8,
-                                                      const int32_t *__restrict__ blk_off8, uint4 *__restrict__ packed) {
+                                                      const int32_t *__restrict__ blk_off8, uint4 *__restrict__ packed,
+                                                      int64_t nnz, int vec) {
   const int lane = threadIdx.x & 31;
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwg = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -462,10 +463,28 @@ __global__ void __launch_bounds__(256) k_sl_fill_rows(int64_t nb, int nwin, cons
     uint4 *out = packed + (int64_t)blk_off8[b] * 32 + lane;
     for (int t = sub; t < len8; t += 8) {
       uint32_t h[8];
+      const int32_t p0 = pb + 8 * t;
+      if (p0 >= pe) {  // past this member's list: padding only
 #pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        const int32_t p = pb + 8 * t + j;
-        h[j] = p < pe ? (uint32_t)(__ldg(items + p) - lo) : (uint32_t)W;
+        for (int j = 0; j < 8; ++j) h[j] = (uint32_t)W;
+      } else if (vec && ((int64_t)(p0 & ~3) + 12 <= nnz)) {
+        // three aligned 16-byte loads cover the 8 items [p0, p0 + 8) (items is 16-byte aligned)
+        const int32_t a0 = p0 & ~3, o = p0 & 3;
+        const int4 A = __ldg(reinterpret_cast<const int4 *>(items + a0));
+        const int4 Bv = __ldg(reinterpret_cast<const int4 *>(items + a0 + 4));
+        const int4 Cv = o ? __ldg(reinterpret_cast<const int4 *>(items + a0 + 8)) : make_int4(0, 0, 0, 0);
+        const int32_t x[12] = {A.x, A.y, A.z, A.w, Bv.x, Bv.y, Bv.z, Bv.w, Cv.x, Cv.y, Cv.z, Cv.w};
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const int32_t v = o == 0 ? x[j] : o == 1 ? x[j + 1] : o == 2 ? x[j + 2] : x[j + 3];
+          h[j] = p0 + j < pe ? (uint32_t)(v - lo) : (uint32_t)W;
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const int32_t p = p0 + j;
+          h[j] = p < pe ? (uint32_t)(__ldg(items + p) - lo) : (uint32_t)W;
+        }
       }
       out[(int64_t)t * 32] = make_uint4(h[0] | (h[1] << 16), h[2] | (h[3] << 16), h[4] | (h[5] << 16), h[6] | (h[7] << 16));
     }
@@ -1516,7 +1535,9 @@ int local_knn(c2_ctx *ctx, const Csr &csr_in, int t, const Clusters &cl, int k, 
                                                            reinterpret_cast<uint16_t *>(packed), 1);
         C2_LAUNCHED(ctx, "k_sl_fill");
       } else {
-        k_sl_fill_rows<<<ctx->num_sms * 16, 256, 0, st>>>(nb, nwin, bounds, csr.items, W, blk_len8, blk_off8, packed);
+        const int vec = ((uintptr_t)csr.items & 15) == 0 ? 1 : 0;
+        k_sl_fill_rows<<<ctx->num_sms * 16, 256, 0, st>>>(nb, nwin, bounds, csr.items, W, blk_len8, blk_off8, packed,
+                                                          csr.nnz, vec);
         C2_LAUNCHED(ctx, "k_sl_fill_rows");
       }
     }
@@ -1535,7 +1556,9 @@ int local_knn(c2_ctx *ctx, const Csr &csr_in, int t, const Clusters &cl, int k, 
   //      re-zeroed by k_surv_merge after every function
   c2_cand *surv = nullptr;
   int32_t *surv_qn = nullptr;
-  const int surv_qmax = ctx->surv_qmax;
+  // survivor slots: the option's value, but at most 8 GiB of slots (halved until it fits, >= 64)
+  int surv_qmax = ctx->surv_qmax;
+  while (surv_qmax > 64 && (size_t)n * surv_qmax * sizeof(c2_cand) > ((size_t)8 << 30)) surv_qmax >>= 1;
   if (fused && C2_LIGHT && surv_qmax > 0 && nslices > 0) {
     surv = (c2_cand *)ws_get(ctx, "surv", (size_t)n * surv_qmax * sizeof(c2_cand), &rc);
     if (rc) return rc;

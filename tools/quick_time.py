@@ -8,6 +8,10 @@ import paper_2010_11497_b200 as c2
 
 cfgs = sys.argv[1:] or ["c1", "c2", "c3", "c4", "c5"]
 ctx = c2.Context(0, timing=True)
+# QT_OPTS="9=1024,11=0": ctx options (C2_OPT_* number = value) for A/B runs
+for kv in filter(None, os.environ.get("QT_OPTS", "").split(",")):
+    k, v = kv.split("=")
+    ctx.set_option(int(k), int(v))
 for spec in cfgs:
     # "c5" or "c5:m=16000:N=256" (overrides of the synthetic config, dev experiments)
     name, *kv = spec.split(":")
