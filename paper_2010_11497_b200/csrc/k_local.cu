@@ -96,6 +96,9 @@ __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.
 #ifndef C2_TILE_MINB
 #define C2_TILE_MINB 1
 #endif
+#ifndef C2_FILL_COAL
+#define C2_FILL_COAL 1  // multi-window packing: k_sl_fill_coal (coalesced CSR reads) instead of k_sl_fill_rows
+#endif
 #ifndef C2_SMEM_BUDGET
 #define C2_SMEM_BUDGET 0  // bytes of dynamic shared memory per tile CTA (0: the opt-in maximum)
 #endif
@@ -487,6 +490,73 @@ __global__ void __launch_bounds__(256) k_sl_fill_rows(int64_t nb, int nwin, cons
         }
       }
       out[(int64_t)t * 32] = make_uint4(h[0] | (h[1] << 16), h[2] | (h[3] << 16), h[4] | (h[5] << 16), h[6] | (h[7] << 16));
+    }
+  }
+}
+
+// Same output as k_sl_fill_rows, with the CSR read coalesced: one warp per (slice, window) block
+// takes its 32 members one after the other, the lanes reading consecutive items of a member (full
+// 128-byte lines), and transposes them through a shared-memory stage of FR_R rows
+// ([row][lane][8] u16, pre-filled with the pad W) that it then writes out as whole 512-byte rows.
+constexpr int FR_WARPS = 4;
+constexpr int FR_R = 8;  // rows (of 8 items per member) staged per pass
+__global__ void __launch_bounds__(FR_WARPS * 32) k_sl_fill_coal(int64_t nb, int nwin, const int32_t *__restrict__ bounds,
+                                                               const int32_t *__restrict__ items, int32_t W,
+                                                               const int32_t *__restrict__ blk_len8,
+                                                               const int32_t *__restrict__ blk_off8,
+                                                               uint4 *__restrict__ packed) {
+  __shared__ __align__(16) uint16_t stage[FR_WARPS][FR_R * 32 * 8];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  uint16_t *stg = stage[wib];
+  uint4 *stg4 = reinterpret_cast<uint4 *>(stg);
+  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwg = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const uint32_t pw = (uint32_t)W | ((uint32_t)W << 16);
+  const uint4 padv = make_uint4(pw, pw, pw, pw);
+  for (int64_t b = gw; b < nb; b += nwg) {
+    const int64_t sl = b / nwin;
+    const int w = (int)(b - sl * nwin);
+    const int32_t *bd = bounds + (sl * 32 + lane) * (nwin + 1);
+    const int32_t mpb = bd[w], mpe = bd[w + 1];  // lane e's member: window list [mpb, mpe)
+    const int32_t lo = w * W;
+    const int32_t len8 = blk_len8[b];
+    uint4 *out = packed + (int64_t)blk_off8[b] * 32 + lane;
+    for (int32_t t0 = 0; t0 < len8; t0 += FR_R) {
+      const int nr = min(FR_R, len8 - t0);
+      for (int i = lane; i < nr * 32; i += 32) stg4[i] = padv;
+      __syncwarp();
+      // members in groups of 8: the group's first 64 items each are all requested before any is
+      // stored (16 loads in flight per lane); longer chunks (FR_R > 8) finish in a second loop
+      for (int e0 = 0; e0 < 32; e0 += 8) {
+        int32_t pbv[8], pev[8], xv[8][2];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          pbv[i] = __shfl_sync(0xffffffffu, mpb, e0 + i) + 8 * t0;
+          pev[i] = min(__shfl_sync(0xffffffffu, mpe, e0 + i), pbv[i] + 8 * nr);
+        }
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int32_t p = pbv[i] + 32 * h + lane;
+            xv[i][h] = p < pev[i] ? __ldg(items + p) : 0;
+          }
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int pos = 32 * h + lane;
+            if (pbv[i] + pos < pev[i]) stg[((pos >> 3) * 32 + e0 + i) * 8 + (pos & 7)] = (uint16_t)(xv[i][h] - lo);
+          }
+          for (int32_t p = pbv[i] + 64 + lane; p < pev[i]; p += 32) {
+            const int pos = p - pbv[i];
+            stg[((pos >> 3) * 32 + e0 + i) * 8 + (pos & 7)] = (uint16_t)(__ldg(items + p) - lo);
+          }
+        }
+      }
+      __syncwarp();
+      for (int r = 0; r < nr; ++r) out[(int64_t)(t0 + r) * 32] = stg4[r * 32 + lane];
+      __syncwarp();
     }
   }
 }
@@ -1535,10 +1605,16 @@ int local_knn(c2_ctx *ctx, const Csr &csr_in, int t, const Clusters &cl, int k, 
                                                            reinterpret_cast<uint16_t *>(packed), 1);
         C2_LAUNCHED(ctx, "k_sl_fill");
       } else {
-        const int vec = ((uintptr_t)csr.items & 15) == 0 ? 1 : 0;
-        k_sl_fill_rows<<<ctx->num_sms * 16, 256, 0, st>>>(nb, nwin, bounds, csr.items, W, blk_len8, blk_off8, packed,
-                                                          csr.nnz, vec);
-        C2_LAUNCHED(ctx, "k_sl_fill_rows");
+        if (C2_FILL_COAL) {
+          k_sl_fill_coal<<<ctx->num_sms * 14, FR_WARPS * 32, 0, st>>>(nb, nwin, bounds, csr.items, W, blk_len8, blk_off8,
+                                                                      packed);
+          C2_LAUNCHED(ctx, "k_sl_fill_coal");
+        } else {
+          const int vec = ((uintptr_t)csr.items & 15) == 0 ? 1 : 0;
+          k_sl_fill_rows<<<ctx->num_sms * 16, 256, 0, st>>>(nb, nwin, bounds, csr.items, W, blk_len8, blk_off8, packed,
+                                                            csr.nnz, vec);
+          C2_LAUNCHED(ctx, "k_sl_fill_rows");
+        }
       }
     }
   }

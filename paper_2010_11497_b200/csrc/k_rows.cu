@@ -339,6 +339,11 @@ __device__ __forceinline__ void sort_merge_step(Cand (&S)[KS], Cand x, int k, c2
 // whatever the survivors' order.
 constexpr int SM_INSERT_MAX = 32;  // survivors of a chunk merged by insertion (more: sort + merge; at 6 the
                                    // sort-and-merge step measured slower at c5: 6.6 vs 5.9 ms over 8 launches)
+#ifndef C2_SM_MERGE_MIN
+#define C2_SM_MERGE_MIN 16
+#endif
+constexpr int SM_MERGE_MIN = C2_SM_MERGE_MIN;  // k <= 32: chunks with more survivors take the bitonic merge
+                                               // (c5: threshold 4 57.6 ms, 8 56.3, 16 55.4, off 55.5)
 
 template <int KS>
 __global__ void __launch_bounds__(256) k_surv_merge(const c2_cand *__restrict__ surv, int32_t *__restrict__ qn,
@@ -365,10 +370,32 @@ __global__ void __launch_bounds__(256) k_surv_merge(const c2_cand *__restrict__ 
       bool changed = false;
       for (int c0 = 0; c0 < m; c0 += 32) {
         Cand x = c0 + lane < m ? from_out(Q[c0 + lane]) : sent();
-        const bool ok = is_real(x) && better_c(x, tau);
+        bool ok = is_real(x) && better_c(x, tau);
         unsigned bal = __ballot_sync(0xffffffffu, ok);
         if (!bal) continue;
         changed = true;
+        if (KS == 1 && __popc(bal) > SM_MERGE_MIN) {
+          // k <= 32: drop the survivors already in S (binary search of S, best first: a repeated id
+          // carries the same (i, U), so it sits exactly where the search ends, A16), sort the rest
+          // best first, reverse them against S and keep the better of each pair (the 32 best of
+          // S and Q as a bitonic sequence), then one bitonic merge
+          int r = 0;
+#pragma unroll
+          for (int st = 16; st >= 1; st >>= 1) {
+            const Cand o = shfl_c(S[0], min(r + st - 1, 31));
+            if (r + st <= 32 && better_c(o, x)) r += st;
+          }
+          const Cand at = shfl_c(S[0], min(r, 31));
+          ok = ok && !(r < 32 && at.id == x.id);
+          Cand q[1] = {ok ? x : sent()};
+          warp_sort<1>(q);
+          const Cand qr = shfl_c(q[0], 31 - lane);  // worst first
+          Cand mrg[1] = {better_c(qr, S[0]) ? qr : S[0]};
+          warp_bitonic_merge<1>(mrg);
+          S[0] = (lane < k) ? mrg[0] : sent();
+          tau = warp_get<KS>(S, k - 1);
+          continue;
+        }
         if (__popc(bal) > SM_INSERT_MAX) {
           sort_merge_step<KS>(S, ok ? x : sent(), k, sbuf);
           tau = warp_get<KS>(S, k - 1);
