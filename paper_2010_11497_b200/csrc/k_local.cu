@@ -345,9 +345,23 @@ __device__ __forceinline__ int32_t lower_bound_items(const int32_t *__restrict__
 // Rows are sorted, so window w of a member's list is the contiguous range [lb(wW), lb((w+1)W)):
 // one thread per member position finds its window boundaries by binary search (no item walk)
 // and folds the lengths into the slice maxima.
+// Per user, once per call (not once per function): the inner window boundaries of its sorted row,
+// ub[u][w-1] = first position with item >= w*W (w = 1..nwin-1).
+__global__ void k_user_bounds(const int32_t *__restrict__ offs, const int32_t *__restrict__ items, int32_t n,
+                              int32_t W, int nwin, int32_t *__restrict__ ub) {
+  const int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (u >= n) return;
+  int32_t p = offs[u];
+  const int32_t pe = offs[u + 1];
+  for (int w = 1; w < nwin; ++w) {
+    p = lower_bound_items(items, p, pe, w * W);
+    ub[u * (nwin - 1) + w - 1] = p;
+  }
+}
+
 __global__ void k_sl_len(const Tile *__restrict__ tiles, int64_t nslices, const BigC *__restrict__ bcs,
                          const int32_t *__restrict__ vperm, const int32_t *__restrict__ offs,
-                         const int32_t *__restrict__ items, int32_t W, int nwin, int32_t *__restrict__ blk_len8,
+                         const int32_t *__restrict__ ub, int32_t W, int nwin, int32_t *__restrict__ blk_len8,
                          int32_t *__restrict__ bounds) {
   const int lane = threadIdx.x & 31;
   const int64_t sl = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -361,7 +375,7 @@ __global__ void k_sl_len(const Tile *__restrict__ tiles, int64_t nslices, const 
   int32_t *bd = bounds + (sl * 32 + lane) * (nwin + 1);  // window w of this member: [bd[w], bd[w+1])
   bd[0] = p;
   for (int w = 0; w < nwin; ++w) {
-    const int32_t q = w + 1 < nwin ? lower_bound_items(items, p, pe, (w + 1) * W) : pe;
+    const int32_t q = w + 1 < nwin ? (v >= 0 ? ub[(int64_t)v * (nwin - 1) + w] : 0) : pe;
     bd[w + 1] = q;
     int c = q - p;
     p = q;
@@ -1590,8 +1604,15 @@ int local_knn(c2_ctx *ctx, const Csr &csr_in, int t, const Clusters &cl, int k, 
       blk_off8 = blk_len8 + nb + 1;
       int32_t *bounds = (int32_t *)ws_get(ctx, "sl_bounds", (size_t)nslices * 32 * (nwin + 1) * 4, &rc);
       if (rc) return rc;
-      k_sl_len<<<nblk(nslices * 32), 256, 0, st>>>(tiles, nslices, bcs, vperm, csr.offs, csr.items, W, nwin,
-                                                   blk_len8, bounds);
+      int32_t *ub = nullptr;
+      if (nwin > 1) {
+        ub = (int32_t *)ws_get(ctx, "user_bounds", (size_t)n * (nwin - 1) * 4, &rc);
+        if (rc) return rc;
+        k_user_bounds<<<nblk(n), 256, 0, st>>>(csr.offs, csr.items, n, W, nwin, ub);
+        C2_LAUNCHED(ctx, "k_user_bounds");
+      }
+      k_sl_len<<<nblk(nslices * 32), 256, 0, st>>>(tiles, nslices, bcs, vperm, csr.offs, ub, W, nwin, blk_len8,
+                                                   bounds);
       C2_LAUNCHED(ctx, "k_sl_len");
       C2_TRY(scan_exclusive(ctx, blk_len8, blk_off8, nb));
       int32_t tot8;
