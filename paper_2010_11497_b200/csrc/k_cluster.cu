@@ -96,6 +96,33 @@ __device__ __forceinline__ uint16_t next_above(const int32_t *__restrict__ offs,
   return (uint16_t)best;
 }
 
+// the D smallest distinct values above eta of {h(i) : i in P_u}, ascending, ABSENT padded
+template <bool TABLE>
+__device__ __noinline__ void refill_above(const int32_t *__restrict__ offs, const int32_t *__restrict__ items,
+                                             int32_t u, int f, uint32_t eta, uint32_t b, uint64_t ha_a, uint64_t ha_c,
+                                             const uint16_t *__restrict__ htab, int32_t m, int D,
+                                             uint16_t *__restrict__ row) {
+  uint32_t s[C2_SKETCH_D];
+#pragma unroll
+  for (int j = 0; j < C2_SKETCH_D; ++j) s[j] = C2_ABSENT16;
+  for (int32_t p = offs[u]; p < offs[u + 1]; ++p) {
+    const uint32_t x = (uint32_t)items[p];
+    const uint32_t v = TABLE ? (uint32_t)htab[(int64_t)f * m + x] : c2d::item_hash(ha_a, ha_c, x, b);
+    if (v <= eta || v >= s[D - 1]) continue;
+    bool dup = false;
+#pragma unroll
+    for (int j = 0; j < C2_SKETCH_D; ++j) dup |= j < D && s[j] == v;
+    if (dup) continue;
+#pragma unroll
+    for (int j = C2_SKETCH_D - 1; j >= 1; --j)
+      if (j < D) s[j] = (v < s[j - 1]) ? s[j - 1] : ((v < s[j]) ? v : s[j]);
+    s[0] = min(s[0], v);
+  }
+#pragma unroll
+  for (int j = 0; j < C2_SKETCH_D; ++j)
+    if (j < D) row[j] = (uint16_t)s[j];
+}
+
 template <bool TABLE>
 __global__ void k_split_count(const int32_t *__restrict__ slot, const uint16_t *__restrict__ sk,
                               const uint16_t *__restrict__ curval, uint16_t *__restrict__ nextval, int64_t TN,
@@ -214,7 +241,8 @@ __device__ __forceinline__ unsigned long long block_excl_scan_u64(unsigned long 
 }
 
 template <bool TABLE>
-__global__ void __launch_bounds__(256) k_split_dev(SplitDev sd, const uint16_t *__restrict__ sk, int32_t *__restrict__ key,
+__global__ void __launch_bounds__(256, 4) k_split_dev(SplitDev sd, const uint16_t *__restrict__ skr, uint16_t *sk,
+                                                  int32_t *__restrict__ key,
                                                   uint16_t *__restrict__ curval, const int32_t *__restrict__ size0,
                                                   int64_t TB, int64_t TN, int32_t n, int Deff, int32_t b, int64_t N,
                                                   const int32_t *__restrict__ offs, const int32_t *__restrict__ items,
@@ -325,8 +353,24 @@ __global__ void __launch_bounds__(256) k_split_dev(SplitDev sd, const uint16_t *
     for (int64_t i = gtid; i < na; i += gstride) {
       const int32_t q = aq[i];
       uint16_t nv;
-      if (d + 1 < Deff) nv = sk[(int64_t)q * C2_SKETCH_D + d + 1];
-      else nv = next_above<TABLE>(offs, items, (int32_t)(q % n), (int)(q / n), curval[q], (uint32_t)b, ha, htab, m);
+      if (d + 1 < Deff) {
+        nv = skr[(int64_t)q * C2_SKETCH_D + d + 1];
+      } else if (d + 1 == Deff) {
+        nv = next_above<TABLE>(offs, items, (int32_t)(q % n), (int)(q / n), curval[q], (uint32_t)b, ha, htab, m);
+      } else {
+        // deeper: every Deff levels one pass over the row refills the user's sketch row with the
+        // next Deff distinct values above its current node's value (H\eta applied Deff times,
+        // P:463; the sketch is dead scratch once the split has passed it) instead of one pass per
+        // level.  Written and read through the coherent pointer only.
+        uint16_t *row = sk + (int64_t)q * C2_SKETCH_D;
+        const int j = (d - Deff) % Deff;
+        if (j == 0) {
+          const int f = (int)(q / n);
+          refill_above<TABLE>(offs, items, (int32_t)(q % n), f, curval[q], (uint32_t)b, TABLE ? 0ull : ha.a[f],
+                              TABLE ? 0ull : ha.c[f], htab, m, Deff, row);
+        }
+        nv = row[j];
+      }
       sd.nvb[i] = nv;
       if (nv != C2_ABSENT16) atomicAdd(&sd.hist[(int64_t)as[i] * b + nv], 1);
     }
@@ -749,7 +793,8 @@ int fastrandomhash(c2_ctx *ctx, const Csr &csr, int t, int b, int64_t N, const H
     int32_t na = n, ba = b, ma = m;
     int Da = Deff;
     const int32_t *oa = csr.offs, *ia = csr.items;
-    void *args[] = {&sd, &sk, &key, &curval, &size0, &TBa, &TNa, &na, &Da, &ba, &Na, &oa, &ia, &ha, &htab, &ma};
+    uint16_t *skw = sk;
+    void *args[] = {&sd, &sk, &skw, &key, &curval, &size0, &TBa, &TNa, &na, &Da, &ba, &Na, &oa, &ia, &ha, &htab, &ma};
     C2_CUDA(ctx, cudaLaunchCooperativeKernel((const void *)kfn, grid, 256, args, 0, st));
     C2_LAUNCHED(ctx, "k_split_dev");
     if (ctx->timing) cudaEventRecord(ev[2], st);

@@ -505,7 +505,7 @@ def test_build_big_clusters_large_k(ctx, k, n, N):
 
 # ------------------------------------------------------------------ N1: device-side split loop
 @pytest.mark.parametrize("split_dev", [0, 1])
-@pytest.mark.parametrize("case", ["random", "c1", "c3", "c4", "depth"])
+@pytest.mark.parametrize("case", ["random", "c1", "c3", "c4", "depth", "deep"])
 def test_split_device_loop(ctx, split_dev, case):
     """The cooperative split kernel (C2_OPT_SPLIT_DEVICE=1) and the host-driven level loop (0)
     both reproduce the oracle's clusters and statistics."""
@@ -516,6 +516,12 @@ def test_split_device_loop(ctx, split_dev, case):
             for s in range(12):
                 offs, items, t, b, N, _, hs = random_case(s)
                 runs.append((offs, items, t, b, N, hs, 8))
+        elif case == "deep":
+            # splits far past the sketch depth (b small against long profiles, N tiny): the
+            # device loop refills each active user's sketch row every D levels
+            rng = np.random.default_rng(77)
+            offs, items = synth.random_instance(rng, 700, 500, 30, 150, zipf=0.8)
+            runs = [(offs, items, 2, b, 6, 11, d) for b in (16, 64) for d in (8, 3)]
         elif case == "depth":
             C = synth.config("c1")
             offs, items = synth.generate("c1")
