@@ -180,3 +180,18 @@ def test_item_ids_past_window_limit(ctx):
         o = oracle.build_graph(offs, items, k=k, t=t, b=b, N=N, seed=4, htab=htab)
         assert np.array_equal(npy(nbr), o["nbr"])
         assert np.array_equal(npy(inter), o["inter"]) and np.array_equal(npy(uni), o["uni"])
+
+
+@pytest.mark.parametrize("cfg", ["c4", "c5"])
+def test_repeated_builds_match_digests(ctx, cfg):
+    """Determinism at full speed (no per-launch synchronisation): three back-to-back builds on one
+    stream, each compared with the oracle's digests -- a race in the tile kernel's shared-memory
+    reuse or the in-place running lists would show up as a run-to-run difference."""
+    rec = golden(cfg, 0)
+    C = synth.config(cfg)
+    offs, items = synth.generate(cfg)
+    d_o, d_i = dev(offs), dev(items)
+    outs = [c2.build(d_o, d_i, k=C.k, t=C.t, b=C.b, N=C.N, seed=C.hash_seed, ctx=ctx) for _ in range(3)]
+    for nbr, inter, uni, sim in outs:
+        assert sha(npy(nbr)) == rec["nbr_sha256"]
+        assert sha(npy(inter)) == rec["inter_sha256"] and sha(npy(uni)) == rec["uni_sha256"]
