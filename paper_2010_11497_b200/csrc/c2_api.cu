@@ -36,6 +36,7 @@ void begin(c2_ctx *ctx) {
   ctx->stats.ms_tile = 0;
   ctx->tile_ev_used = 0;
   ctx->err[0] = 0;
+  ctx->presketched = false;
   cudaSetDevice(ctx->device);
 }
 
@@ -79,12 +80,14 @@ float ev_ms(cudaEvent_t a, cudaEvent_t b) {
 // Steps 1-3 on device data.  ev[6] validation start, ev[0..3] step 1, ev[4] step 2, ev[5] step 3.
 int build_device(c2_ctx *ctx, const int32_t *offs, const int32_t *items, int32_t n, int32_t t, int32_t b, int32_t N,
                  int32_t k, int32_t sim_mode, uint64_t seed, int32_t *nbr, uint16_t *inter, uint16_t *uni,
-                 float *sim) {
+                 float *sim, const Csr *prevalidated = nullptr) {
   cudaStream_t st = ctx->stream;
   C2Range r_build("c2_build");
-  if (ctx->timing) cudaEventRecord(ctx->ev[6], st);
+  if (ctx->timing && !prevalidated) cudaEventRecord(ctx->ev[6], st);
   Csr csr{offs, items, n, -1, 0, 0, nullptr};
-  {
+  if (prevalidated) {
+    csr = *prevalidated;  // c2_build_host: validated (and sketched) chunk by chunk during the upload
+  } else {
     C2Range r("validate");
     C2_TRY(validate_csr(ctx, &csr));
   }
@@ -175,6 +178,12 @@ void c2_ctx_destroy(c2_ctx *ctx) {
   for (auto &e : ctx->ev)
     if (e) cudaEventDestroy(e);
   for (auto &e : ctx->tile_ev) cudaEventDestroy(e);
+  if (ctx->copy_stream) {
+    cudaStreamSynchronize(ctx->copy_stream);
+    cudaStreamDestroy(ctx->copy_stream);
+    for (auto &e : ctx->chunk_ev)
+      if (e) cudaEventDestroy(e);
+  }
   if (ctx->h_small) cudaFreeHost(ctx->h_small);
   if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
   delete ctx;
@@ -361,10 +370,52 @@ int c2_build_host(c2_ctx *ctx, const int32_t *csr_offsets, const int32_t *item_i
   float *d_sim = (float *)(d_out + nk * 4);
   uint16_t *d_inter = (uint16_t *)(d_out + nk * 8);
   uint16_t *d_uni = (uint16_t *)(d_out + nk * 10);
-  C2_CUDA(ctx, cudaMemcpyAsync(d_offs, csr_offsets, (size_t)(n_users + 1) * 4, cudaMemcpyHostToDevice, st));
-  C2_CUDA(ctx, cudaMemcpyAsync(d_items, item_ids, (size_t)nnz * 4, cudaMemcpyHostToDevice, st));
+  // Upload in user chunks of ~equal item counts on a copy stream; each chunk is validated and
+  // (FastRandomHash path) sketched on the compute stream as soon as it has arrived, so the PCIe
+  // transfer overlaps Step 1's first kernels.  The validation result is read once at the end.
+  if (!ctx->copy_stream) {
+    C2_CUDA(ctx, cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
+    for (auto &e : ctx->chunk_ev) C2_CUDA(ctx, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  }
+  cudaStream_t cs = ctx->copy_stream;
+  if (ctx->timing) cudaEventRecord(ctx->ev[6], st);
+  C2_CUDA(ctx, cudaEventRecord(ctx->chunk_ev[15], st));  // earlier work on these buffers is done first
+  C2_CUDA(ctx, cudaStreamWaitEvent(cs, ctx->chunk_ev[15], 0));
+  const int nch = (int)std::min<int64_t>(8, n_users);
+  HashParams hp;
+  make_hash_params(seed, t, &hp, ctx->func_offset);
+  const bool frh = ctx->clustering == 0;
+  uint16_t *skb = nullptr;
+  if (frh) {
+    skb = (uint16_t *)ws_get(ctx, "sketch", (size_t)t * n_users * C2_SKETCH_D * 2, &rc);
+    if (rc) return rc;
+  }
+  Csr csr{d_offs, d_items, n_users, nnz, -1, 0, nullptr};
+  C2_TRY(validate_begin(ctx, n_users));
+  int32_t u0 = 0;
+  for (int c = 0; c < nch; ++c) {
+    int32_t u1 = n_users;
+    if (c + 1 < nch) {  // first user whose row starts at or after the chunk's share of the items
+      const int64_t target = nnz * (c + 1) / nch;
+      u1 = (int32_t)(std::lower_bound(csr_offsets + u0, csr_offsets + n_users, (int32_t)target) - csr_offsets);
+      u1 = std::max(u1, u0 + 1);
+    }
+    const int64_t p0 = std::max<int64_t>(csr_offsets[u0], 0), p1 = std::min<int64_t>(csr_offsets[u1], nnz);
+    C2_CUDA(ctx, cudaMemcpyAsync(d_offs + u0, csr_offsets + u0, (size_t)(u1 - u0 + 1) * 4, cudaMemcpyHostToDevice,
+                                 cs));  // (offsets u0..u1: the chunk's rows and the end of its last row)
+    if (p1 > p0)
+      C2_CUDA(ctx, cudaMemcpyAsync(d_items + p0, item_ids + p0, (size_t)(p1 - p0) * 4, cudaMemcpyHostToDevice, cs));
+    C2_CUDA(ctx, cudaEventRecord(ctx->chunk_ev[c], cs));
+    C2_CUDA(ctx, cudaStreamWaitEvent(st, ctx->chunk_ev[c], 0));
+    C2_TRY(validate_chunk(ctx, csr, u0, u1));
+    if (frh) C2_TRY(sketch_range(ctx, csr, t, b, &hp, u0, u1, skb));
+    if (u1 >= n_users) break;
+    u0 = u1;
+  }
+  C2_TRY(validate_finish(ctx, &csr, nnz));
+  ctx->presketched = frh;
   C2_TRY(build_device(ctx, d_offs, d_items, n_users, t, b, max_cluster_N, k, sim_mode, seed, d_nbr, d_inter, d_uni,
-                      sim ? d_sim : nullptr));
+                      sim ? d_sim : nullptr, &csr));
   C2_CUDA(ctx, cudaMemcpyAsync(nbr, d_nbr, nk * 4, cudaMemcpyDeviceToHost, st));
   C2_CUDA(ctx, cudaMemcpyAsync(inter, d_inter, nk * 2, cudaMemcpyDeviceToHost, st));
   C2_CUDA(ctx, cudaMemcpyAsync(uni, d_uni, nk * 2, cudaMemcpyDeviceToHost, st));

@@ -42,6 +42,9 @@ struct c2_ctx {
   uint64_t hyrec_seed = 0;  // the call's seed (Hyrec's random initial graphs)   // C2_OPT_CLUSTERING: 0 FastRandomHash (Step 1 of C^2), 1 MinHash (N3 variant)
   int surv_qmax = 1024;  // C2_OPT_SURVIVORS: light-row survivor slots per user (0: off; capped to 8 GiB of slots)
   bool gf_tensor = false;  // C2_OPT_GF_TENSOR: GoldFinger big clusters on the tensor cores (k_gf_mma; measured slower, off)
+  bool presketched = false;  // c2_build_host: the sketch of the next fastrandomhash call is already in "sketch"
+  cudaStream_t copy_stream = nullptr;  // c2_build_host: chunked H2D upload overlapping validation + sketch
+  cudaEvent_t chunk_ev[16] = {};
   bool split_dev = true;  // C2_OPT_SPLIT_DEVICE: device-side split loop (k_split_dev)
   bool relabel = true;  // C2_OPT_RELABEL  (C2_OPT_KSTATS: kstats = dev [80] K7/K8 counters)
   c2_stats stats{};
@@ -97,6 +100,9 @@ struct Csr {
 };
 // K0: CSR rules + |P_u| + max item / max row length (one host sync).
 int validate_csr(c2_ctx *ctx, Csr *csr);
+int validate_begin(c2_ctx *ctx, int32_t n);
+int validate_chunk(c2_ctx *ctx, const Csr &csr, int32_t u0, int32_t u1);
+int validate_finish(c2_ctx *ctx, Csr *csr, int64_t nnz);
 
 // Step 1 (k_sketch.cu + k_cluster.cu).  htab == nullptr -> hashed with params.
 struct Clusters {
@@ -106,6 +112,8 @@ struct Clusters {
 };
 int sketch(c2_ctx *ctx, const Csr &csr, int t, int b, const HashParams *hp, const uint16_t *htab, int32_t m,
            int D, uint16_t *out);
+int sketch_range(c2_ctx *ctx, const Csr &csr, int t, int b, const HashParams *hp, int32_t u0, int32_t u1,
+                 uint16_t *out);
 int fastrandomhash(c2_ctx *ctx, const Csr &csr, int t, int b, int64_t N, const HashParams *hp,
                    const uint16_t *htab, int32_t m, Clusters *out);
 // C^2/MinHash variant: one cluster per min-hash item, no splitting (chunk guard

@@ -729,7 +729,8 @@ int fastrandomhash(c2_ctx *ctx, const Csr &csr, int t, int b, int64_t N, const H
   if (rc) return rc;
   cudaEvent_t *ev = ctx->ev;
   if (ctx->timing) cudaEventRecord(ev[0], st);
-  C2_TRY(sketch(ctx, csr, t, b, hp, htab, m, C2_SKETCH_D, sk));
+  if (ctx->presketched && !htab) ctx->presketched = false;  // computed chunk by chunk during the upload
+  else C2_TRY(sketch(ctx, csr, t, b, hp, htab, m, C2_SKETCH_D, sk));
   if (ctx->timing) cudaEventRecord(ev[1], st);
 
   int32_t *key = (int32_t *)ws_get(ctx, "key", (size_t)TN * 4, &rc);

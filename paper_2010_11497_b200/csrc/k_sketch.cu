@@ -96,7 +96,10 @@ template <bool POW2>
 __global__ void __launch_bounds__(SK_WARPS * 32, 3) k_sketch_w(const int32_t *__restrict__ offs,
                                                             const int32_t *__restrict__ items, int32_t n, int t,
                                                             uint32_t b, HashArgs ha, int D,
-                                                            uint16_t *__restrict__ out) {
+                                                            uint16_t *__restrict__ out, int64_t u0 = 0,
+                                                            int64_t n_total = -1, int32_t nnz = INT32_MAX) {
+  // users [u0, u0 + n) of a CSR of n_total users (offs points at user u0); out is [t][n_total][D]
+  if (n_total < 0) n_total = n;
   __shared__ __align__(16) uint32_t bm[SK_WARPS][SK_FG * SK_CAPW];
   __shared__ __align__(16) uint16_t sv[SK_WARPS][SK_FG][C2_SKETCH_D];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -117,7 +120,8 @@ __global__ void __launch_bounds__(SK_WARPS * 32, 3) k_sketch_w(const int32_t *__
       fc[f] = f < nf ? ha.c[f0 + f] : 0;
     }
     for (int64_t u = (int64_t)blockIdx.x * SK_WARPS + w; u < n; u += nwarps) {
-      const int32_t p0 = __ldg(offs + u), p1 = __ldg(offs + u + 1);
+      // (clamped: the chunked upload path hashes rows before their validation result is read)
+      const int32_t p0 = max(__ldg(offs + u), 0), p1 = max(min(__ldg(offs + u + 1), nnz), p0);
       // first window: ~SK_K of the |P_u| hashes (uniform over [0, b)) expected inside; a multiple
       // of 512 values, so every lane's quarter of the words is a whole number of uint4
       const float wf = kb / (float)max(p1 - p0, 1);
@@ -218,7 +222,7 @@ __global__ void __launch_bounds__(SK_WARPS * 32, 3) k_sketch_w(const int32_t *__
                                    q.z & 0xFFFFu, q.z >> 16, q.w & 0xFFFFu, q.w >> 16};
 #pragma unroll
         for (int j = 0; j < C2_SKETCH_D; ++j) s[j] = j < mycnt ? s[j] : C2_ABSENT16;
-        uint16_t *o = out + ((int64_t)(f0 + myf) * n + u) * D;
+        uint16_t *o = out + ((int64_t)(f0 + myf) * n_total + u0 + u) * D;
         if (D == C2_SKETCH_D) {
           *reinterpret_cast<uint4 *>(o) = make_uint4(s[0] | (s[1] << 16), s[2] | (s[3] << 16), s[4] | (s[5] << 16),
                                                      s[6] | (s[7] << 16));
@@ -250,6 +254,28 @@ static int launch_sketch(c2_ctx *ctx, const Csr &csr, int t, int f0, int b, cons
   return C2_OK;
 }
 
+// users [u0, u1) of the hashed (no table) sketch, depth C2_SKETCH_D, into out [t][csr.n][D]
+int sketch_range(c2_ctx *ctx, const Csr &csr, int t, int b, const HashParams *hp, int32_t u0, int32_t u1,
+                 uint16_t *out) {
+  HashArgs ha;
+  for (int f = 0; f < t; ++f) {
+    ha.a[f] = hp->a[f];
+    ha.c[f] = hp->c[f];
+  }
+  const int32_t nloc = u1 - u0;
+  if (nloc <= 0) return C2_OK;
+  const bool pow2 = b >= 2 && (b & (b - 1)) == 0;
+  auto kern = pow2 ? k_sketch_w<true> : k_sketch_w<false>;
+  static int occ[2] = {0, 0};
+  if (!occ[pow2]) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ[pow2], kern, SK_WARPS * 32, 0);
+  const unsigned grid = (unsigned)std::min<int64_t>((int64_t)ctx->num_sms * std::max(occ[pow2], 1),
+                                                    ((int64_t)nloc + SK_WARPS - 1) / SK_WARPS);
+  kern<<<grid, SK_WARPS * 32, 0, ctx->stream>>>(csr.offs + u0, csr.items, nloc, t, (uint32_t)b, ha, C2_SKETCH_D, out,
+                                                 (int64_t)u0, (int64_t)csr.n, (int32_t)csr.nnz);
+  C2_LAUNCHED(ctx, "k_sketch_w");
+  return C2_OK;
+}
+
 int sketch(c2_ctx *ctx, const Csr &csr, int t, int b, const HashParams *hp, const uint16_t *htab, int32_t m, int D,
            uint16_t *out) {
   HashArgs ha;
@@ -265,7 +291,8 @@ int sketch(c2_ctx *ctx, const Csr &csr, int t, int b, const HashParams *hp, cons
     if (!occ[pow2]) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ[pow2], kern, SK_WARPS * 32, 0);
     const unsigned grid = (unsigned)std::min<int64_t>((int64_t)ctx->num_sms * std::max(occ[pow2], 1),
                                                       ((int64_t)csr.n + SK_WARPS - 1) / SK_WARPS);
-    kern<<<grid, SK_WARPS * 32, 0, ctx->stream>>>(csr.offs, csr.items, csr.n, t, (uint32_t)b, ha, D, out);
+    kern<<<grid, SK_WARPS * 32, 0, ctx->stream>>>(csr.offs, csr.items, csr.n, t, (uint32_t)b, ha, D, out, (int64_t)0,
+                                                   (int64_t)csr.n, csr.nnz > 0 ? (int32_t)csr.nnz : INT32_MAX);
     C2_LAUNCHED(ctx, "k_sketch_w");
     return C2_OK;
   }

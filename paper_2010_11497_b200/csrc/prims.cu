@@ -261,7 +261,12 @@ int radix_sort_pairs(c2_ctx *ctx, const uint32_t *keys_in, const uint32_t *vals_
 // flags[0] = first bad row (INT32_MAX if none), flags[1] = max item, flags[2] = max length,
 // flags[3] = nnz consistency (offsets[0] must be 0).
 __global__ void k_validate(const int32_t *__restrict__ offs, const int32_t *__restrict__ items, int32_t n,
-                           int32_t *__restrict__ psize, int32_t *__restrict__ flags) {
+                           int32_t *__restrict__ psize, int32_t *__restrict__ flags, int32_t u_base,
+                           const int32_t *__restrict__ last, int32_t nnz_known) {
+  // users [u_base, u_base + n) of the CSR; offs and psize point at user u_base; nnz = nnz_known
+  // if >= 0 (host entry point), else *last (the device CSR's final offset).  A row reaching
+  // outside [0, nnz) is flagged before any of its items is read.
+  const int32_t nnz = nnz_known >= 0 ? nnz_known : *last;
   int lane = threadIdx.x & 31;
   int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -269,7 +274,7 @@ __global__ void k_validate(const int32_t *__restrict__ offs, const int32_t *__re
   for (int64_t u = warp; u < n; u += nwarps) {  // warp per user, coalesced row reads
     int32_t s = offs[u], e = offs[u + 1];
     int32_t len = e - s;
-    bool bad = len <= 0 || len > 32767 || (u == 0 && s != 0);
+    bool bad = len <= 0 || len > 32767 || (u + u_base == 0 && s != 0) || s < 0 || e > nnz;
     for (int32_t p = s + lane; p < e && !bad; p += 32) {
       int32_t x = items[p];
       int32_t prev = p > s ? items[p - 1] : -1;
@@ -280,7 +285,7 @@ __global__ void k_validate(const int32_t *__restrict__ offs, const int32_t *__re
     bad = __any_sync(0xffffffffu, bad);
     if (lane == 0) {
       psize[u] = len;
-      if (bad) atomicMin(&flags[0], (int32_t)u);
+      if (bad) atomicMin(&flags[0], (int32_t)(u + u_base));
     }
     mx_len = max(mx_len, len);
   }
@@ -302,6 +307,48 @@ __global__ void k_init_flags(int32_t *flags) {
   flags[3] = 0;
 }
 
+// Chunked form (c2_build_host overlaps the CSR upload with validation): validate_begin once,
+// validate_chunk per user range as its rows arrive, validate_finish reads the flags (one sync).
+int validate_begin(c2_ctx *ctx, int32_t n) {
+  int rc;
+  ws_get(ctx, "psize", (size_t)n * 4, &rc);
+  if (rc) return rc;
+  int32_t *flags = (int32_t *)ws_get(ctx, "vflags", 64, &rc);
+  if (rc) return rc;
+  k_init_flags<<<1, 1, 0, ctx->stream>>>(flags);
+  C2_LAUNCHED(ctx, "k_init_flags");
+  return C2_OK;
+}
+int validate_chunk(c2_ctx *ctx, const Csr &csr, int32_t u0, int32_t u1) {
+  int rc;
+  int32_t *psize = (int32_t *)ws_get(ctx, "psize", (size_t)csr.n * 4, &rc);
+  if (rc) return rc;
+  int32_t *flags = (int32_t *)ws_get(ctx, "vflags", 64, &rc);
+  if (rc) return rc;
+  k_validate<<<ctx->num_sms * 8, 256, 0, ctx->stream>>>(csr.offs + u0, csr.items, u1 - u0, psize + u0, flags, u0,
+                                                         csr.offs + csr.n, (int32_t)csr.nnz);
+  C2_LAUNCHED(ctx, "k_validate");
+  return C2_OK;
+}
+int validate_finish(c2_ctx *ctx, Csr *csr, int64_t nnz) {
+  int rc;
+  int32_t *psize = (int32_t *)ws_get(ctx, "psize", (size_t)csr->n * 4, &rc);
+  if (rc) return rc;
+  int32_t *flags = (int32_t *)ws_get(ctx, "vflags", 64, &rc);
+  if (rc) return rc;
+  int32_t h[4];
+  C2_CUDA(ctx, cudaMemcpyAsync(h, flags, 16, cudaMemcpyDeviceToHost, ctx->stream));
+  C2_TRY(stream_sync(ctx, "validate"));
+  if (h[0] != INT32_MAX)
+    return set_err(ctx, C2_EDATA, "CSR row %d violates the input rules (empty, unsorted, duplicate, negative id or "
+                   "|P_u| > 32767)", h[0]);
+  csr->nnz = nnz;
+  csr->max_item = h[1];
+  csr->max_len = h[2];
+  csr->psize = psize;
+  return C2_OK;
+}
+
 int validate_csr(c2_ctx *ctx, Csr *csr) {
   int rc;
   int32_t *psize = (int32_t *)ws_get(ctx, "psize", (size_t)csr->n * 4, &rc);
@@ -311,7 +358,7 @@ int validate_csr(c2_ctx *ctx, Csr *csr) {
   k_init_flags<<<1, 1, 0, ctx->stream>>>(flags);
   C2_LAUNCHED(ctx, "k_init_flags");
   int blocks = ctx->num_sms * 8;
-  k_validate<<<blocks, 256, 0, ctx->stream>>>(csr->offs, csr->items, csr->n, psize, flags);
+  k_validate<<<blocks, 256, 0, ctx->stream>>>(csr->offs, csr->items, csr->n, psize, flags, 0, csr->offs + csr->n, -1);
   C2_LAUNCHED(ctx, "k_validate");
   int32_t h[5];
   C2_CUDA(ctx, cudaMemcpyAsync(h, flags, 16, cudaMemcpyDeviceToHost, ctx->stream));

@@ -195,3 +195,15 @@ def test_repeated_builds_match_digests(ctx, cfg):
     for nbr, inter, uni, sim in outs:
         assert sha(npy(nbr)) == rec["nbr_sha256"]
         assert sha(npy(inter)) == rec["inter_sha256"] and sha(npy(uni)) == rec["uni_sha256"]
+
+
+@pytest.mark.parametrize("cfg", ["c4", "c5"])
+def test_build_host_all_users_bytewise(ctx, cfg):
+    """c2_build_host (host buffers, chunked upload overlapped with validation and sketch) equals the
+    oracle on every user."""
+    rec = golden(cfg, 0)
+    C = synth.config(cfg)
+    offs, items = synth.generate(cfg)
+    nbr, inter, uni, sim = c2.build_host(offs, items, k=C.k, t=C.t, b=C.b, N=C.N, seed=C.hash_seed, ctx=ctx)
+    assert sha(nbr) == rec["nbr_sha256"] and sha(inter) == rec["inter_sha256"] and sha(uni) == rec["uni_sha256"]
+    assert sha(sim) == rec["sim_sha256"]

@@ -559,3 +559,41 @@ def test_split_device_loop_fewer_syncs():
         c.close()
     assert syncs[1] < syncs[0]
     assert syncs[1] <= 3, syncs
+
+
+# ------------------------------------------------------------------ c2_build_host: chunked upload
+@pytest.mark.parametrize("n", [1, 2, 5, 9, 40])
+@pytest.mark.parametrize("clustering", [0, 1])
+def test_build_host_small_and_minhash(ctx, n, clustering):
+    """The host entry point uploads the CSR in up to 8 user chunks, validating and sketching each
+    as it arrives; fewer users than chunks, and the MinHash clustering (no sketch), still give the
+    device entry point's result."""
+    rng = np.random.default_rng(900 + n)
+    offs, items = synth.random_instance(rng, n, 60, 1, 25)
+    ctx.set_option(c2.OPT_CLUSTERING, clustering)
+    try:
+        a = c2.build(dev(offs), dev(items), k=7, t=3, b=16, N=4, seed=5, ctx=ctx)
+        h = c2.build_host(offs, items, k=7, t=3, b=16, N=4, seed=5, ctx=ctx)
+    finally:
+        ctx.set_option(c2.OPT_CLUSTERING, 0)
+    for x, y in zip(a, h):
+        assert np.array_equal(npy(x), y)
+
+
+@pytest.mark.parametrize("where", ["first", "middle", "last"])
+def test_build_host_reports_bad_row(ctx, where):
+    """A rule violation in any upload chunk is reported as C2_EDATA with that row's index, and the
+    context stays usable (the next call's sketch is recomputed)."""
+    C = synth.config("c1")
+    offs, items = synth.generate("c1")
+    n = len(offs) - 1
+    row = {"first": 0, "middle": n // 2, "last": n - 1}[where]
+    bad = items.copy()
+    p0, p1 = offs[row], offs[row + 1]
+    bad[p0:p1] = bad[p0:p1][::-1]  # unsorted row (profiles have >= 5 items)
+    with pytest.raises(c2.C2Error) as ei:
+        c2.build_host(offs, bad, k=C.k, t=C.t, b=C.b, N=C.N, seed=C.hash_seed, ctx=ctx)
+    assert f"row {row}" in str(ei.value)
+    a = c2.build(dev(offs), dev(items), k=C.k, t=C.t, b=C.b, N=C.N, seed=C.hash_seed, ctx=ctx)
+    o = oracle.build_graph(offs, items, k=C.k, t=C.t, b=C.b, N=C.N, seed=C.hash_seed)
+    assert np.array_equal(npy(a[0]), o["nbr"])
