@@ -435,14 +435,6 @@ __global__ void __launch_bounds__(256, 4) k_split_dev(SplitDev sd, const uint16_
 }
 
 // ------------------------------------------------------------------ canonical form
-__global__ void k_count_keys(const int32_t *__restrict__ key, int64_t TN, int32_t *__restrict__ size) {
-  int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const bool valid = q < TN;
-  const unsigned mask = __ballot_sync(0xffffffffu, valid);
-  if (!valid) return;
-  int32_t k = key[q];
-  c2d::agg_inc(mask, &size[k], k);
-}
 
 __global__ void __launch_bounds__(256) k_max(const int32_t *__restrict__ x, int64_t E, int32_t *__restrict__ out,
                                              const long long *__restrict__ dE = nullptr) {
@@ -463,17 +455,22 @@ __global__ void __launch_bounds__(256) k_max(const int32_t *__restrict__ x, int6
   }
 }
 
-__global__ void k_rep(const int32_t *__restrict__ key, int64_t TN, int32_t n, int32_t *__restrict__ rep) {
-  // rep[node] = smallest member; lanes hold ascending q, so among the lanes of one node the lowest
-  // lane carries the smallest user (within one function) and alone does the atomicMin
+// node sizes and smallest members in one pass; lanes hold ascending q, so among the lanes of one
+// node the lowest carries its smallest user in this warp (nodes never span functions)
+__global__ void k_count_rep(const int32_t *__restrict__ key, int64_t TN, int32_t n, int32_t *__restrict__ size,
+                            int32_t *__restrict__ rep) {
   int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const bool valid = q < TN;
   const unsigned mask = __ballot_sync(0xffffffffu, valid);
   if (!valid) return;
   const int32_t k = key[q];
   const unsigned peers = __match_any_sync(mask, k);
-  if ((int)(threadIdx.x & 31) == __ffs(peers) - 1) atomicMin(&rep[k], (int32_t)(q % n));
+  if ((int)(threadIdx.x & 31) == __ffs(peers) - 1) {  // lowest lane: smallest user of the node in this warp
+    atomicAdd(&size[k], __popc(peers));
+    atomicMin(&rep[k], (int32_t)(q % n));
+  }
 }
+
 
 __global__ void k_heads(const int32_t *__restrict__ key, const int32_t *__restrict__ rep, int64_t TN, int32_t n,
                         int32_t *__restrict__ head) {
@@ -595,8 +592,11 @@ static int canonicalize(c2_ctx *ctx, int32_t n, int t, int64_t N, int32_t *key, 
   int32_t *size = (int32_t *)ws_get(ctx, "nsize", (size_t)(next_id + TN + 1) * 4, &rc);
   if (rc) return rc;
   C2_CUDA(ctx, cudaMemsetAsync(size, 0, (size_t)next_id * 4, st));
-  k_count_keys<<<nblk(TN), 256, 0, st>>>(key, TN, size);
-  C2_LAUNCHED(ctx, "k_count_keys");
+  int32_t *rep = (int32_t *)ws_get(ctx, "rep", (size_t)(next_id + TN + 1) * 4, &rc);
+  if (rc) return rc;
+  C2_CUDA(ctx, cudaMemsetAsync(rep, 0x7F, (size_t)next_id * 4, st));
+  k_count_rep<<<nblk(TN), 256, 0, st>>>(key, TN, n, size, rep);
+  C2_LAUNCHED(ctx, "k_count_rep");
   int32_t *mx = (int32_t *)(acc + 2);
   C2_CUDA(ctx, cudaMemsetAsync(mx, 0, 4, st));
   k_max<<<std::min<unsigned>(nblk(next_id), ctx->num_sms * 8), 256, 0, st>>>(size, next_id, mx, dev_split);
@@ -653,15 +653,13 @@ static int canonicalize(c2_ctx *ctx, int32_t n, int t, int64_t N, int32_t *key, 
     size = (int32_t *)ws_get(ctx, "nsize", (size_t)(next_id + 1) * 4, &rc);
     if (rc) return rc;
     C2_CUDA(ctx, cudaMemsetAsync(size, 0, (size_t)next_id * 4, st));
-    k_count_keys<<<nblk(TN), 256, 0, st>>>(key, TN, size);
-    C2_LAUNCHED(ctx, "k_count_keys");
+    rep = (int32_t *)ws_get(ctx, "rep", (size_t)(next_id + 1) * 4, &rc);
+    if (rc) return rc;
+    C2_CUDA(ctx, cudaMemsetAsync(rep, 0x7F, (size_t)next_id * 4, st));
+    k_count_rep<<<nblk(TN), 256, 0, st>>>(key, TN, n, size, rep);
+    C2_LAUNCHED(ctx, "k_count_rep");
   }
-  // rep[node] = smallest member; heads; canonical cluster index by scan over users
-  int32_t *rep = (int32_t *)ws_get(ctx, "rep", (size_t)next_id * 4, &rc);
-  if (rc) return rc;
-  C2_CUDA(ctx, cudaMemsetAsync(rep, 0x7F, (size_t)next_id * 4, st));
-  k_rep<<<nblk(TN), 256, 0, st>>>(key, TN, n, rep);
-  C2_LAUNCHED(ctx, "k_rep");
+  // (rep[node] = smallest member, from k_count_rep); heads; canonical cluster index by scan over users
   int32_t *head = (int32_t *)ws_get(ctx, "head", (size_t)(2 * TN + 2) * 4, &rc);
   if (rc) return rc;
   int32_t *hscan = head + TN + 1;
