@@ -99,6 +99,13 @@ __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.
 #ifndef C2_FILL_COAL
 #define C2_FILL_COAL 1  // multi-window packing: k_sl_fill_coal (coalesced CSR reads) instead of k_sl_fill_rows
 #endif
+#ifndef C2_PACK32
+#define C2_PACK32 0  // 1: packed member lists hold 32-bit byte offsets into the mask M (4 per 16-byte row and
+                     // lane; the probe's mask loads need no id extraction) instead of 16-bit ids (8 per row).
+                     // Measured at c5: the probe loop drops from ~143 to ~67 instructions per 16 items,
+                     // yet the tile kernel takes 35.3 vs 34.4 ms and the packing 2.8 vs 2.0 ms (twice
+                     // the bytes): the probe is not issue-bound.  Off by default; parity-tested.
+#endif
 #ifndef C2_SMEM_BUDGET
 #define C2_SMEM_BUDGET 0  // bytes of dynamic shared memory per tile CTA (0: the opt-in maximum)
 #endif
@@ -107,6 +114,24 @@ constexpr int TILE_WARPS = TILE_T / 32;
 constexpr int MAX_WIN = 16;
 
 static inline unsigned nblk(int64_t x, int bs = 256) { return (unsigned)((x + bs - 1) / bs); }
+
+// Packed member lists: per (32-member slice, window) block, rows of 512 bytes; row t holds, for
+// the member in lane e, its list positions IPR*t .. IPR*t+IPR-1 as PackT: the window-local item
+// id (16-bit) or its byte offset in the mask M (32-bit, C2_PACK32).  Pads: enc(W), with M[W] = 0.
+constexpr int IPR = C2_PACK32 ? 4 : 8;
+typedef std::conditional<C2_PACK32 != 0, uint32_t, uint16_t>::type PackT;
+__host__ __device__ __forceinline__ PackT pk_enc(uint32_t id) { return (PackT)(C2_PACK32 ? id * 4u : id); }
+__device__ __forceinline__ PackT *pk_row_ptr(PackT *base, int64_t blk_off, int e) {
+  return base + blk_off * (32 * IPR) + e * IPR;
+}
+__device__ __forceinline__ int64_t pk_idx(int pos) { return (int64_t)(pos / IPR) * (32 * IPR) + (pos % IPR); }
+// rows of a block holding c items per member; 32-bit packing rounds to whole quads of rows (the
+// probe's step) so its loads never need a bounds test
+__host__ __device__ __forceinline__ int32_t pk_rows(int32_t c) {
+  const int32_t r = (c + IPR - 1) / IPR;
+  return C2_PACK32 ? (r + 3) & ~3 : r;
+}
+constexpr int PK_SLACK_ROWS = 8;  // rows readable past any block (prefetch of the probe's next step)
 static inline int bits_for(int64_t x) {
   int b = 1;
   while ((1LL << b) < x) ++b;
@@ -381,7 +406,7 @@ __global__ void k_sl_len(const Tile *__restrict__ tiles, int64_t nslices, const 
     p = q;
 #pragma unroll
     for (int o = 16; o; o >>= 1) c = max(c, __shfl_xor_sync(0xffffffffu, c, o));
-    if (lane == 0) blk_len8[sl * nwin + w] = (c + 7) / 8;
+    if (lane == 0) blk_len8[sl * nwin + w] = pk_rows(c);
   }
 }
 
@@ -392,7 +417,7 @@ __global__ void k_sl_len(const Tile *__restrict__ tiles, int64_t nslices, const 
 __global__ void __launch_bounds__(256) k_sl_fill(int64_t nslices, const int32_t *__restrict__ bounds,
                                                  const int32_t *__restrict__ items, int32_t W, int nwin,
                                                  const int32_t *__restrict__ blk_len8,
-                                                 const int32_t *__restrict__ blk_off8, uint16_t *__restrict__ packed16,
+                                                 const int32_t *__restrict__ blk_off8, PackT *__restrict__ packedT,
                                                  int bank_order) {
   __shared__ int hist[8][32];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
@@ -406,8 +431,8 @@ __global__ void __launch_bounds__(256) k_sl_fill(int64_t nslices, const int32_t 
     const int32_t lo = w * W;
     // this window's items: the contiguous range [pb, pe) of the sorted row (from k_sl_len)
     const int32_t pb = bd[w], pe = bd[w + 1];
-    const int32_t len = blk_len8[sl * nwin + w] * 8;
-    uint16_t *dst = packed16 + (int64_t)blk_off8[sl * nwin + w] * 256 + e * 8;
+    const int32_t len = blk_len8[sl * nwin + w] * IPR;
+    PackT *dst = pk_row_ptr(packedT, blk_off8[sl * nwin + w], e);
     if (!bank_order) {  // plain order: one pass, ballot compaction
       int cnt = 0;
       for (int32_t p0 = pb; p0 < pe; p0 += 32) {
@@ -416,10 +441,10 @@ __global__ void __launch_bounds__(256) k_sl_fill(int64_t nslices, const int32_t 
         const bool in = r >= 0 && r < W;
         const unsigned bal = __ballot_sync(0xffffffffu, in);
         const int pos = cnt + __popc(bal & ((1u << lane) - 1));
-        if (in) dst[(pos >> 3) * 256 + (pos & 7)] = (uint16_t)r;
+        if (in) dst[pk_idx(pos)] = pk_enc((uint32_t)r);
         cnt += __popc(bal);
       }
-      for (int pos = cnt + lane; pos < len; pos += 32) dst[(pos >> 3) * 256 + (pos & 7)] = (uint16_t)W;
+      for (int pos = cnt + lane; pos < len; pos += 32) dst[pk_idx(pos)] = pk_enc((uint32_t)W);
       continue;
     }
     h[lane] = 0;
@@ -447,10 +472,10 @@ __global__ void __launch_bounds__(256) k_sl_fill(int64_t nslices, const int32_t 
       const int32_t r = p < pe ? items[p] - lo : -1;
       if (r >= 0 && r < W) {
         const int pos = atomicAdd(&h[(r - e) & 31], 1);
-        dst[(pos >> 3) * 256 + (pos & 7)] = (uint16_t)r;
+        dst[pk_idx(pos)] = pk_enc((uint32_t)r);
       }
     }
-    for (int pos = cnt + lane; pos < len; pos += 32) dst[(pos >> 3) * 256 + (pos & 7)] = (uint16_t)W;
+    for (int pos = cnt + lane; pos < len; pos += 32) dst[pk_idx(pos)] = pk_enc((uint32_t)W);
     __syncwarp();
   }
 }
@@ -460,6 +485,7 @@ __global__ void __launch_bounds__(256) k_sl_fill(int64_t nslices, const int32_t 
 // 16-byte row t of a (slice, window) block: lane e gathers positions 8t..8t+7 of member e and the
 // warp writes the block's 512-byte row t with one coalesced uint4 store per lane (the per-list
 // form wrote 2-byte scattered stores, i.e. partial sectors).
+#if !C2_PACK32
 __global__ void __launch_bounds__(256) k_sl_fill_rows(int64_t nb, int nwin, const int32_t *__restrict__ bounds,
                                                       const int32_t *__restrict__ items, int32_t W,
                                                       const int32_t *__restrict__ blk_len8,
@@ -507,6 +533,7 @@ __global__ void __launch_bounds__(256) k_sl_fill_rows(int64_t nb, int nwin, cons
     }
   }
 }
+#endif
 
 // Same output as k_sl_fill_rows, with the CSR read coalesced: one warp per (slice, window) block
 // takes its 32 members one after the other, the lanes reading consecutive items of a member (full
@@ -519,13 +546,14 @@ __global__ void __launch_bounds__(FR_WARPS * 32) k_sl_fill_coal(int64_t nb, int 
                                                                const int32_t *__restrict__ blk_len8,
                                                                const int32_t *__restrict__ blk_off8,
                                                                uint4 *__restrict__ packed) {
-  __shared__ __align__(16) uint16_t stage[FR_WARPS][FR_R * 32 * 8];
+  __shared__ __align__(16) PackT stage[FR_WARPS][FR_R * 32 * IPR];
+  constexpr int NH = FR_R * IPR / 32;  // loads per member and chunk
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  uint16_t *stg = stage[wib];
+  PackT *stg = stage[wib];
   uint4 *stg4 = reinterpret_cast<uint4 *>(stg);
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwg = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  const uint32_t pw = (uint32_t)W | ((uint32_t)W << 16);
+  const uint32_t pw = C2_PACK32 ? (uint32_t)pk_enc((uint32_t)W) : ((uint32_t)W | ((uint32_t)W << 16));
   const uint4 padv = make_uint4(pw, pw, pw, pw);
   for (int64_t b = gw; b < nb; b += nwg) {
     const int64_t sl = b / nwin;
@@ -539,32 +567,29 @@ __global__ void __launch_bounds__(FR_WARPS * 32) k_sl_fill_coal(int64_t nb, int 
       const int nr = min(FR_R, len8 - t0);
       for (int i = lane; i < nr * 32; i += 32) stg4[i] = padv;
       __syncwarp();
-      // members in groups of 8: the group's first 64 items each are all requested before any is
-      // stored (16 loads in flight per lane); longer chunks (FR_R > 8) finish in a second loop
+      // members in groups of 8: the group's chunk items (FR_R * IPR each) are all requested
+      // before any is stored (8 * NH loads in flight per lane)
       for (int e0 = 0; e0 < 32; e0 += 8) {
-        int32_t pbv[8], pev[8], xv[8][2];
+        int32_t pbv[8], pev[8], xv[8][NH];
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
-          pbv[i] = __shfl_sync(0xffffffffu, mpb, e0 + i) + 8 * t0;
-          pev[i] = min(__shfl_sync(0xffffffffu, mpe, e0 + i), pbv[i] + 8 * nr);
+          pbv[i] = __shfl_sync(0xffffffffu, mpb, e0 + i) + IPR * t0;
+          pev[i] = min(__shfl_sync(0xffffffffu, mpe, e0 + i), pbv[i] + IPR * nr);
         }
 #pragma unroll
         for (int i = 0; i < 8; ++i)
 #pragma unroll
-          for (int h = 0; h < 2; ++h) {
+          for (int h = 0; h < NH; ++h) {
             const int32_t p = pbv[i] + 32 * h + lane;
             xv[i][h] = p < pev[i] ? __ldg(items + p) : 0;
           }
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
 #pragma unroll
-          for (int h = 0; h < 2; ++h) {
+          for (int h = 0; h < NH; ++h) {
             const int pos = 32 * h + lane;
-            if (pbv[i] + pos < pev[i]) stg[((pos >> 3) * 32 + e0 + i) * 8 + (pos & 7)] = (uint16_t)(xv[i][h] - lo);
-          }
-          for (int32_t p = pbv[i] + 64 + lane; p < pev[i]; p += 32) {
-            const int pos = p - pbv[i];
-            stg[((pos >> 3) * 32 + e0 + i) * 8 + (pos & 7)] = (uint16_t)(__ldg(items + p) - lo);
+            if (pbv[i] + pos < pev[i])
+              stg[((pos / IPR) * 32 + e0 + i) * IPR + (pos % IPR)] = pk_enc((uint32_t)(xv[i][h] - lo));
           }
         }
       }
@@ -600,7 +625,7 @@ __global__ void k_sl_maxlen(const Tile *__restrict__ tiles, int64_t nslices, con
   int c = v >= 0 ? psize[v] : 0;
 #pragma unroll
   for (int o = 16; o; o >>= 1) c = max(c, __shfl_xor_sync(0xffffffffu, c, o));
-  if (lane == 0) len8[sl] = (c + 7) / 8;
+  if (lane == 0) len8[sl] = pk_rows(c);
 }
 
 constexpr int RL_T = 256;
@@ -615,7 +640,7 @@ __global__ void __launch_bounds__(RL_T) k_relabel(BigC *__restrict__ bcs, int64_
                                                  const int32_t *__restrict__ vperm, const int32_t *__restrict__ offs,
                                                  const int32_t *__restrict__ items, int32_t nw,
                                                  const int32_t *__restrict__ blk_off8, int32_t *__restrict__ blk_len8,
-                                                 uint16_t *__restrict__ packed16, int *__restrict__ counter,
+                                                 PackT *__restrict__ packedT, int *__restrict__ counter,
                                                  int *__restrict__ max_kc) {
   extern __shared__ __align__(16) uint32_t rsm[];
   uint32_t *seen = rsm, *seen2 = rsm + nw, *wslot = rsm + 2 * nw, *touched = rsm + 3 * nw, *tbase = rsm + 4 * nw;
@@ -692,7 +717,7 @@ __global__ void __launch_bounds__(RL_T) k_relabel(BigC *__restrict__ bcs, int64_
       const int32_t v = i < b.s ? vp[i] : -1;
       int cnt = 0;
       if (v >= 0) {
-        uint16_t *dst = packed16 + (int64_t)blk_off8[b.sl_off + (i >> 5)] * 256 + (i & 31) * 8;
+        PackT *dst = pk_row_ptr(packedT, blk_off8[b.sl_off + (i >> 5)], i & 31);
         for (int32_t p0 = offs[v]; p0 < offs[v + 1]; p0 += 32) {
           const int32_t p = p0 + lane;
           bool keep = false;
@@ -705,7 +730,7 @@ __global__ void __launch_bounds__(RL_T) k_relabel(BigC *__restrict__ bcs, int64_
           }
           const unsigned bal = __ballot_sync(0xffffffffu, keep);
           const int pos = cnt + __popc(bal & ((1u << lane) - 1));
-          if (keep) dst[(pos >> 3) * 256 + (pos & 7)] = (uint16_t)lid;
+          if (keep) dst[pk_idx(pos)] = pk_enc(lid);
           cnt += __popc(bal);
         }
       }
@@ -717,11 +742,11 @@ __global__ void __launch_bounds__(RL_T) k_relabel(BigC *__restrict__ bcs, int64_
       int mx = slen[i];
 #pragma unroll
       for (int o = 16; o; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-      const int len8 = (mx + 7) / 8;
+      const int len8 = pk_rows(mx);
       const int sl = b.sl_off + (i >> 5);
       if ((i & 31) == 0) blk_len8[sl] = len8;
-      uint16_t *dst = packed16 + (int64_t)blk_off8[sl] * 256 + (i & 31) * 8;
-      for (int pos = slen[i]; pos < len8 * 8; ++pos) dst[(pos >> 3) * 256 + (pos & 7)] = (uint16_t)kc;
+      PackT *dst = pk_row_ptr(packedT, blk_off8[sl], i & 31);
+      for (int pos = slen[i]; pos < len8 * IPR; ++pos) dst[pk_idx(pos)] = pk_enc(kc);
     }
     for (int i = tid; i < nt; i += RL_T) {
       const uint32_t w = touched[i];
@@ -825,6 +850,15 @@ __device__ __forceinline__ void masks8(const uint32_t *__restrict__ M, uint4 d, 
   m[5] = M[d.z >> 16];
   m[6] = M[d.w & 0xFFFFu];
   m[7] = M[d.w >> 16];
+}
+
+// 4 masks of one uint4 of byte offsets into M (C2_PACK32)
+__device__ __forceinline__ void masks4b(const uint32_t *__restrict__ M, uint4 d, uint32_t *m) {
+  const char *Mb = reinterpret_cast<const char *>(M);
+  m[0] = *reinterpret_cast<const uint32_t *>(Mb + d.x);
+  m[1] = *reinterpret_cast<const uint32_t *>(Mb + d.y);
+  m[2] = *reinterpret_cast<const uint32_t *>(Mb + d.z);
+  m[3] = *reinterpret_cast<const uint32_t *>(Mb + d.w);
 }
 
 template <int NHI>
@@ -1017,17 +1051,24 @@ __global__ void __launch_bounds__(TILE_T, C2_TILE_MINB) k_local_tile(TileArgs a)
         const bool stgd = s_stg[cur] != 0;
         const int32_t n4r = s_bl[cur][w] * 32;
         const uint4 *srcr = stgd ? stg + s_so[cur][w] : a.packed + (int64_t)s_bo[cur][w] * 32;
-        const uint32_t pw = W | (W << 16);
+        const uint32_t pw = C2_PACK32 ? (uint32_t)pk_enc(W) : (W | (W << 16));
         const uint4 padv = make_uint4(pw, pw, pw, pw);
         const uint4 dkeep = tid < n4r ? srcr[tid] : padv;
         for (int gi = tid; gi < n4r; gi += TILE_T) {
           const uint4 d = gi == tid ? dkeep : srcr[gi];
           const uint32_t bit = 1u << (gi & 31);
+#if C2_PACK32
+          const uint32_t xs[4] = {d.x, d.y, d.z, d.w};  // byte offsets into M
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            if (xs[q] < 4u * W) atomicOr(reinterpret_cast<uint32_t *>(reinterpret_cast<char *>(M) + xs[q]), bit);
+#else
           const uint32_t xs[8] = {d.x & 0xFFFFu, d.x >> 16, d.y & 0xFFFFu, d.y >> 16,
                                   d.z & 0xFFFFu, d.z >> 16, d.w & 0xFFFFu, d.w >> 16};
 #pragma unroll
           for (int q = 0; q < 8; ++q)
             if (xs[q] < W) atomicOr(&M[xs[q]], bit);
+#endif
         }
         __syncthreads();
         // the next tile's row blocks go to the other staging buffer as soon as its record is in
@@ -1045,6 +1086,46 @@ __global__ void __launch_bounds__(TILE_T, C2_TILE_MINB) k_local_tile(TileArgs a)
             const int32_t len8 = own ? s_bl[cur][w] : a.blk_len8[bi];
             const uint4 *src = (own ? stg + s_so[cur][w] : a.packed + (int64_t)a.blk_off8[bi] * 32) + lane;
             auto ld = [&](int32_t p) { return p < len8 ? src[(int64_t)p * 32] : padv; };
+#if C2_PACK32
+            // rows of 4 byte offsets per lane; 16 items (4 rows) per step, the next step in flight
+            int32_t plo = 0, phi = len8;  // this warp's part of the lists (quads of rows)
+            if (G > 1) {
+              const int32_t np = (len8 + 3) >> 2;
+              plo = 4 * ((part * np) / G);
+              phi = 4 * (((part + 1) * np) / G);
+            }
+            // blocks are whole quads of rows with >= PK_SLACK_ROWS readable rows after them (global:
+            // allocation slack; staged: shared-memory slack), so the step loads need no bounds test
+            (void)ld;
+            const uint4 *sp = src + (int64_t)plo * 32;
+            auto step = [&](const uint4 &d0, const uint4 &d1, const uint4 &d2, const uint4 &d3) {
+              uint32_t m[8];
+              masks4b(M, d0, m);
+              masks4b(M, d1, m + 4);
+              uint32_t e8a = C[q].add8(m);
+              masks4b(M, d2, m);
+              masks4b(M, d3, m + 4);
+              uint32_t e8b = C[q].add8(m);
+              C[q].add16(e8a, e8b);
+            };
+            uint4 a0 = sp[0], a1 = sp[32], a2 = sp[64], a3 = sp[96];
+            int32_t p4 = plo;
+            for (; p4 + 4 < phi; p4 += 8) {  // two steps per iteration (ping-pong, no register moves)
+              const uint4 b0 = sp[128], b1 = sp[160], b2 = sp[192], b3 = sp[224];
+              step(a0, a1, a2, a3);
+              a0 = sp[256];
+              a1 = sp[288];
+              a2 = sp[320];
+              a3 = sp[352];
+              step(b0, b1, b2, b3);
+              sp += 256;
+              nsteps += 2;
+            }
+            if (p4 < phi) {
+              step(a0, a1, a2, a3);
+              ++nsteps;
+            }
+#else
             int32_t plo = 0, phi = len8;  // this warp's part of the lists (pairs of 8-item groups)
             if (G > 1) {
               const int32_t np = (len8 + 1) >> 1;
@@ -1066,6 +1147,7 @@ __global__ void __launch_bounds__(TILE_T, C2_TILE_MINB) k_local_tile(TileArgs a)
               n1 = f1;
               ++nsteps;
             }
+#endif
           }
         }
         if (a.kstats && lane == 0 && s > 1024) {  // probe busy time per step (big tiles)
@@ -1076,11 +1158,18 @@ __global__ void __launch_bounds__(TILE_T, C2_TILE_MINB) k_local_tile(TileArgs a)
         // ---- clear M
         for (int gi = tid; gi < n4r; gi += TILE_T) {
           const uint4 d = gi == tid ? dkeep : srcr[gi];
+#if C2_PACK32
+          const uint32_t xs[4] = {d.x, d.y, d.z, d.w};
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            if (xs[q] < 4u * W) *reinterpret_cast<uint32_t *>(reinterpret_cast<char *>(M) + xs[q]) = 0;
+#else
           const uint32_t xs[8] = {d.x & 0xFFFFu, d.x >> 16, d.y & 0xFFFFu, d.y >> 16,
                                   d.z & 0xFFFFu, d.z >> 16, d.w & 0xFFFFu, d.w >> 16};
 #pragma unroll
           for (int q = 0; q < 8; ++q)
             if (xs[q] < W) M[xs[q]] = 0;
+#endif
         }
         if (lt && w == nwin - 1 && warp == TILE_WARPS - 1) {
           // light rows: the running k-th best tau (one global read per row) as a Ref
@@ -1576,7 +1665,7 @@ int local_knn(c2_ctx *ctx, const Csr &csr_in, int t, const Clusters &cl, int k, 
       int32_t tot8;
       C2_CUDA(ctx, cudaMemcpyAsync(&tot8, blk_off8 + nslices, 4, cudaMemcpyDeviceToHost, st));
       C2_TRY(stream_sync(ctx, "packed size"));
-      packed = (uint4 *)ws_get(ctx, "packed", (size_t)tot8 * 32 * 16 + 16, &rc);
+      packed = (uint4 *)ws_get(ctx, "packed", ((size_t)tot8 + PK_SLACK_ROWS) * 32 * 16 + 16, &rc);
       if (rc) return rc;
       int *rl = (int *)ws_get(ctx, "relabel_ctr", 16, &rc);
       if (rc) return rc;
@@ -1585,7 +1674,7 @@ int local_knn(c2_ctx *ctx, const Csr &csr_in, int t, const Clusters &cl, int k, 
       int rl_occ = 1;
       C2_CUDA(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&rl_occ, k_relabel, RL_T, rl_smem));
       k_relabel<<<ctx->num_sms * std::max(rl_occ, 1), RL_T, rl_smem, st>>>(bcs, ncl, vperm, csr.offs, csr.items, nwq, blk_off8, blk_len8,
-                                                     reinterpret_cast<uint16_t *>(packed), rl, rl + 1);
+                                                     reinterpret_cast<PackT *>(packed), rl, rl + 1);
       C2_LAUNCHED(ctx, "k_relabel");
       int32_t hkc;
       C2_CUDA(ctx, cudaMemcpyAsync(&hkc, rl + 1, 4, cudaMemcpyDeviceToHost, st));
@@ -1618,12 +1707,12 @@ int local_knn(c2_ctx *ctx, const Csr &csr_in, int t, const Clusters &cl, int k, 
       int32_t tot8;
       C2_CUDA(ctx, cudaMemcpyAsync(&tot8, blk_off8 + nb, 4, cudaMemcpyDeviceToHost, st));
       C2_TRY(stream_sync(ctx, "packed size"));
-      packed = (uint4 *)ws_get(ctx, "packed", (size_t)tot8 * 32 * 16 + 16, &rc);
+      packed = (uint4 *)ws_get(ctx, "packed", ((size_t)tot8 + PK_SLACK_ROWS) * 32 * 16 + 16, &rc);
       if (rc) return rc;
       // bank-rotated order pays for its second pass only when lists are long (one window)
       if (nwin == 1) {
         k_sl_fill<<<nblk(nslices * 32 * 32), 256, 0, st>>>(nslices, bounds, csr.items, W, nwin, blk_len8, blk_off8,
-                                                           reinterpret_cast<uint16_t *>(packed), 1);
+                                                           reinterpret_cast<PackT *>(packed), 1);
         C2_LAUNCHED(ctx, "k_sl_fill");
       } else {
         if (C2_FILL_COAL) {
@@ -1631,10 +1720,12 @@ int local_knn(c2_ctx *ctx, const Csr &csr_in, int t, const Clusters &cl, int k, 
                                                                       packed);
           C2_LAUNCHED(ctx, "k_sl_fill_coal");
         } else {
+#if !C2_PACK32
           const int vec = ((uintptr_t)csr.items & 15) == 0 ? 1 : 0;
           k_sl_fill_rows<<<ctx->num_sms * 16, 256, 0, st>>>(nb, nwin, bounds, csr.items, W, blk_len8, blk_off8, packed,
                                                             csr.nnz, vec);
           C2_LAUNCHED(ctx, "k_sl_fill_rows");
+#endif
         }
       }
     }
@@ -1693,9 +1784,10 @@ int local_knn(c2_ctx *ctx, const Csr &csr_in, int t, const Clusters &cl, int k, 
     const size_t scr_own = (size_t)W + 1 >= scrw ? 0 : scrw;
     scr_off = scr_own ? (int32_t)mw : 0;
     stg_off = (int32_t)(mw + scr_own);
-    stg_cap = (int32_t)std::min<int64_t>(2048, ((int64_t)budget / 4 - stg_off) / 8);  // 16-byte groups, each
+    const int64_t slack_w = C2_PACK32 ? PK_SLACK_ROWS * 32 * 4 : 0;  // words readable past the staging
+    stg_cap = (int32_t)std::min<int64_t>(2048, ((int64_t)budget / 4 - stg_off - slack_w) / 8);  // 16-byte groups, each
     if (stg_cap < 64) stg_cap = 0;
-    smem = ((size_t)stg_off + (size_t)stg_cap * 8) * 4;
+    smem = ((size_t)stg_off + (size_t)stg_cap * 8 + (size_t)slack_w) * 4;
     tk = pick_tile(nhi, vpt);
     C2_CUDA(ctx, cudaFuncSetAttribute(tk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int occ = 0;
