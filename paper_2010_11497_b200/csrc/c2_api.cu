@@ -178,6 +178,12 @@ void c2_ctx_destroy(c2_ctx *ctx) {
   for (auto &e : ctx->ev)
     if (e) cudaEventDestroy(e);
   for (auto &e : ctx->tile_ev) cudaEventDestroy(e);
+  if (ctx->side_stream) {
+    cudaStreamSynchronize(ctx->side_stream);
+    cudaStreamDestroy(ctx->side_stream);
+    for (auto &e : ctx->side_ev)
+      if (e) cudaEventDestroy(e);
+  }
   if (ctx->copy_stream) {
     cudaStreamSynchronize(ctx->copy_stream);
     cudaStreamDestroy(ctx->copy_stream);

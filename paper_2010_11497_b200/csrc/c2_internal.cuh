@@ -43,6 +43,8 @@ struct c2_ctx {
   int surv_qmax = 1024;  // C2_OPT_SURVIVORS: light-row survivor slots per user (0: off; capped to 8 GiB of slots)
   bool gf_tensor = false;  // C2_OPT_GF_TENSOR: GoldFinger big clusters on the tensor cores (k_gf_mma; measured slower, off)
   bool presketched = false;  // c2_build_host: the sketch of the next fastrandomhash call is already in "sketch"
+  cudaStream_t side_stream = nullptr;  // Step 2: light rows' merge concurrent with the per-row top-k
+  cudaEvent_t side_ev[2] = {};
   cudaStream_t copy_stream = nullptr;  // c2_build_host: chunked H2D upload overlapping validation + sketch
   cudaEvent_t chunk_ev[16] = {};
   bool split_dev = true;  // C2_OPT_SPLIT_DEVICE: device-side split loop (k_split_dev)

@@ -99,6 +99,9 @@ __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.
 #ifndef C2_FILL_COAL
 #define C2_FILL_COAL 1  // multi-window packing: k_sl_fill_coal (coalesced CSR reads) instead of k_sl_fill_rows
 #endif
+#ifndef C2_SIDE_MERGE
+#define C2_SIDE_MERGE 1  // light rows' merge on a side stream, concurrent with k_row_topk
+#endif
 #ifndef C2_PACK32
 #define C2_PACK32 0  // 1: packed member lists hold 32-bit byte offsets into the mask M (4 per 16-byte row and
                      // lane; the probe's mask loads need no id extraction) instead of 16-bit ids (8 per row).
@@ -1893,8 +1896,23 @@ int local_knn(c2_ctx *ctx, const Csr &csr_in, int t, const Clusters &cl, int k, 
       C2_TRY(launch_tiles(blo, bhi, 2 * f, f));
     }
     C2_TRY(launch_tiles(nbigtiles + mix_lo[f], nbigtiles + mix_lo[f + 1], 2 * f + 1, f));
-    C2_TRY(launch_rows(f));
-    if (surv) C2_TRY(launch_surv_merge(ctx, surv, surv_qn, surv_qmax, n, k, out));  // light rows' Alg. 3 step
+    if (surv && C2_SIDE_MERGE) {
+      // the light rows' Alg. 3 step and the other rows' top-k update disjoint users' lists: they run
+      // concurrently (side stream); the next function's tiles wait for both
+      if (!ctx->side_stream) {
+        C2_CUDA(ctx, cudaStreamCreateWithFlags(&ctx->side_stream, cudaStreamNonBlocking));
+        for (auto &e : ctx->side_ev) C2_CUDA(ctx, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      }
+      C2_CUDA(ctx, cudaEventRecord(ctx->side_ev[0], st));
+      C2_CUDA(ctx, cudaStreamWaitEvent(ctx->side_stream, ctx->side_ev[0], 0));
+      C2_TRY(launch_surv_merge(ctx, surv, surv_qn, surv_qmax, n, k, out, ctx->side_stream));
+      C2_CUDA(ctx, cudaEventRecord(ctx->side_ev[1], ctx->side_stream));
+      C2_TRY(launch_rows(f));
+      C2_CUDA(ctx, cudaStreamWaitEvent(st, ctx->side_ev[1], 0));
+    } else {
+      C2_TRY(launch_rows(f));
+      if (surv) C2_TRY(launch_surv_merge(ctx, surv, surv_qn, surv_qmax, n, k, out));  // light rows' Alg. 3 step
+    }
     blo = bhi;
   }
   if (!fused) C2_TRY(launch_singles(0, nsingle, nullptr, out));

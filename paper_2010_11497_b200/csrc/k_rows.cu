@@ -433,10 +433,12 @@ int launch_row_topk(c2_ctx *ctx, const RowArgs &ra) {
   return C2_OK;
 }
 
-int launch_surv_merge(c2_ctx *ctx, const c2_cand *surv, int32_t *qn, int qmax, int32_t n, int k, c2_cand *run) {
+int launch_surv_merge(c2_ctx *ctx, const c2_cand *surv, int32_t *qn, int qmax, int32_t n, int k, c2_cand *run,
+                      cudaStream_t st) {
   const int g = ctx->num_sms * 8;
-  if (k <= 32) k_surv_merge<1><<<g, 256, 0, ctx->stream>>>(surv, qn, qmax, n, k, run);
-  else k_surv_merge<2><<<g, 256, 0, ctx->stream>>>(surv, qn, qmax, n, k, run);
+  if (!st) st = ctx->stream;
+  if (k <= 32) k_surv_merge<1><<<g, 256, 0, st>>>(surv, qn, qmax, n, k, run);
+  else k_surv_merge<2><<<g, 256, 0, st>>>(surv, qn, qmax, n, k, run);
   C2_LAUNCHED(ctx, "k_surv_merge");
   return C2_OK;
 }

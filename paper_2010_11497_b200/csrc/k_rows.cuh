@@ -38,6 +38,7 @@ struct RowArgs {
 };
 
 int launch_row_topk(c2_ctx *ctx, const RowArgs &ra);
-int launch_surv_merge(c2_ctx *ctx, const c2_cand *surv, int32_t *qn, int qmax, int32_t n, int k, c2_cand *run);
+int launch_surv_merge(c2_ctx *ctx, const c2_cand *surv, int32_t *qn, int qmax, int32_t n, int k, c2_cand *run,
+                      cudaStream_t st = nullptr);
 
 }  // namespace c2
