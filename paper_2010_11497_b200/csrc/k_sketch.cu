@@ -142,11 +142,11 @@ __global__ void __launch_bounds__(SK_WARPS * 32, 3) k_sketch_w(const int32_t *__
           if (d < Wv) atomicOr(&B[f * SK_CAPW + (d >> 5)], 1u << (d & 31));
         };
         const bool all = need == (1u << SK_FG) - 1u;  // (every function of a full group: round 1)
-        int32_t p = p0 + lane;
-        for (; p + 96 < p1; p += 128) {  // four items per lane, no bounds checks
+        int32_t bq = p0;
+        for (; bq + 128 <= p1; bq += 128) {  // four items per lane, no bounds checks (warp-uniform trip count)
           uint32_t x[4];
 #pragma unroll
-          for (int q = 0; q < 4; ++q) x[q] = (uint32_t)__ldg(items + p + 32 * q);
+          for (int q = 0; q < 4; ++q) x[q] = (uint32_t)__ldg(items + bq + lane + 32 * q);
           if (all) {
 #pragma unroll
             for (int q = 0; q < 4; ++q)
@@ -160,7 +160,7 @@ __global__ void __launch_bounds__(SK_WARPS * 32, 3) k_sketch_w(const int32_t *__
                 if ((need >> f) & 1u) hset(f, x[q]);
           }
         }
-        for (; p < p1; p += 32) {
+        for (int32_t p = bq + lane; p < p1; p += 32) {
           const uint32_t x = (uint32_t)__ldg(items + p);
 #pragma unroll
           for (int f = 0; f < SK_FG; ++f)
