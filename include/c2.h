@@ -194,9 +194,12 @@ C2_API int c2_build(c2_ctx *ctx, const int32_t *csr_offsets, const int32_t *item
              int32_t b, int32_t max_cluster_N, int32_t k, int32_t sim_mode, uint64_t seed, int32_t *nbr,
              uint16_t *inter, uint16_t *uni, float *sim);
 
-/* As c2_build with HOST inputs and outputs (nnz = csr_offsets[n_users]); the host<->device
- * copies run on the ctx stream inside the call.  Host buffers may be pageable or pinned;
- * sim may be NULL.  Returns after the outputs are in host memory. */
+/* As c2_build with HOST inputs and outputs (nnz = csr_offsets[n_users]).  The CSR is uploaded
+ * in up to 8 user chunks on a ctx-owned copy stream; each chunk is validated and (FastRandomHash
+ * clustering) sketched on the ctx stream as soon as it has arrived, so the transfer overlaps
+ * Step 1; the outputs come back on the ctx stream.  Host buffers may be pageable or pinned
+ * (pinned: full PCIe rate); sim may be NULL.  A rule violation in any chunk returns C2_EDATA
+ * with that row's index.  Returns after the outputs are in host memory. */
 C2_API int c2_build_host(c2_ctx *ctx, const int32_t *csr_offsets, const int32_t *item_ids, int32_t n_users, int32_t t,
                   int32_t b, int32_t max_cluster_N, int32_t k, int32_t sim_mode, uint64_t seed, int32_t *nbr,
                   uint16_t *inter, uint16_t *uni, float *sim);
