@@ -27,7 +27,10 @@ constexpr int RT_WARPS = 8;
 constexpr int RT_QCAP = 256;  // survivor queue per warp (>= 64 * KS)
 
 template <int KS>
-__global__ void __launch_bounds__(RT_WARPS * 32) k_row_topk(RowArgs a) {
+#ifndef C2_RT_MINB
+#define C2_RT_MINB 4
+#endif
+__global__ void __launch_bounds__(RT_WARPS * 32, C2_RT_MINB) k_row_topk(RowArgs a) {
   constexpr int R1 = C2_R1MUL * KS;
   __shared__ __align__(16) Cand s_q[RT_WARPS][RT_QCAP];
   __shared__ __align__(16) c2_cand s_run[RT_WARPS][C2_MAX_K];
