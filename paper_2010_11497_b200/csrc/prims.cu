@@ -119,7 +119,7 @@ __global__ void k_scan_down(const int32_t *__restrict__ in, int64_t n, const int
 #pragma unroll
   for (int j = 0; j < SCAN_I; ++j) v[j] = base + j < n ? in[base + j] : 0;
   block_scan_excl(v, sm);
-  int off = part_scan[blockIdx.x];
+  int off = part_scan ? part_scan[blockIdx.x] : 0;  // (nullptr: a single tile)
 #pragma unroll
   for (int j = 0; j < SCAN_I; ++j)
     if (base + j <= n) out[base + j] = v[j] + off;  // out has n+1 entries
@@ -128,6 +128,11 @@ __global__ void k_scan_down(const int32_t *__restrict__ in, int64_t n, const int
 int scan_exclusive(c2_ctx *ctx, const int32_t *in, int32_t *out, int64_t n) {
   // out[n] is produced by the tile that contains index n (value = total).
   int64_t nb = (n + 1 + SCAN_TILE - 1) / SCAN_TILE;
+  if (nb == 1) {  // one tile: one launch
+    k_scan_down<<<1, SCAN_T, 0, ctx->stream>>>(in, n, nullptr, out);
+    C2_LAUNCHED(ctx, "k_scan_down");
+    return C2_OK;
+  }
   int rc;
   // scratch names depend on depth so recursion does not alias
   static const char *names[4] = {"scan_p0", "scan_p1", "scan_p2", "scan_p3"};
@@ -225,9 +230,87 @@ __global__ void __launch_bounds__(RS_T) k_radix_scatter(const uint32_t *__restri
   }
 }
 
+// One tile (n <= RS_TILE): every pass in one CTA, keys and values ping-ponging in shared memory;
+// the same stable digit-major / thread-major ranking as k_radix_scatter.
+__global__ void __launch_bounds__(RS_T) k_radix_small(const uint32_t *__restrict__ kin, const uint32_t *__restrict__ vin,
+                                                      uint32_t *__restrict__ kout, uint32_t *__restrict__ vout, int n,
+                                                      int passes) {
+  extern __shared__ __align__(16) uint32_t rsm[];
+  uint32_t *sk0 = rsm, *sv0 = rsm + RS_TILE, *sk1 = rsm + 2 * RS_TILE, *sv1 = rsm + 3 * RS_TILE;
+  int *cnt = reinterpret_cast<int *>(rsm + 4 * RS_TILE);  // [RS_BINS][RS_T]
+  __shared__ int sm_warp[RS_T / 32 + 1];
+  for (int i = threadIdx.x; i < n; i += RS_T) {
+    sk0[i] = kin[i];
+    sv0[i] = vin[i];
+  }
+  const int base = threadIdx.x * RS_I;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (int p = 0; p < passes; ++p) {
+    const int shift = p * RS_BITS;
+    for (int j = threadIdx.x; j < RS_BINS * RS_T; j += RS_T) cnt[j] = 0;
+    __syncthreads();
+    uint32_t k[RS_I], v[RS_I];
+    int loc[RS_I];
+#pragma unroll
+    for (int j = 0; j < RS_I; ++j) {
+      const bool ok = base + j < n;
+      k[j] = ok ? sk0[base + j] : 0u;
+      v[j] = ok ? sv0[base + j] : 0u;
+      const int d = (k[j] >> shift) & (RS_BINS - 1);
+      loc[j] = ok ? cnt[d * RS_T + threadIdx.x]++ : 0;
+    }
+    __syncthreads();
+    int run[RS_BINS];
+    int s = 0;
+#pragma unroll
+    for (int j = 0; j < RS_BINS; ++j) {
+      run[j] = s;
+      s += cnt[threadIdx.x * RS_BINS + j];
+    }
+    const int incl = c2d::warp_incl_scan(s);
+    if (lane == 31) sm_warp[w] = incl;
+    __syncthreads();
+    if (w == 0) {
+      const int x = lane < RS_T / 32 ? sm_warp[lane] : 0;
+      const int y = c2d::warp_incl_scan(x);
+      if (lane < RS_T / 32) sm_warp[lane] = y - x;
+    }
+    __syncthreads();
+    const int off = sm_warp[w] + incl - s;
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < RS_BINS; ++j) cnt[threadIdx.x * RS_BINS + j] = run[j] + off;
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < RS_I; ++j) {
+      if (base + j < n) {
+        const int d = (k[j] >> shift) & (RS_BINS - 1);
+        const int dst = cnt[d * RS_T + threadIdx.x] + loc[j];
+        sk1[dst] = k[j];
+        sv1[dst] = v[j];
+      }
+    }
+    __syncthreads();
+    uint32_t *t = sk0; sk0 = sk1; sk1 = t;
+    t = sv0; sv0 = sv1; sv1 = t;
+  }
+  for (int i = threadIdx.x; i < n; i += RS_T) {
+    kout[i] = sk0[i];
+    vout[i] = sv0[i];
+  }
+}
+
 int radix_sort_pairs(c2_ctx *ctx, const uint32_t *keys_in, const uint32_t *vals_in, uint32_t *keys_out,
                      uint32_t *vals_out, int64_t n, int bits) {
   if (n == 0) return C2_OK;
+  if (n <= RS_TILE) {
+    const int passes = std::max(1, (bits + RS_BITS - 1) / RS_BITS);
+    const size_t sm = (size_t)(4 * RS_TILE + RS_BINS * RS_T) * 4;
+    C2_CUDA(ctx, cudaFuncSetAttribute(k_radix_small, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    k_radix_small<<<1, RS_T, sm, ctx->stream>>>(keys_in, vals_in, keys_out, vals_out, (int)n, passes);
+    C2_LAUNCHED(ctx, "k_radix_small");
+    return C2_OK;
+  }
   int passes = (bits + RS_BITS - 1) / RS_BITS;
   if (passes < 1) passes = 1;
   int nblocks = (int)((n + RS_TILE - 1) / RS_TILE);
