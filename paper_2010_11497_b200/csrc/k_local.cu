@@ -159,34 +159,50 @@ __device__ __forceinline__ int slot_class(int32_t s) {  // slot = 2^class >= s, 
   return c;
 }
 
-__global__ void k_wl_classify(const int32_t *__restrict__ offsets, const int32_t *__restrict__ ccum, int t,
-                              int32_t n, int64_t C, uint32_t *__restrict__ key, uint32_t *__restrict__ val,
-                              uint32_t maxs, int sized, int32_t *__restrict__ cnt_fc, uint32_t hyrec_min) {
-  int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (g >= C) return;
+__device__ __forceinline__ void k_wl_classify_one(const int32_t *__restrict__ offsets, const int32_t *__restrict__ ccum,
+                                                  int t, int32_t n, int64_t g, uint32_t *__restrict__ key,
+                                                  uint32_t *__restrict__ val, uint32_t maxs, int sized,
+                                                  int32_t *__restrict__ cnt_fc, uint32_t hyrec_min, int sb) {
+  // sort key: class (2 bits) | function (6 bits) | sb bits of size field; only these 8 + sb bits
+  // are sorted (radix passes of 5 bits)
   int f = find_f(ccum, t, g);
+  const int fs = sb, cs = sb + 6;
   int64_t c = g - ccum[f];
   const int32_t *off = offsets + (int64_t)f * (n + 1);
   uint32_t s = (uint32_t)(off[c + 1] - off[c]);
   uint32_t k;
   if (s >= hyrec_min) {  // Alg. 2 else-branch: Hyrec (C2_SOLVER_HYBRID only; hyrec_min = UINT32_MAX otherwise)
-    k = (3u << 30) | ((uint32_t)f << 24);
+    k = (3u << cs) | ((uint32_t)f << fs);
     atomicAdd(&cnt_fc[f * WLC + 8], 1);
   } else if (s > 32) {
-    k = ((uint32_t)f << 24) | (sized ? min(maxs - s, 0xFFFFFFu) : 0u);
+    k = ((uint32_t)f << fs) | (sized ? min(maxs - s, (1u << sb) - 1u) : 0u);
     atomicAdd(&cnt_fc[f * WLC + 0], (int32_t)((s + 31) / 32));  // big tiles of f
     atomicAdd(&cnt_fc[f * WLC + 7], 1);                          // big clusters of f
     atomicAdd(&cnt_fc[f * WLC + 9], (int32_t)s);                 // their members
   } else if (s >= 2) {
     int cl = slot_class((int32_t)s);
-    k = (1u << 30) | ((uint32_t)f << 24) | (uint32_t)cl;
+    k = (1u << cs) | ((uint32_t)f << fs) | (uint32_t)cl;
     atomicAdd(&cnt_fc[f * WLC + cl], 1);  // small clusters of (f, class), class 1..5
   } else {
-    k = (2u << 30) | ((uint32_t)f << 24);
+    k = (2u << cs) | ((uint32_t)f << fs);
     atomicAdd(&cnt_fc[f * WLC + 6], 1);  // singletons of f
   }
   key[g] = k;
   val[g] = (uint32_t)g;
+}
+
+__global__ void k_wl_classify(const int32_t *__restrict__ offsets, const int32_t *__restrict__ ccum, int t,
+                              int32_t n, int64_t C, uint32_t *__restrict__ key, uint32_t *__restrict__ val,
+                              uint32_t maxs, int sized, int32_t *__restrict__ cnt_fc_g, uint32_t hyrec_min, int sb) {
+  // counters summed per block in shared memory, then one global atomic per non-zero counter
+  __shared__ int32_t cnt_fc[WLC * C2_MAX_T];
+  for (int i = threadIdx.x; i < WLC * t; i += blockDim.x) cnt_fc[i] = 0;
+  __syncthreads();
+  int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (g < C) k_wl_classify_one(offsets, ccum, t, n, g, key, val, maxs, sized, cnt_fc, hyrec_min, sb);
+  __syncthreads();
+  for (int i = threadIdx.x; i < WLC * t; i += blockDim.x)
+    if (cnt_fc[i]) atomicAdd(&cnt_fc_g[i], cnt_fc[i]);
 }
 
 __global__ void k_bc_sizes(const uint32_t *__restrict__ sval, int64_t nbig, const int32_t *__restrict__ offsets,
@@ -1421,12 +1437,21 @@ static TileKernel pick_tile(int nhi, int vpt) {
 // Per function: count entries (s * s4 per cluster: every member is a row) and rows the tiles of
 // that function can hand to k_row_topk -- the exact sizes of its buffers.
 __global__ void k_cnt_need(const BigC *__restrict__ bcs, int64_t ncl, unsigned long long *__restrict__ need, int t) {
+  // per-block sums in shared memory (clusters are ordered by function, so a block touches few
+  // functions), then one global atomic per non-zero entry
+  __shared__ unsigned long long sn[2 * C2_MAX_T];
+  for (int i = threadIdx.x; i < 2 * t; i += blockDim.x) sn[i] = 0ull;
+  __syncthreads();
   const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= ncl) return;
-  const BigC B = bcs[c];
-  const unsigned long long s = (unsigned long long)B.s;
-  atomicAdd(&need[B.f], s * ((s + 3) & ~3ull));
-  atomicAdd(&need[t + B.f], s);
+  if (c < ncl) {
+    const BigC B = bcs[c];
+    const unsigned long long s = (unsigned long long)B.s;
+    atomicAdd(&sn[B.f], s * ((s + 3) & ~3ull));
+    atomicAdd(&sn[t + B.f], s);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < 2 * t; i += blockDim.x)
+    if (sn[i]) atomicAdd(&need[i], sn[i]);
 }
 
 __global__ void k_init_pads(c2_cand *__restrict__ R, int64_t E) {
@@ -1538,9 +1563,11 @@ int local_knn(c2_ctx *ctx, const Csr &csr_in, int t, const Clusters &cl, int k, 
   const uint32_t hyrec_min = ctx->solver == 1 ? (uint32_t)(5 * k * k) : 0xFFFFFFFFu;
   const uint32_t maxs = (uint32_t)std::max(std::min<int64_t>(cl.max_size, (int64_t)hyrec_min - 1), (int64_t)1);
   const int sized = maxs < (1u << 24) ? 1 : 0;
-  k_wl_classify<<<nblk(C), 256, 0, st>>>(cl.offsets, ccum, t, n, C, key, val, maxs, sized, cnt_fc, hyrec_min);
+  int sb = 3;  // bits of the key's size field: maxs - s (big clusters) or the slot class (<= 5)
+  while (sized && sb < 24 && (1u << sb) <= maxs) ++sb;
+  k_wl_classify<<<nblk(C), 256, 0, st>>>(cl.offsets, ccum, t, n, C, key, val, maxs, sized, cnt_fc, hyrec_min, sb);
   C2_LAUNCHED(ctx, "k_wl_classify");
-  C2_TRY(radix_sort_pairs(ctx, key, val, skey, sval, C, 32));
+  C2_TRY(radix_sort_pairs(ctx, key, val, skey, sval, C, sb + 8));
   unsigned long long *wacc = (unsigned long long *)ws_get(ctx, "work_acc", 16, &rc);
   if (rc) return rc;
   C2_CUDA(ctx, cudaMemsetAsync(wacc, 0, 8, st));
