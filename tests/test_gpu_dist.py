@@ -36,3 +36,30 @@ def test_shards_merge_to_single_build(ctx, cfg, G):
     nbr, inter, uni, _ = c2.merge(torch.stack(parts).contiguous(), ctx=ctx)
     assert np.array_equal(nbr.cpu().numpy(), ref[0])
     assert np.array_equal(inter.cpu().numpy(), ref[1]) and np.array_equal(uni.cpu().numpy(), ref[2])
+
+
+def test_build_sharded_over_nccl_single_rank(ctx):
+    """The real exchange path (NCCL all-to-all + all-gather of CUDA tensors, c2_merge of the
+    received lists) in a one-rank NCCL group: equals the single-process build bytewise."""
+    import os
+    import socket
+    import torch.distributed as dist
+    if not dist.is_nccl_available():
+        pytest.skip("no NCCL")
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1)
+    try:
+        C = synth.config("c3")
+        offs, items = synth.generate("c3")
+        o, i = torch.from_numpy(offs).cuda(), torch.from_numpy(items).cuda()
+        ref = [x.cpu().numpy() for x in c2.build(o, i, k=C.k, t=C.t, b=C.b, N=C.N, seed=C.hash_seed, ctx=ctx)[:3]]
+        o2, i2 = c2d.broadcast_csr(o, i)
+        nbr, inter, uni, _ = c2d.build_sharded(o2, i2, k=C.k, t=C.t, b=C.b, N=C.N, seed=C.hash_seed, ctx=ctx)
+        torch.cuda.synchronize()
+        assert np.array_equal(nbr.cpu().numpy(), ref[0])
+        assert np.array_equal(inter.cpu().numpy(), ref[1].astype(np.int32))
+        assert np.array_equal(uni.cpu().numpy(), ref[2].astype(np.int32))
+    finally:
+        dist.destroy_process_group()
