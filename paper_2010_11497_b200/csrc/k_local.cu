@@ -1040,6 +1040,11 @@ __global__ void __launch_bounds__(TILE_T, C2_TILE_MINB) k_local_tile(TileArgs a)
     const unsigned valid = __ballot_sync(0xffffffffu, lane < nr && s_ru[lane] >= 0);
     unsigned k8rows = valid;  // rows handed to k_row_topk
     const bool lt = light_on && nsl <= VPT * TILE_WARPS;  // (one g0 group: counters of all members live)
+    // light rows: the running k-th best tau of every row (one global read per row) is requested now
+    // by the last warp and turned into its Ref after the first mask build, so the epilogue can start
+    // without a barrier after the last window's mask clear
+    c2_cand tl_pre = c2_cand{-1, 0, 0};
+    if (lt && warp == TILE_WARPS - 1 && ((valid >> lane) & 1u)) tl_pre = a.seed[(int64_t)s_ru[lane] * kk + kk - 1];
     // small tiles (<= TILE_WARPS/2 slices): G warps share a slice, each probing a contiguous part
     // of its member lists; the partial bit-sliced counters are then added (bit-sliced ripple
     // carry), so no warp idles through the probe of a tile with few slices
@@ -1091,7 +1096,18 @@ __global__ void __launch_bounds__(TILE_T, C2_TILE_MINB) k_local_tile(TileArgs a)
         }
         __syncthreads();
         // the next tile's row blocks go to the other staging buffer as soon as its record is in
-        if (g0 == 0 && w == 0 && warp == TILE_WARPS - 1) fetch_finish(cur ^ 1);
+        if (g0 == 0 && w == 0 && warp == TILE_WARPS - 1) {
+          if (lt) {
+            const bool light = tl_pre.id >= 0 && tl_pre.inter >= 1;
+            if (light) {
+              const Ref R = make_ref(from_out(tl_pre), s_rp[lane], false);
+              s_ref[lane] = make_uint4(R.A, R.B, R.iT, R.idlim);
+            }
+            const unsigned lm = __ballot_sync(0xffffffffu, light);
+            if (lane == 0) s_light = lm;
+          }
+          fetch_finish(cur ^ 1);
+        }
         // ---- probe: each warp streams VPT slices of v lists, two 16-byte loads per step with
         //      the next two steps in flight (odd tails padded with the sentinel item W, M[W] = 0)
         const long long ckpb = a.kstats ? clock64() : 0;
@@ -1190,19 +1206,10 @@ __global__ void __launch_bounds__(TILE_T, C2_TILE_MINB) k_local_tile(TileArgs a)
             if (xs[q] < W) M[xs[q]] = 0;
 #endif
         }
-        if (lt && w == nwin - 1 && warp == TILE_WARPS - 1) {
-          // light rows: the running k-th best tau (one global read per row) as a Ref
-          const int r = lane;
-          const c2_cand tl = ((valid >> r) & 1u) ? a.seed[(int64_t)s_ru[r] * kk + kk - 1] : c2_cand{-1, 0, 0};
-          const bool light = tl.id >= 0 && tl.inter >= 1;
-          if (light) {
-            const Ref R = make_ref(from_out(tl), s_rp[r], false);
-            s_ref[r] = make_uint4(R.A, R.B, R.iT, R.idlim);
-          }
-          const unsigned lm = __ballot_sync(0xffffffffu, light);
-          if (lane == 0) s_light = lm;
-        }
-        __syncthreads();
+        // (after the last window's clear no barrier is needed unless the split-probe partial
+        // counters use M's words as scratch (G > 1): the next mask build follows the next tile's
+        // top-of-loop barrier, and s_ref / s_light were published by the probe's barrier)
+        if (w + 1 < nwin || G > 1) __syncthreads();
       }
       if (G > 1) {
         // add the G partial counters of each slice into its part-0 warp (scratch: [warp][plane][lane]
