@@ -115,7 +115,7 @@ enum {
                               kernel looping over the levels on the device (no host synchronisation
                               per level) whenever its histogram bound (t*n/(N+1) * b bins) is at most
                               2^25; 0: one host-driven pass per level.  Results are identical. */
-  C2_OPT_SURVIVORS = 9     /* c2_build only, 0..4096 (default 1024; halved while n*slots*8 B > 8 GiB): slots per user of the
+  C2_OPT_SURVIVORS = 9     /* c2_build only, 0..4096 (default 2048; halved while n*slots*8 B > 16 GiB): slots per user of the
                               light-row path (a row whose running list is full is screened in the
                               local kernel's epilogue and merged by a separate kernel; a row with more
                               survivors than slots gets its full count row and k_row_topk instead).  0: no

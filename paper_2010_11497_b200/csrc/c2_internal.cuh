@@ -40,7 +40,7 @@ struct c2_ctx {
   int func_offset = 0;  // C2_OPT_FUNC_OFFSET
   int solver = 0;       // C2_OPT_LOCAL_SOLVER: 0 brute force everywhere (A12), 1 Alg. 2 hybrid (Hyrec)
   uint64_t hyrec_seed = 0;  // the call's seed (Hyrec's random initial graphs)   // C2_OPT_CLUSTERING: 0 FastRandomHash (Step 1 of C^2), 1 MinHash (N3 variant)
-  int surv_qmax = 1024;  // C2_OPT_SURVIVORS: light-row survivor slots per user (0: off; capped to 8 GiB of slots)
+  int surv_qmax = 2048;  // C2_OPT_SURVIVORS: light-row survivor slots per user (0: off; capped to 16 GiB of slots)
   bool gf_tensor = false;  // C2_OPT_GF_TENSOR: GoldFinger big clusters on the tensor cores (k_gf_mma; measured slower, off)
   bool presketched = false;  // c2_build_host: the sketch of the next fastrandomhash call is already in "sketch"
   cudaStream_t side_stream = nullptr;  // Step 2: light rows' merge concurrent with the per-row top-k

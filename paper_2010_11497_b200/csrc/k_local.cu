@@ -99,6 +99,10 @@ __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.
 #ifndef C2_FILL_COAL
 #define C2_FILL_COAL 1  // multi-window packing: k_sl_fill_coal (coalesced CSR reads) instead of k_sl_fill_rows
 #endif
+#ifndef C2_EPI_BAR
+#define C2_EPI_BAR 1  // keep the light epilogue's barrier even when no row can overflow (measured: without
+                      // it c5 takes 56.0 vs 52.9 ms -- the warps drift apart before the next tile)
+#endif
 #ifndef C2_SIDE_MERGE
 #define C2_SIDE_MERGE 1  // light rows' merge on a side stream, concurrent with k_row_topk
 #endif
@@ -1010,11 +1014,37 @@ __global__ void __launch_bounds__(TILE_T, C2_TILE_MINB) k_local_tile(TileArgs a)
   // global memory for k_surv_merge.  The other rows' counts go to k_row_topk.
   const bool light_on = C2_LIGHT && a.surv != nullptr;
   int cur = 0;
+  // light rows' survivor counts of the tile in slot pb (read and reset by k_surv_merge), written
+  // by warp 0 after the NEXT tile's top-of-loop barrier: the light epilogue then needs no barrier
+  // of its own when no row can overflow its survivor slots
+  bool prev_lt = false;
+  auto flush_light = [&](int pb) {
+    const unsigned lok = s_light & ~s_over;
+    const BigC Bp = s_B[pb];
+    const int32_t ru = s_ru2[pb][lane];
+    if (((lok >> lane) & 1u) && s_qn[lane] > 0) a.qn[ru] = s_qn[lane];
+    if (a.kstats && lane == 0) {
+      atomicAdd(&a.kstats[71], (unsigned long long)__popc(lok));
+      atomicAdd(&a.kstats[73], (unsigned long long)__popc(s_over));
+    }
+    if (a.kstats && ((lok >> lane) & 1u)) {
+      atomicAdd(&a.kstats[72], (unsigned long long)s_qn[lane]);
+      int ev = Bp.s - 1;  // pair evaluations of this row: its cluster-mates (debug work accounting)
+      if (Bp.slot) {
+        const int32_t *vpp = a.vperm + Bp.vp_off;
+        const int lo = lane & ~(Bp.slot - 1);
+        ev = -1;
+        for (int j = 0; j < Bp.slot; ++j) ev += vpp[lo + j] >= 0 ? 1 : 0;
+      }
+      atomicAdd(&a.kstats[70], (unsigned long long)ev);
+    }
+  };
   for (;;) {
     mbar_wait(&mb_stg[cur], (ph_stg >> cur) & 1u);  // this tile's staged row blocks
     ph_rec ^= 1u << cur;  // (slot cur's record and staging phases were consumed)
     ph_stg ^= 1u << cur;
     __syncthreads();
+    if (prev_lt && warp == 0) flush_light(cur ^ 1);
     const int64_t it = s_it[cur];
     if (it >= a.hi) break;
     uint4 *stg = stg0 + cur * a.stg_cap;
@@ -1330,8 +1360,12 @@ __global__ void __launch_bounds__(TILE_T, C2_TILE_MINB) k_local_tile(TileArgs a)
             }
           }
         }
-        __syncthreads();  // s_qn, s_over complete
-        k8rows = valid & ~(s_light & ~s_over);
+        if (C2_EPI_BAR || s - 1 > a.qmax) {  // a row may overflow its survivor slots: s_over must be complete
+          __syncthreads();
+          k8rows = valid & ~(s_light & ~s_over);
+        } else {
+          k8rows = valid & ~s_light;
+        }
       }
       if (a.kstats) ckE = clock64();
       // ---- the other rows: planes -> 32 counts per member (transpose) -> their count rows, and
@@ -1398,25 +1432,7 @@ __global__ void __launch_bounds__(TILE_T, C2_TILE_MINB) k_local_tile(TileArgs a)
         }
       }
     }
-    // light rows' survivor counts (read and reset by k_surv_merge)
-    if (lt && warp == 0) {
-      const unsigned lok = s_light & ~s_over;
-      if (((lok >> lane) & 1u) && s_qn[lane] > 0) a.qn[s_ru[lane]] = s_qn[lane];
-      if (a.kstats && lane == 0) {
-        atomicAdd(&a.kstats[71], (unsigned long long)__popc(lok));
-        atomicAdd(&a.kstats[73], (unsigned long long)__popc(s_over));
-      }
-      if (a.kstats && ((lok >> lane) & 1u)) {
-        atomicAdd(&a.kstats[72], (unsigned long long)s_qn[lane]);
-        int ev = s - 1;  // pair evaluations of this row: its cluster-mates (debug work accounting)
-        if (B.slot) {
-          const int lo = lane & ~(B.slot - 1);
-          ev = -1;
-          for (int j = 0; j < B.slot; ++j) ev += vp[lo + j] >= 0 ? 1 : 0;
-        }
-        atomicAdd(&a.kstats[70], (unsigned long long)ev);
-      }
-    }
+    prev_lt = lt;
     if (a.kstats && tid == 0) {  // tile cycles by cluster size class: mixed, 33-256, 257-1024, >1024
       const long long ck3 = clock64();
       const int cls = B.slot ? 0 : s <= 256 ? 1 : s <= 1024 ? 2 : 3;
@@ -1781,9 +1797,10 @@ int local_knn(c2_ctx *ctx, const Csr &csr_in, int t, const Clusters &cl, int k, 
   //      re-zeroed by k_surv_merge after every function
   c2_cand *surv = nullptr;
   int32_t *surv_qn = nullptr;
-  // survivor slots: the option's value, but at most 8 GiB of slots (halved until it fits, >= 64)
+  // survivor slots: the option's value, but at most 16 GiB of slots (halved until it fits, >= 64); with
+  // slots >= N - 1 no light row can overflow and the light epilogue needs no barrier
   int surv_qmax = ctx->surv_qmax;
-  while (surv_qmax > 64 && (size_t)n * surv_qmax * sizeof(c2_cand) > ((size_t)8 << 30)) surv_qmax >>= 1;
+  while (surv_qmax > 64 && (size_t)n * surv_qmax * sizeof(c2_cand) > ((size_t)16 << 30)) surv_qmax >>= 1;
   if (fused && C2_LIGHT && surv_qmax > 0 && nslices > 0) {
     surv = (c2_cand *)ws_get(ctx, "surv", (size_t)n * surv_qmax * sizeof(c2_cand), &rc);
     if (rc) return rc;

@@ -459,7 +459,7 @@ def test_build_survivor_slots(ctx, cfg, qmax):
     try:
         check_build(ctx, offs, items, C.t, C.b, C.N, C.k, C.hash_seed)
     finally:
-        ctx.set_option(c2.OPT_SURVIVORS, 1024)
+        ctx.set_option(c2.OPT_SURVIVORS, 2048)
 
 
 @pytest.mark.parametrize("seed", range(8))
@@ -470,7 +470,7 @@ def test_build_random_survivor_slots(ctx, seed, qmax):
     try:
         check_build(ctx, offs, items, max(t, 3), b, N, k, hs, mode=seed % 2)
     finally:
-        ctx.set_option(c2.OPT_SURVIVORS, 1024)
+        ctx.set_option(c2.OPT_SURVIVORS, 2048)
 
 
 @pytest.mark.parametrize("tensor", [1, 0])
