@@ -935,6 +935,7 @@ __global__ void __launch_bounds__(TILE_T, C2_TILE_MINB) k_local_tile(TileArgs a)
   __shared__ unsigned s_light;      // light rows (running list full, k-th best with i >= 1)
   __shared__ unsigned s_over;       // light rows with more than qmax survivors (handed to k_row_topk)
   __shared__ int64_t s_cbase, s_rbase;  // this tile's first count entry / record for k_row_topk
+  __shared__ int s_pre;                 // 1: s_cbase / s_rbase were allocated early (no barrier needed)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   for (int i = tid; i < a.W + 1; i += TILE_T) M[i] = 0;
   uint4 *stg0 = reinterpret_cast<uint4 *>(dyn + a.stg_off);  // staged rows' blocks, one buffer per slot
@@ -1018,6 +1019,18 @@ __global__ void __launch_bounds__(TILE_T, C2_TILE_MINB) k_local_tile(TileArgs a)
   // by warp 0 after the NEXT tile's top-of-loop barrier: the light epilogue then needs no barrier
   // of its own when no row can overflow its survivor slots
   bool prev_lt = false;
+  // count rows of the tile's k8 rows: bump-allocated in the per-function buffers (one thread)
+  auto alloc_rows = [&](unsigned k8, int s4v) {
+    const int n8 = __popc(k8);
+    if (n8 == 0) return;
+    const unsigned long long cb = atomicAdd(a.hv_used, (unsigned long long)n8 * s4v);
+    const unsigned long long rb = atomicAdd(a.hv_nrec, (unsigned long long)n8);
+    const bool fits = cb + (unsigned long long)n8 * s4v <= (unsigned long long)a.hv_cap &&
+                      rb + (unsigned long long)n8 <= (unsigned long long)a.hv_rcap;
+    if (!fits) atomicExch(a.err, 1);
+    s_cbase = fits ? (int64_t)cb : -1;
+    s_rbase = (int64_t)rb;
+  };
   auto flush_light = [&](int pb) {
     const unsigned lok = s_light & ~s_over;
     const BigC Bp = s_B[pb];
@@ -1070,6 +1083,16 @@ __global__ void __launch_bounds__(TILE_T, C2_TILE_MINB) k_local_tile(TileArgs a)
     const unsigned valid = __ballot_sync(0xffffffffu, lane < nr && s_ru[lane] >= 0);
     unsigned k8rows = valid;  // rows handed to k_row_topk
     const bool lt = light_on && nsl <= VPT * TILE_WARPS;  // (one g0 group: counters of all members live)
+    // rows handed to k_row_topk known now (no light rows), or after the light rows are known when no
+    // row can overflow its survivor slots: their count rows are allocated early, the atomics'
+    // latency hidden behind the probe (published by the first window's barriers)
+    if (tid == 0) {
+      s_pre = 0;
+      if (!lt) {
+        alloc_rows(valid, s4);
+        s_pre = 1;
+      }
+    }
     // light rows: the running k-th best tau of every row (one global read per row) is requested now
     // by the last warp and turned into its Ref after the first mask build, so the epilogue can start
     // without a barrier after the last window's mask clear
@@ -1134,7 +1157,13 @@ __global__ void __launch_bounds__(TILE_T, C2_TILE_MINB) k_local_tile(TileArgs a)
               s_ref[lane] = make_uint4(R.A, R.B, R.iT, R.idlim);
             }
             const unsigned lm = __ballot_sync(0xffffffffu, light);
-            if (lane == 0) s_light = lm;
+            if (lane == 0) {
+              s_light = lm;
+              if (s - 1 <= a.qmax) {
+                alloc_rows(valid & ~lm, s4);
+                s_pre = 1;
+              }
+            }
           }
           fetch_finish(cur ^ 1);
         }
@@ -1372,17 +1401,10 @@ __global__ void __launch_bounds__(TILE_T, C2_TILE_MINB) k_local_tile(TileArgs a)
       //      one RowRec per row, for k_row_topk
       if (k8rows) {
         if (g0 == 0) {
-          const int n8 = __popc(k8rows);
-          if (tid == 0) {
-            const unsigned long long cb = atomicAdd(a.hv_used, (unsigned long long)n8 * s4);
-            const unsigned long long rb = atomicAdd(a.hv_nrec, (unsigned long long)n8);
-            const bool fits = cb + (unsigned long long)n8 * s4 <= (unsigned long long)a.hv_cap &&
-                              rb + (unsigned long long)n8 <= (unsigned long long)a.hv_rcap;
-            if (!fits) atomicExch(a.err, 1);
-            s_cbase = fits ? (int64_t)cb : -1;
-            s_rbase = (int64_t)rb;
+          if (!s_pre) {
+            if (tid == 0) alloc_rows(k8rows, s4);
+            __syncthreads();
           }
-          __syncthreads();
           if (warp == 0 && ((k8rows >> lane) & 1u) && s_cbase >= 0) {
             const int rk = __popc(k8rows & ((1u << lane) - 1u));
             const int slot = B.slot;
