@@ -345,6 +345,9 @@ constexpr int SM_INSERT_MAX = 32;  // survivors of a chunk merged by insertion (
 #ifndef C2_SM_MERGE_MIN
 #define C2_SM_MERGE_MIN 16
 #endif
+#ifndef C2_SM_RANK
+#define C2_SM_RANK 1  // k <= 32: every survivor chunk merged by ranks (0: insertion / bitonic merge below)
+#endif
 constexpr int SM_MERGE_MIN = C2_SM_MERGE_MIN;  // k <= 32: chunks with more survivors take the bitonic merge
                                                // (c5: threshold 4 57.6 ms, 8 56.3, 16 55.4, off 55.5)
 
@@ -377,6 +380,43 @@ __global__ void __launch_bounds__(256) k_surv_merge(const c2_cand *__restrict__ 
         unsigned bal = __ballot_sync(0xffffffffu, ok);
         if (!bal) continue;
         changed = true;
+        if (KS == 1 && C2_SM_RANK) {
+          // k <= 32, every chunk by ranks (independent comparisons, no serial insertion chain):
+          // rs = the survivor's rank in S (binary search; a repeated id carries the same (i, U),
+          // so its twin sits exactly at rs, A16), then over the kept survivors o: rq = the
+          // survivor's rank among them, sh = lane's S entry's; new positions rs + rq and lane + sh
+          int r = 0;
+#pragma unroll
+          for (int st = 16; st >= 1; st >>= 1) {
+            const Cand o = shfl_c(S[0], min(r + st - 1, 31));
+            if (r + st <= 32 && better_c(o, x)) r += st;
+          }
+          const Cand at = shfl_c(S[0], min(r, 31));
+          ok = ok && !(r < 32 && at.id == x.id);
+          const unsigned km = __ballot_sync(0xffffffffu, ok);
+          const int nS = __popc(__ballot_sync(0xffffffffu, lane < k && is_real(S[0])));
+          const uint32_t xi = x.iu & 0xFFFFu, xU = x.iu >> 16;
+          const uint32_t si = S[0].iu & 0xFFFFu, sU = S[0].iu >> 16;
+          int rq = 0, sh = 0;
+          for (unsigned mm = km; mm; mm &= mm - 1u) {
+            const int j = __ffs(mm) - 1;
+            const uint32_t oiu = __shfl_sync(0xffffffffu, x.iu, j);
+            const int32_t oid = __shfl_sync(0xffffffffu, x.id, j);
+            const uint32_t oi = oiu & 0xFFFFu, oU = oiu >> 16;
+            const uint32_t l1 = oi * xU, r1 = xi * oU;  // o before x?
+            rq += (l1 > r1 || (l1 == r1 && oid < x.id)) ? 1 : 0;
+            const uint32_t l2 = oi * sU, r2 = si * oU;  // o before lane's S entry?
+            sh += (l2 > r2 || (l2 == r2 && oid < S[0].id)) ? 1 : 0;
+          }
+          if (ok && r + rq < k) sbuf[r + rq] = to_out(x);
+          if (lane < nS && lane + sh < k) sbuf[lane + sh] = to_out(S[0]);
+          for (int p = nS + __popc(km) + lane; p < k; p += 32) sbuf[p] = c2_cand{-1, 0, 0};
+          __syncwarp();
+          S[0] = lane < k ? from_out(sbuf[lane]) : sent();
+          __syncwarp();
+          tau = warp_get<KS>(S, k - 1);
+          continue;
+        }
         if (KS == 1 && __popc(bal) > SM_MERGE_MIN) {
           // k <= 32: drop the survivors already in S (binary search of S, best first: a repeated id
           // carries the same (i, U), so it sits exactly where the search ends, A16), sort the rest

@@ -87,6 +87,9 @@ __global__ void __launch_bounds__(256) k_sketch(const int32_t *__restrict__ offs
 // above the window) slides its window up and re-reads the items -- exact for every (b, |P_u|).
 // Per item and function: one 64-bit multiply-add, a compare, and for ~SK_K/|P_u| of them one
 // shared atomic; no per-lane sorted inserts (the divergence of the thread-per-(user, f) form).
+#ifndef C2_SK_NOBR
+#define C2_SK_NOBR 1  // 1: no per-function branch in the item loops (finished functions' windows moved out of range)
+#endif
 constexpr int SK_WARPS = 8;
 constexpr int SK_FG = 8;      // functions per pass over the items
 constexpr int SK_CAPW = 128;  // window words per function (4096 values)
@@ -132,8 +135,13 @@ __global__ void __launch_bounds__(SK_WARPS * 32, 3) k_sketch_w(const int32_t *__
       uint32_t Wv = W0;
       while (need) {
         uint32_t base[SK_FG];
+        // a function that needs no more values gets a window start no hash reaches (v < b <= 2^16,
+        // so v - base >= 2^31 > Wv): the item loops test every function without a per-function branch
 #pragma unroll
-        for (int f = 0; f < SK_FG; ++f) base[f] = __shfl_sync(0xffffffffu, mybase, 4 * f);
+        for (int f = 0; f < SK_FG; ++f) {
+          base[f] = __shfl_sync(0xffffffffu, mybase, 4 * f);
+          if (C2_SK_NOBR && !((need >> f) & 1u)) base[f] = 0x80000000u;
+        }
         // ---- hash pass: set the bits of the values inside each needing function's window
         auto hset = [&](int f, uint32_t x) {
           const uint64_t z = fa[f] * (uint64_t)x + fc[f];
@@ -147,7 +155,7 @@ __global__ void __launch_bounds__(SK_WARPS * 32, 3) k_sketch_w(const int32_t *__
           uint32_t x[4];
 #pragma unroll
           for (int q = 0; q < 4; ++q) x[q] = (uint32_t)__ldg(items + bq + lane + 32 * q);
-          if (all) {
+          if (all || C2_SK_NOBR) {
 #pragma unroll
             for (int q = 0; q < 4; ++q)
 #pragma unroll
@@ -164,7 +172,7 @@ __global__ void __launch_bounds__(SK_WARPS * 32, 3) k_sketch_w(const int32_t *__
           const uint32_t x = (uint32_t)__ldg(items + p);
 #pragma unroll
           for (int f = 0; f < SK_FG; ++f)
-            if ((need >> f) & 1u) hset(f, x);
+            if (C2_SK_NOBR || ((need >> f) & 1u)) hset(f, x);
         }
         __syncwarp();
         // ---- extraction, all functions at once: lane sub of function myf reads its quarter of the
