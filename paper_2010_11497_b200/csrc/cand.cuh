@@ -70,6 +70,14 @@ __device__ __forceinline__ KC shfl_xor_e(KC a, int m) {
 __device__ __forceinline__ KC shfl_up_e(KC a) {
   return KC{__shfl_up_sync(0xffffffffu, a.k, 1), __shfl_up_sync(0xffffffffu, a.iu, 1)};
 }
+// Key-only element (the key's payload looked up afterwards): one 64-bit shuffle per exchange
+struct KO {
+  uint64_t k;
+};
+__device__ __forceinline__ bool better_e(KO a, KO b) { return a.k > b.k; }
+__device__ __forceinline__ KO shfl_e(KO a, int src) { return KO{__shfl_sync(0xffffffffu, a.k, src)}; }
+__device__ __forceinline__ KO shfl_xor_e(KO a, int m) { return KO{__shfl_xor_sync(0xffffffffu, a.k, m)}; }
+__device__ __forceinline__ KO shfl_up_e(KO a) { return KO{__shfl_up_sync(0xffffffffu, a.k, 1)}; }
 __device__ __forceinline__ Cand shfl_e(Cand a, int src) { return shfl_c(a, src); }
 __device__ __forceinline__ Cand shfl_xor_e(Cand a, int m) { return shfl_xor_c(a, m); }
 __device__ __forceinline__ Cand shfl_up_e(Cand a) { return shfl_up_c(a); }
@@ -186,6 +194,24 @@ __device__ __noinline__ KCA<R> merge_kc_ni(KCA<R> a) {
   return a;
 }
 template <int R>
+struct KOA {
+  KO e[R];
+};
+template <int R>
+__device__ __noinline__ KOA<R> sort_ko_ni(KOA<R> a) {
+  warp_sort<R>(a.e);
+  return a;
+}
+template <int R>
+__device__ __forceinline__ void sort_ko(KO (&x)[R]) {
+  KOA<R> t;
+#pragma unroll
+  for (int j = 0; j < R; ++j) t.e[j] = x[j];
+  t = sort_ko_ni<R>(t);
+#pragma unroll
+  for (int j = 0; j < R; ++j) x[j] = t.e[j];
+}
+template <int R>
 __device__ __forceinline__ void sort_kc(KC (&x)[R]) {
   KCA<R> t;
 #pragma unroll
@@ -246,6 +272,54 @@ __device__ __forceinline__ void rank_merge(const Cand *qr, int m, const c2_cand 
     if (i < nS && i + sh[jj] < kk) dst[i + sh[jj]] = to_out(sv[jj]);
   }
   for (int p = nS + m - __popc(dm) + lane; p < kk; p += 32) dst[p] = c2_cand{-1, 0, 0};
+}
+
+// rank_merge for k <= 32 on exact 64-bit keys (to_kc): the rank of a queued survivor in S by a
+// binary search over the warp-held keys of S, the pairwise ranks by 64-bit compares against the
+// kept survivors' keys compacted into kb (a per-warp shared buffer of 32 keys, read as
+// broadcasts); no S-side ranks when S is empty (a row's first cluster).  Same result as rank_merge.
+__device__ __forceinline__ void rank_merge_k1(const Cand *qr, int m, const c2_cand *S, int kk, c2_cand *dst,
+                                              uint64_t *kb) {
+  const int lane = threadIdx.x & 31;
+  const Cand sv = lane < kk ? from_out(S[lane]) : sent();
+  const int nS = __popc(__ballot_sync(0xffffffffu, is_real(sv)));
+  const Cand q = lane < m ? qr[lane] : sent();
+  const uint64_t qk = to_kc(q).k, sk = to_kc(sv).k;
+  int rs = 0;
+  bool keep = lane < m;
+  if (nS > 0) {
+#pragma unroll
+    for (int st = 16; st >= 1; st >>= 1) {
+      const uint64_t o = __shfl_sync(0xffffffffu, sk, min(rs + st - 1, 31));
+      if (rs + st <= 32 && o > qk) rs += st;
+    }
+    const int32_t at_id = __shfl_sync(0xffffffffu, sv.id, min(rs, 31));
+    keep = keep && !(rs < 32 && at_id == q.id);  // a repeated id carries identical (i, U) (A16)
+  }
+  const unsigned km = __ballot_sync(0xffffffffu, keep);
+  const int mk = __popc(km);
+  if (keep) kb[__popc(km & ((1u << lane) - 1u))] = qk;
+  if (lane >= mk) kb[lane] = 0ull;
+  __syncwarp();
+  int rq = 0, sh = 0;
+  if (nS > 0) {
+    for (int j = 0; j < mk; j += 4) {
+      const ulonglong2 a = *reinterpret_cast<const ulonglong2 *>(kb + j);
+      const ulonglong2 b = *reinterpret_cast<const ulonglong2 *>(kb + j + 2);
+      rq += (a.x > qk) + (a.y > qk) + (b.x > qk) + (b.y > qk);
+      sh += (a.x > sk) + (a.y > sk) + (b.x > sk) + (b.y > sk);
+    }
+  } else {
+    for (int j = 0; j < mk; j += 4) {
+      const ulonglong2 a = *reinterpret_cast<const ulonglong2 *>(kb + j);
+      const ulonglong2 b = *reinterpret_cast<const ulonglong2 *>(kb + j + 2);
+      rq += (a.x > qk) + (a.y > qk) + (b.x > qk) + (b.y > qk);
+    }
+  }
+  __syncwarp();
+  if (keep && rs + rq < kk) dst[rs + rq] = to_out(q);
+  if (lane < nS && lane + sh < kk) dst[lane + sh] = to_out(sv);
+  for (int p = nS + mk + lane; p < kk; p += 32) dst[p] = c2_cand{-1, 0, 0};
 }
 
 // A fixed reference candidate of row r (|P_r| = pr) in the form that makes the order test of a

@@ -1616,7 +1616,7 @@ int local_knn(c2_ctx *ctx, const Csr &csr_in, int t, const Clusters &cl, int k, 
   unsigned long long *wacc = (unsigned long long *)ws_get(ctx, "work_acc", 16, &rc);
   if (rc) return rc;
   C2_CUDA(ctx, cudaMemsetAsync(wacc, 0, 8, st));
-  k_work_steps<<<std::min<unsigned>(nblk((int64_t)t * n), ctx->num_sms * 8), 256, 0, st>>>(cl.offsets, cl.cluster_of, csr.psize, (int64_t)t * n, n, wacc);
+  k_work_steps<<<std::min<unsigned>(nblk((int64_t)t * n), ctx->num_sms * 5), 256, 0, st>>>(cl.offsets, cl.cluster_of, csr.psize, (int64_t)t * n, n, wacc);
   C2_LAUNCHED(ctx, "k_work_steps");
   int32_t hfc[WLC * C2_MAX_T];
   unsigned long long hwork = 0;
@@ -1791,7 +1791,10 @@ int local_knn(c2_ctx *ctx, const Csr &csr_in, int t, const Clusters &cl, int k, 
         C2_LAUNCHED(ctx, "k_sl_fill");
       } else {
         if (C2_FILL_COAL) {
-          k_sl_fill_coal<<<ctx->num_sms * 14, FR_WARPS * 32, 0, st>>>(nb, nwin, bounds, csr.items, W, blk_len8, blk_off8,
+          // one resident wave (the grid-stride loop splits the blocks evenly over the warps)
+          static int occ_fc = 0;
+          if (!occ_fc) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_fc, k_sl_fill_coal, FR_WARPS * 32, 0);
+          k_sl_fill_coal<<<ctx->num_sms * std::max(occ_fc, 1), FR_WARPS * 32, 0, st>>>(nb, nwin, bounds, csr.items, W, blk_len8, blk_off8,
                                                                       packed);
           C2_LAUNCHED(ctx, "k_sl_fill_coal");
         } else {

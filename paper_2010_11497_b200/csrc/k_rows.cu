@@ -20,6 +20,12 @@ namespace c2 {
 // Alg. 3 list in place (c2_build).  Exactness: a candidate is queued only if it is not
 // worse than a valid lower bound of the k-th best (the running k-th best, or the k-th best of any
 // k distinct candidates); the queue is then sorted on exact keys (cand.cuh).
+#ifndef C2_RM_KEYS
+#define C2_RM_KEYS 1  // k <= 32: the <= 32-survivor Alg. 3 step by ranks on exact 64-bit keys (rank_merge_k1)
+#endif
+#ifndef C2_R1_KO
+#define C2_R1_KO 1  // round 1's bound by a key-only sort (the payload fetched afterwards)
+#endif
 #ifndef C2_R1MUL
 #define C2_R1MUL 2  // round 1 keeps C2_R1MUL * KS best candidates per lane
 #endif
@@ -35,6 +41,7 @@ __global__ void __launch_bounds__(RT_WARPS * 32, C2_RT_MINB) k_row_topk(RowArgs 
   __shared__ __align__(16) Cand s_q[RT_WARPS][RT_QCAP];
   __shared__ __align__(16) c2_cand s_run[RT_WARPS][C2_MAX_K];
   __shared__ int s_wq[RT_WARPS];
+  __shared__ __align__(16) uint64_t s_kb[RT_WARPS][32];  // rank_merge_k1's key buffers
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int kk = a.k;
   const int qcap = RT_QCAP;
@@ -143,12 +150,30 @@ __global__ void __launch_bounds__(RT_WARPS * 32, C2_RT_MINB) k_row_topk(RowArgs 
           }
         }
       }
+#if C2_R1_KO
+      // the k-th best of the 32*R1 tops by a key-only sort; its (i, U) is then fetched from the
+      // lane that holds it (keys are distinct for distinct ids)
+      KO e[R1], e0[R1];
+#pragma unroll
+      for (int j = 0; j < R1; ++j) e0[j] = e[j] = KO{to_kc(t[j]).k};
+      sort_ko<R1>(e);
+      const uint64_t kT = warp_get<R1>(e, kk - 1).k;
+      uint32_t iuT = 1u << 16;
+#pragma unroll
+      for (int j = 0; j < R1; ++j) {
+        const unsigned hb = __ballot_sync(0xffffffffu, kT != 0ull && e0[j].k == kT);
+        if (hb) iuT = __shfl_sync(0xffffffffu, t[j].iu, __ffs(hb) - 1);
+      }
+      const Cand Tc = kT != 0ull ? Cand{iuT, (int32_t)(0xFFFFFFFFu - (uint32_t)kT)} : sent();
+      if (is_real(Tc) && better_c(Tc, tau)) T = make_ref(Tc, prr, true);
+#else
       KC e[R1];
 #pragma unroll
       for (int j = 0; j < R1; ++j) e[j] = to_kc(t[j]);
       sort_kc<R1>(e);
       const KC Tr = warp_get<R1>(e, kk - 1);
       if (kc_real(Tr) && better_c(kc_cand(Tr), tau)) T = make_ref(kc_cand(Tr), prr, true);
+#endif
     };
     Ref T = make_ref(tau, prr, false);
     // rows without a running list yet (tau = sentinel) whose candidates cannot all be queued
@@ -209,7 +234,12 @@ __global__ void __launch_bounds__(RT_WARPS * 32, C2_RT_MINB) k_row_topk(RowArgs 
     if (a.seed && m == 0) continue;
     if (a.seed && m <= 32) {
       // few survivors: Alg. 3 step by ranks (no sorting network, no f64 keys)
+#if C2_RM_KEYS
+      if (KS == 1) rank_merge_k1(qr, m, run, kk, dst, s_kb[warp]);
+      else rank_merge<KS>(qr, m, run, kk, dst);
+#else
       rank_merge<KS>(qr, m, run, kk, dst);
+#endif
       __syncwarp();
       continue;
     }
@@ -346,7 +376,8 @@ constexpr int SM_INSERT_MAX = 32;  // survivors of a chunk merged by insertion (
 #define C2_SM_MERGE_MIN 16
 #endif
 #ifndef C2_SM_RANK
-#define C2_SM_RANK 1  // k <= 32: every survivor chunk merged by ranks (0: insertion / bitonic merge below)
+#define C2_SM_RANK 2  // k <= 32: every survivor chunk merged by ranks (2: on exact 64-bit keys, 1: cross products;
+                      // 0: insertion / bitonic merge below)
 #endif
 constexpr int SM_MERGE_MIN = C2_SM_MERGE_MIN;  // k <= 32: chunks with more survivors take the bitonic merge
                                                // (c5: threshold 4 57.6 ms, 8 56.3, 16 55.4, off 55.5)
@@ -355,6 +386,7 @@ template <int KS>
 __global__ void __launch_bounds__(256) k_surv_merge(const c2_cand *__restrict__ surv, int32_t *__restrict__ qn,
                                                     int qmax, int32_t n, int k, c2_cand *__restrict__ run) {
   __shared__ c2_cand s_buf[8][32 * KS];
+  __shared__ __align__(16) uint64_t s_key[8][32];  // C2_SM_RANK == 2: kept survivors' keys
   const int lane = threadIdx.x & 31;
   c2_cand *sbuf = s_buf[threadIdx.x >> 5];
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -385,6 +417,35 @@ __global__ void __launch_bounds__(256) k_surv_merge(const c2_cand *__restrict__ 
           // rs = the survivor's rank in S (binary search; a repeated id carries the same (i, U),
           // so its twin sits exactly at rs, A16), then over the kept survivors o: rq = the
           // survivor's rank among them, sh = lane's S entry's; new positions rs + rq and lane + sh
+#if C2_SM_RANK == 2
+          // exact 64-bit keys (cand.cuh to_kc: larger = better, distinct for distinct ids): the
+          // binary search and the pairwise ranks are plain 64-bit compares; the kept survivors'
+          // keys are compacted into shared memory and read back as broadcasts
+          const uint64_t xk = to_kc(ok ? x : sent()).k, sk = to_kc(S[0]).k;
+          int r = 0;
+#pragma unroll
+          for (int st = 16; st >= 1; st >>= 1) {
+            const uint64_t o = __shfl_sync(0xffffffffu, sk, min(r + st - 1, 31));
+            if (r + st <= 32 && o > xk) r += st;
+          }
+          const int32_t at_id = __shfl_sync(0xffffffffu, S[0].id, min(r, 31));
+          ok = ok && !(r < 32 && at_id == x.id);
+          const unsigned km = __ballot_sync(0xffffffffu, ok);
+          const int nS = __popc(__ballot_sync(0xffffffffu, lane < k && is_real(S[0])));
+          const int mk = __popc(km);
+          uint64_t *kb = s_key[threadIdx.x >> 5];
+          if (ok) kb[__popc(km & ((1u << lane) - 1u))] = xk;  // positions < mk
+          if (lane >= mk) kb[lane] = 0ull;  // padding read by the last group of 4 (0: better than nothing)
+          __syncwarp();
+          int rq = 0, sh = 0;
+          for (int j = 0; j < mk; j += 4) {
+            const ulonglong2 k01 = *reinterpret_cast<const ulonglong2 *>(kb + j);
+            const ulonglong2 k23 = *reinterpret_cast<const ulonglong2 *>(kb + j + 2);
+            rq += (k01.x > xk) + (k01.y > xk) + (k23.x > xk) + (k23.y > xk);
+            sh += (k01.x > sk) + (k01.y > sk) + (k23.x > sk) + (k23.y > sk);
+          }
+          __syncwarp();
+#else
           int r = 0;
 #pragma unroll
           for (int st = 16; st >= 1; st >>= 1) {
@@ -408,6 +469,7 @@ __global__ void __launch_bounds__(256) k_surv_merge(const c2_cand *__restrict__ 
             const uint32_t l2 = oi * sU, r2 = si * oU;  // o before lane's S entry?
             sh += (l2 > r2 || (l2 == r2 && oid < S[0].id)) ? 1 : 0;
           }
+#endif
           if (ok && r + rq < k) sbuf[r + rq] = to_out(x);
           if (lane < nS && lane + sh < k) sbuf[lane + sh] = to_out(S[0]);
           for (int p = nS + __popc(km) + lane; p < k; p += 32) sbuf[p] = c2_cand{-1, 0, 0};
@@ -478,10 +540,15 @@ int launch_row_topk(c2_ctx *ctx, const RowArgs &ra) {
 
 int launch_surv_merge(c2_ctx *ctx, const c2_cand *surv, int32_t *qn, int qmax, int32_t n, int k, c2_cand *run,
                       cudaStream_t st) {
-  const int g = ctx->num_sms * 8;
+  // one resident wave: the grid-stride loop gives every block the same share of users, so blocks
+  // beyond the resident ones would run as a second, partial wave
+  static int occ[2] = {0, 0};
+  const int ks = k <= 32 ? 0 : 1;
+  auto kern = ks ? k_surv_merge<2> : k_surv_merge<1>;
+  if (!occ[ks]) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ[ks], kern, 256, 0);
+  const int g = ctx->num_sms * std::max(occ[ks], 1);
   if (!st) st = ctx->stream;
-  if (k <= 32) k_surv_merge<1><<<g, 256, 0, st>>>(surv, qn, qmax, n, k, run);
-  else k_surv_merge<2><<<g, 256, 0, st>>>(surv, qn, qmax, n, k, run);
+  kern<<<g, 256, 0, st>>>(surv, qn, qmax, n, k, run);
   C2_LAUNCHED(ctx, "k_surv_merge");
   return C2_OK;
 }

@@ -88,7 +88,7 @@ __global__ void __launch_bounds__(256) k_sketch(const int32_t *__restrict__ offs
 // Per item and function: one 64-bit multiply-add, a compare, and for ~SK_K/|P_u| of them one
 // shared atomic; no per-lane sorted inserts (the divergence of the thread-per-(user, f) form).
 #ifndef C2_SK_NOBR
-#define C2_SK_NOBR 1  // 1: no per-function branch in the item loops (finished functions' windows moved out of range)
+#define C2_SK_NOBR 0  // 1: no per-function branch in the item loops (finished functions' windows moved out of range)
 #endif
 constexpr int SK_WARPS = 8;
 constexpr int SK_FG = 8;      // functions per pass over the items
