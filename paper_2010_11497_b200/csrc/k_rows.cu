@@ -21,10 +21,12 @@ namespace c2 {
 // worse than a valid lower bound of the k-th best (the running k-th best, or the k-th best of any
 // k distinct candidates); the queue is then sorted on exact keys (cand.cuh).
 #ifndef C2_RM_KEYS
-#define C2_RM_KEYS 1  // k <= 32: the <= 32-survivor Alg. 3 step by ranks on exact 64-bit keys (rank_merge_k1)
+#define C2_RM_KEYS 1  // k <= 32: the <= 32-survivor Alg. 3 step by ranks on exact 64-bit keys (rank_merge_k1;
+                      // c5: 51.3 vs 51.5 ms without)
 #endif
 #ifndef C2_R1_KO
-#define C2_R1_KO 1  // round 1's bound by a key-only sort (the payload fetched afterwards)
+#define C2_R1_KO 0  // 1: round 1's bound by a key-only sort, the payload fetched afterwards (measured at c5:
+                    // 51.6 vs 51.3 ms with the payload carried through the sort -- off)
 #endif
 #ifndef C2_R1MUL
 #define C2_R1MUL 2  // round 1 keeps C2_R1MUL * KS best candidates per lane
