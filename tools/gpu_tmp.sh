@@ -1,6 +1,9 @@
 set -o pipefail
 mkdir -p gpurun_out
-AB="base rmk0 ko0 both0 base rmk0 ko0 both0" QT_CFGS="c5" bash tools/ab.sh run > gpurun_out/ab4.log 2>&1
-grep "c5 mode\|==" gpurun_out/ab4.log | cut -c1-130
-timeout 1500 python -m pytest tests -m gpu -x -q 2>&1 | tail -5 > gpurun_out/pytest_gpu.log; cat gpurun_out/pytest_gpu.log
-timeout 600 python tools/quick_time.py > gpurun_out/quick.log 2>&1; cat gpurun_out/quick.log | cut -c1-200
+timeout 900 python bench.py --steps 5 --warmup 3 > gpurun_out/bench.log 2>&1; tail -c 600 gpurun_out/bench.log
+timeout 900 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/bench_ref.log 2>&1; tail -c 600 gpurun_out/bench_ref.log
+bash tools/gpu_launches.sh c5 > /dev/null 2>&1; head -14 gpurun_out/launches_c5.txt
+timeout 300 python tools/run_cfg.py c5 0 1 > gpurun_out/plain_c5.log 2>&1 && \
+timeout 900 python tools/ncu_pipes.py run c5 gpurun_out/ncu_pipes_c5.csv > gpurun_out/ncu_pipes.log 2>&1
+tail -2 gpurun_out/ncu_pipes.log
+python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -1
