@@ -46,6 +46,10 @@
 #ifndef C2_SPLIT
 #define C2_SPLIT 1  // 1: tiles of <= 8 slices split each member list over several warps
 #endif
+#ifndef C2_HSPLIT
+#define C2_HSPLIT 0  // tiles of > TILE_WARPS/2 slices with a free counter slot: the C2_HSPLIT longest slices
+                     // (members are longest-first) are each probed by TILE_WARPS/C2_HSPLIT warps (0: off)
+#endif
 #ifndef C2_RANKMERGE
 #define C2_RANKMERGE 1  // 1: rank-based Alg. 3 step for <= 32 survivors; 0: insertion (<= 16)
 #endif
@@ -865,6 +869,18 @@ struct TileArgs {
 
 // 8 masks of one uint4 of packed u16 item ids
 __device__ __forceinline__ void masks8(const uint32_t *__restrict__ M, uint4 d, uint32_t (&m)[8]) {
+#ifdef C2_TIMING_NOCONFLICT  // timing experiment only (wrong counts): every lane reads its own bank
+  const uint32_t ln = threadIdx.x & 31u;
+  m[0] = M[((d.x & 0xFFFFu) & ~31u) | ln];
+  m[1] = M[((d.x >> 16) & ~31u) | ln];
+  m[2] = M[((d.y & 0xFFFFu) & ~31u) | ln];
+  m[3] = M[((d.y >> 16) & ~31u) | ln];
+  m[4] = M[((d.z & 0xFFFFu) & ~31u) | ln];
+  m[5] = M[((d.z >> 16) & ~31u) | ln];
+  m[6] = M[((d.w & 0xFFFFu) & ~31u) | ln];
+  m[7] = M[((d.w >> 16) & ~31u) | ln];
+  return;
+#endif
   m[0] = M[d.x & 0xFFFFu];
   m[1] = M[d.x >> 16];
   m[2] = M[d.y & 0xFFFFu];
@@ -933,6 +949,7 @@ __global__ void __launch_bounds__(TILE_T, C2_TILE_MINB) k_local_tile(TileArgs a)
   __shared__ uint4 s_ref[32];       // light rows: the running k-th best as a Ref (see make_ref)
   __shared__ int s_qn[32];          // light rows: survivors found by the phase-A epilogue
   __shared__ unsigned s_light;      // light rows (running list full, k-th best with i >= 1)
+  __shared__ unsigned s_mxst, s_sumst;  // kstats: probe steps of the tile's busiest warp / of all warps
   __shared__ unsigned s_over;       // light rows with more than qmax survivors (handed to k_row_topk)
   __shared__ int64_t s_cbase, s_rbase;  // this tile's first count entry / record for k_row_topk
   __shared__ int s_pre;                 // 1: s_cbase / s_rbase were allocated early (no barrier needed)
@@ -1079,6 +1096,8 @@ __global__ void __launch_bounds__(TILE_T, C2_TILE_MINB) k_local_tile(TileArgs a)
     if (tid == 0) {
       s_light = 0u;
       s_over = 0u;
+      s_mxst = 0u;
+      s_sumst = 0u;
     }
     const unsigned valid = __ballot_sync(0xffffffffu, lane < nr && s_ru[lane] >= 0);
     unsigned k8rows = valid;  // rows handed to k_row_topk
@@ -1101,13 +1120,23 @@ __global__ void __launch_bounds__(TILE_T, C2_TILE_MINB) k_local_tile(TileArgs a)
     // small tiles (<= TILE_WARPS/2 slices): G warps share a slice, each probing a contiguous part
     // of its member lists; the partial bit-sliced counters are then added (bit-sliced ripple
     // carry), so no warp idles through the probe of a tile with few slices
-    int G = 1;
+    // bigger tiles whose whole slices leave the last counter slot free: the profile lengths are
+    // heavy-tailed, so the longest slice alone outlasts the mean warp (c5, kstats: busiest warp
+    // 31 steps vs 11 mean in clusters of 257-1024); its lists are split over G warps the same way
+    int G = 1;   // warps per split slice
+    int Hs = 0;  // slices [0, Hs) are split; their (partial) counters live in slot QS
+    constexpr int QS = VPT - 1;
+    if (C2_HSPLIT && VPT >= 2 && nsl > TILE_WARPS / 2 && nsl - C2_HSPLIT <= TILE_WARPS * (VPT - 1)) {
+      Hs = C2_HSPLIT;
+      G = TILE_WARPS / C2_HSPLIT;
+    }
     if (C2_SPLIT && nsl <= TILE_WARPS / 2) {
       // parts of >= ~4 steps (pairs of 8-item groups; the rows' own lengths stand for the slices')
       int np = 0;
       for (int w = 0; w < nwin; ++w) np += (s_bl[cur][w] + 1) >> 1;
       G = TILE_WARPS;
       while (G > 1 && (G * nsl > TILE_WARPS || 4 * G > np)) G >>= 1;
+      if (G > 1) Hs = nsl;
     }
     const int part = warp % G;
     // ================= phase A: counts |P_r ∩ P_v| for the 32 rows x all v of the cluster
@@ -1115,13 +1144,14 @@ __global__ void __launch_bounds__(TILE_T, C2_TILE_MINB) k_local_tile(TileArgs a)
       // the slice of this warp's q-th counter (nsl: none); after the probe (all = false) a split
       // slice belongs to its part-0 warp only, which holds the added counters
       auto slice_of = [&](int q, bool all = false) -> int {
-        if (G > 1) return (q == 0 && warp / G < nsl && (all || part == 0)) ? warp / G : nsl;
-        const int jj = g0 + q * TILE_WARPS + ((C2_SNAKE && (q & 1)) ? TILE_WARPS - 1 - warp : warp);
+        if (Hs > 0 && q == QS) return (warp / G < Hs && (all || part == 0)) ? warp / G : nsl;
+        const int jj = Hs + g0 + q * TILE_WARPS + ((C2_SNAKE && (q & 1)) ? TILE_WARPS - 1 - warp : warp);
         return jj < nsl ? jj : nsl;
       };
       Counter<NHI> C[VPT];
 #pragma unroll
       for (int q = 0; q < VPT; ++q) C[q].zero();
+      unsigned tsteps = 0u;  // (kstats)
       for (int w = 0; w < nwin; ++w) {
         // ---- build M for window w from the tile's own slice (rows), lane r -> bit r (the first
         //      16-byte group of every thread is kept for the clear below)
@@ -1183,7 +1213,7 @@ __global__ void __launch_bounds__(TILE_T, C2_TILE_MINB) k_local_tile(TileArgs a)
 #if C2_PACK32
             // rows of 4 byte offsets per lane; 16 items (4 rows) per step, the next step in flight
             int32_t plo = 0, phi = len8;  // this warp's part of the lists (quads of rows)
-            if (G > 1) {
+            if (G > 1 && q == QS) {
               const int32_t np = (len8 + 3) >> 2;
               plo = 4 * ((part * np) / G);
               phi = 4 * (((part + 1) * np) / G);
@@ -1221,7 +1251,7 @@ __global__ void __launch_bounds__(TILE_T, C2_TILE_MINB) k_local_tile(TileArgs a)
             }
 #else
             int32_t plo = 0, phi = len8;  // this warp's part of the lists (pairs of 8-item groups)
-            if (G > 1) {
+            if (G > 1 && q == QS) {
               const int32_t np = (len8 + 1) >> 1;
               plo = 2 * ((part * np) / G);
               phi = 2 * (((part + 1) * np) / G);
@@ -1243,6 +1273,11 @@ __global__ void __launch_bounds__(TILE_T, C2_TILE_MINB) k_local_tile(TileArgs a)
             }
 #endif
           }
+        }
+        tsteps += (unsigned)nsteps;
+        if (a.kstats && lane == 0 && w + 1 == nwin) {
+          atomicMax(&s_mxst, tsteps);
+          atomicAdd(&s_sumst, tsteps);
         }
         if (a.kstats && lane == 0 && s > 1024) {  // probe busy time per step (big tiles)
           atomicAdd(&a.kstats[64], (unsigned long long)(clock64() - ckpb));
@@ -1275,17 +1310,17 @@ __global__ void __launch_bounds__(TILE_T, C2_TILE_MINB) k_local_tile(TileArgs a)
         // in M's words when M is big enough -- re-zeroed by the reader -- else a region of its own)
         constexpr int NPL = 4 + NHI;
         uint32_t *scr = a.scr_off ? dyn + a.scr_off : M;
-        if (part != 0 && warp / G < nsl) {
+        if (part != 0 && warp / G < Hs) {
           uint32_t *o = scr + warp * NPL * 32 + lane;
-          o[0] = C[0].ones;
-          o[32] = C[0].twos;
-          o[64] = C[0].fours;
-          o[96] = C[0].eights;
+          o[0] = C[QS].ones;
+          o[32] = C[QS].twos;
+          o[64] = C[QS].fours;
+          o[96] = C[QS].eights;
 #pragma unroll
-          for (int i = 0; i < NHI; ++i) o[(4 + i) * 32] = C[0].H[i];
+          for (int i = 0; i < NHI; ++i) o[(4 + i) * 32] = C[QS].H[i];
         }
         __syncthreads();
-        if (part == 0 && warp / G < nsl) {
+        if (part == 0 && warp / G < Hs) {
           for (int pw = 1; pw < G; ++pw) {
             uint32_t *o = scr + (warp + pw) * NPL * 32 + lane;
             uint32_t b[NPL];
@@ -1295,12 +1330,12 @@ __global__ void __launch_bounds__(TILE_T, C2_TILE_MINB) k_local_tile(TileArgs a)
               if (!a.scr_off) o[j * 32] = 0u;
             }
             uint32_t *pa[NPL];
-            pa[0] = &C[0].ones;
-            pa[1] = &C[0].twos;
-            pa[2] = &C[0].fours;
-            pa[3] = &C[0].eights;
+            pa[0] = &C[QS].ones;
+            pa[1] = &C[QS].twos;
+            pa[2] = &C[QS].fours;
+            pa[3] = &C[QS].eights;
 #pragma unroll
-            for (int i = 0; i < NHI; ++i) pa[4 + i] = &C[0].H[i];
+            for (int i = 0; i < NHI; ++i) pa[4 + i] = &C[QS].H[i];
             uint32_t cy = 0u;
 #pragma unroll
             for (int j = 0; j < NPL; ++j) {
@@ -1464,6 +1499,11 @@ __global__ void __launch_bounds__(TILE_T, C2_TILE_MINB) k_local_tile(TileArgs a)
       atomicAdd(&kc3[0], (unsigned long long)(ckA - ck0));
       atomicAdd(&kc3[1], (unsigned long long)(ckE - ckA));
       atomicAdd(&kc3[2], (unsigned long long)(ck3 - ckE));
+      if (lt) {  // (the light epilogue's barrier orders the warps' step counts before this read)
+        atomicAdd(&a.kstats[52 + cls], (unsigned long long)s_mxst);
+        atomicAdd(&a.kstats[56 + cls], (unsigned long long)s_sumst);
+        atomicAdd(&a.kstats[60 + cls], 1ull);
+      }
     }
     cur ^= 1;
   }

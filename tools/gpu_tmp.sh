@@ -1,9 +1,3 @@
-set -o pipefail
 mkdir -p gpurun_out
-timeout 900 python bench.py --steps 5 --warmup 3 > gpurun_out/bench.log 2>&1; tail -c 600 gpurun_out/bench.log
-timeout 900 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/bench_ref.log 2>&1; tail -c 600 gpurun_out/bench_ref.log
-bash tools/gpu_launches.sh c5 > /dev/null 2>&1; head -14 gpurun_out/launches_c5.txt
-timeout 300 python tools/run_cfg.py c5 0 1 > gpurun_out/plain_c5.log 2>&1 && \
-timeout 900 python tools/ncu_pipes.py run c5 gpurun_out/ncu_pipes_c5.csv > gpurun_out/ncu_pipes.log 2>&1
-tail -2 gpurun_out/ncu_pipes.log
-python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -1
+echo "== base"; timeout 600 python tools/kstats.py c5 2>&1 | tail -9 | head -5
+echo "== nocf"; C2_LIB=$PWD/paper_2010_11497_b200/lib/variants/nocf.so timeout 600 python tools/kstats.py c5 2>&1 | tail -9 | head -5
