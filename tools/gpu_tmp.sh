@@ -1,3 +1,5 @@
+set -o pipefail
 mkdir -p gpurun_out
-echo "== base"; timeout 600 python tools/kstats.py c5 2>&1 | tail -9 | head -5
-echo "== nocf"; C2_LIB=$PWD/paper_2010_11497_b200/lib/variants/nocf.so timeout 600 python tools/kstats.py c5 2>&1 | tail -9 | head -5
+timeout 1500 python -m pytest tests -m gpu -x -q 2>&1 | tail -4
+timeout 900 python bench.py --steps 5 --warmup 3 > gpurun_out/bench.log 2>&1; tail -c 300 gpurun_out/bench.log
+python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -1
