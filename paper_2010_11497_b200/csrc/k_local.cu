@@ -50,6 +50,10 @@
 #define C2_HSPLIT 0  // tiles of > TILE_WARPS/2 slices with a free counter slot: the C2_HSPLIT longest slices
                      // (members are longest-first) are each probed by TILE_WARPS/C2_HSPLIT warps (0: off)
 #endif
+#ifndef C2_KSTATS_STEPS
+#define C2_KSTATS_STEPS 0  // 1: kstats also count the probe steps of each tile's busiest warp (diagnostic
+                           // build: the extra live register costs 0.7 ms per c5 build even with kstats off)
+#endif
 #ifndef C2_RANKMERGE
 #define C2_RANKMERGE 1  // 1: rank-based Alg. 3 step for <= 32 survivors; 0: insertion (<= 16)
 #endif
@@ -1151,7 +1155,9 @@ __global__ void __launch_bounds__(TILE_T, C2_TILE_MINB) k_local_tile(TileArgs a)
       Counter<NHI> C[VPT];
 #pragma unroll
       for (int q = 0; q < VPT; ++q) C[q].zero();
-      unsigned tsteps = 0u;  // (kstats)
+#if C2_KSTATS_STEPS
+      unsigned tsteps = 0u;
+#endif
       for (int w = 0; w < nwin; ++w) {
         // ---- build M for window w from the tile's own slice (rows), lane r -> bit r (the first
         //      16-byte group of every thread is kept for the clear below)
@@ -1274,11 +1280,13 @@ __global__ void __launch_bounds__(TILE_T, C2_TILE_MINB) k_local_tile(TileArgs a)
 #endif
           }
         }
+#if C2_KSTATS_STEPS
         tsteps += (unsigned)nsteps;
         if (a.kstats && lane == 0 && w + 1 == nwin) {
           atomicMax(&s_mxst, tsteps);
           atomicAdd(&s_sumst, tsteps);
         }
+#endif
         if (a.kstats && lane == 0 && s > 1024) {  // probe busy time per step (big tiles)
           atomicAdd(&a.kstats[64], (unsigned long long)(clock64() - ckpb));
           atomicAdd(&a.kstats[65], (unsigned long long)nsteps);

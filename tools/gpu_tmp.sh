@@ -1,5 +1,2 @@
-set -o pipefail
-mkdir -p gpurun_out
-timeout 1500 python -m pytest tests -m gpu -x -q 2>&1 | tail -4
-timeout 900 python bench.py --steps 5 --warmup 3 > gpurun_out/bench.log 2>&1; tail -c 300 gpurun_out/bench.log
-python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -1
+AB="old main hs2n hs4n old main hs2n" QT_CFGS="c4 c5" bash tools/ab.sh run > gpurun_out/ab7.log 2>&1
+grep "c5 mode\|c4 mode=0\|==" gpurun_out/ab7.log | cut -c1-130
