@@ -27,5 +27,7 @@ for i, nm in enumerate(["mixed", "33-256", "257-1024", ">1024"]):
           f"phase A {k[40 + 3 * i] / mt:8.0f}  light epilogue {k[41 + 3 * i] / mt:7.0f}  count rows {k[42 + 3 * i] / mt:7.0f}")
 print(f"  probe of >1024 tiles: busy cycles per warp-step {k[64] / max(k[65], 1):.0f}  steps {k[65]}")
 for i, nm in enumerate(["mixed", "33-256", "257-1024", ">1024"]):
+    if not k[52 + i]:  # (counted only by a -DC2_KSTATS_STEPS=1 build)
+        continue
     nt = max(k[60 + i], 1)
     print(f"  probe balance {nm:9s} light tiles {k[60 + i]:7d}: steps of the busiest warp {k[52 + i] / nt:7.1f}  mean per warp {k[56 + i] / nt / 16:7.1f}")
