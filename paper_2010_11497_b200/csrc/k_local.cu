@@ -54,6 +54,9 @@
 #define C2_KSTATS_STEPS 0  // 1: kstats also count the probe steps of each tile's busiest warp (diagnostic
                            // build: the extra live register costs 0.7 ms per c5 build even with kstats off)
 #endif
+#ifndef C2_NHI7
+#define C2_NHI7 1  // 1: an 11-plane counter instantiation (item lists of <= 2047) beside the 8-, 12- and 15-plane ones
+#endif
 #ifndef C2_RANKMERGE
 #define C2_RANKMERGE 1  // 1: rank-based Alg. 3 step for <= 32 survivors; 0: insertion (<= 16)
 #endif
@@ -1524,6 +1527,9 @@ static TileKernel pick_vpt(int vpt) {
   return vpt <= 1 ? k_local_tile<NHI, 1> : vpt <= 2 ? k_local_tile<NHI, 2> : k_local_tile<NHI, 4>;
 }
 static TileKernel pick_tile(int nhi, int vpt) {
+#if C2_NHI7
+  if (nhi > 4 && nhi <= 7) return pick_vpt<7>(vpt);  // lists of <= 2047 items (c5: max 2000)
+#endif
   return nhi <= 4 ? pick_vpt<4>(vpt) : nhi <= 8 ? pick_vpt<8>(vpt) : pick_vpt<11>(vpt);
 }
 
@@ -1907,7 +1913,7 @@ int local_knn(c2_ctx *ctx, const Csr &csr_in, int t, const Clusters &cl, int k, 
                           4096;  // minus the kernel's static shared memory (~2.5 KB)
     const size_t mw = (size_t)((W + 4) & ~3);  // M: W + 1 words
     // split-probe scratch: TILE_WARPS x (4 + nhi) planes x 32 lanes, in M's words when W + 1 allows
-    const size_t scrw = (size_t)TILE_WARPS * (4 + (nhi <= 4 ? 4 : nhi <= 8 ? 8 : 11)) * 32;
+    const size_t scrw = (size_t)TILE_WARPS * (4 + (nhi <= 4 ? 4 : (C2_NHI7 && nhi <= 7) ? 7 : nhi <= 8 ? 8 : 11)) * 32;
     const size_t scr_own = (size_t)W + 1 >= scrw ? 0 : scrw;
     scr_off = scr_own ? (int32_t)mw : 0;
     stg_off = (int32_t)(mw + scr_own);
