@@ -57,6 +57,9 @@
 #ifndef C2_NHI7
 #define C2_NHI7 1  // 1: an 11-plane counter instantiation (item lists of <= 2047) beside the 8-, 12- and 15-plane ones
 #endif
+#ifndef C2_HIPLANES
+#define C2_HIPLANES 0  // h > 0: tiles whose rows all hold < 16 * 2^h items skip the probe's carry ripple above plane H[h-1]
+#endif
 #ifndef C2_RANKMERGE
 #define C2_RANKMERGE 1  // 1: rank-based Alg. 3 step for <= 32 survivors; 0: insertion (<= 16)
 #endif
@@ -928,6 +931,27 @@ struct Counter {
     csa(e8, fours, fours, fA, fB);
     return e8;
   }
+  // add16 for tiles whose counts stay below 2^(4 + LO) unless hi (CTA-uniform): the carry out of
+  // plane H[LO - 1] is then always zero and the upper planes need no update
+  template <int LO>
+  __device__ __forceinline__ void add16h(uint32_t e8a, uint32_t e8b, bool hi) {
+    uint32_t carry;
+    csa(carry, eights, eights, e8a, e8b);
+#pragma unroll
+    for (int i = 0; i < (LO < NHI ? LO : NHI); ++i) {
+      uint32_t tt = H[i] & carry;
+      H[i] ^= carry;
+      carry = tt;
+    }
+    if (hi) {
+#pragma unroll
+      for (int i = LO; i < NHI; ++i) {
+        uint32_t tt = H[i] & carry;
+        H[i] ^= carry;
+        carry = tt;
+      }
+    }
+  }
   __device__ __forceinline__ void add16(uint32_t e8a, uint32_t e8b) {
     uint32_t carry;
     csa(carry, eights, eights, e8a, e8b);
@@ -1107,6 +1131,10 @@ __global__ void __launch_bounds__(TILE_T, C2_TILE_MINB) k_local_tile(TileArgs a)
       s_sumst = 0u;
     }
     const unsigned valid = __ballot_sync(0xffffffffu, lane < nr && s_ru[lane] >= 0);
+#if C2_HIPLANES
+    // every count of the tile is <= its longest row: short rows never carry into the upper planes
+    const bool hi_planes = __reduce_max_sync(0xffffffffu, s_rp[lane]) >= (16u << C2_HIPLANES);
+#endif
     unsigned k8rows = valid;  // rows handed to k_row_topk
     const bool lt = light_on && nsl <= VPT * TILE_WARPS;  // (one g0 group: counters of all members live)
     // rows handed to k_row_topk known now (no light rows), or after the light rows are known when no
@@ -1273,7 +1301,11 @@ __global__ void __launch_bounds__(TILE_T, C2_TILE_MINB) k_local_tile(TileArgs a)
               uint32_t e8a = C[q].add8(m);
               masks8(M, d1, m);
               uint32_t e8b = C[q].add8(m);
+#if C2_HIPLANES
+              C[q].template add16h<C2_HIPLANES>(e8a, e8b, hi_planes);
+#else
               C[q].add16(e8a, e8b);
+#endif
               d0 = n0;
               d1 = n1;
               n0 = f0;
