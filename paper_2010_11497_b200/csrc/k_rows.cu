@@ -386,7 +386,8 @@ constexpr int SM_MERGE_MIN = C2_SM_MERGE_MIN;  // k <= 32: chunks with more surv
 
 template <int KS>
 __global__ void __launch_bounds__(256) k_surv_merge(const c2_cand *__restrict__ surv, int32_t *__restrict__ qn,
-                                                    int qmax, int32_t n, int k, c2_cand *__restrict__ run) {
+                                                    int qmax, int32_t n, int k, c2_cand *__restrict__ run,
+                                                    unsigned long long *kstats = nullptr) {
   __shared__ c2_cand s_buf[8][32 * KS];
   __shared__ __align__(16) uint64_t s_key[8][32];  // C2_SM_RANK == 2: kept survivors' keys
   const int lane = threadIdx.x & 31;
@@ -433,6 +434,12 @@ __global__ void __launch_bounds__(256) k_surv_merge(const c2_cand *__restrict__ 
           const int32_t at_id = __shfl_sync(0xffffffffu, S[0].id, min(r, 31));
           ok = ok && !(r < 32 && at_id == x.id);
           const unsigned km = __ballot_sync(0xffffffffu, ok);
+#ifdef C2_KSTATS_SURV  // diagnostic build: survivors still better than tau / of those, not yet in the list
+          if (kstats && lane == 0) {
+            atomicAdd(&kstats[75], (unsigned long long)__popc(bal));
+            atomicAdd(&kstats[76], (unsigned long long)__popc(km));
+          }
+#endif
           const int nS = __popc(__ballot_sync(0xffffffffu, lane < k && is_real(S[0])));
           const int mk = __popc(km);
           uint64_t *kb = s_key[threadIdx.x >> 5];
@@ -550,7 +557,11 @@ int launch_surv_merge(c2_ctx *ctx, const c2_cand *surv, int32_t *qn, int qmax, i
   if (!occ[ks]) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ[ks], kern, 256, 0);
   const int g = ctx->num_sms * std::max(occ[ks], 1);
   if (!st) st = ctx->stream;
-  kern<<<g, 256, 0, st>>>(surv, qn, qmax, n, k, run);
+#ifdef C2_KSTATS_SURV
+  kern<<<g, 256, 0, st>>>(surv, qn, qmax, n, k, run, ctx->kstats);
+#else
+  kern<<<g, 256, 0, st>>>(surv, qn, qmax, n, k, run, nullptr);
+#endif
   C2_LAUNCHED(ctx, "k_surv_merge");
   return C2_OK;
 }

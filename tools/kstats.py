@@ -31,3 +31,6 @@ for i, nm in enumerate(["mixed", "33-256", "257-1024", ">1024"]):
         continue
     nt = max(k[60 + i], 1)
     print(f"  probe balance {nm:9s} light tiles {k[60 + i]:7d}: steps of the busiest warp {k[52 + i] / nt:7.1f}  mean per warp {k[56 + i] / nt / 16:7.1f}")
+if k[75]:  # (a -DC2_KSTATS_SURV build)
+    print(f"  k_surv_merge: survivors better than the current k-th best {k[75]} ({k[75] / max(k[71], 1):.2f} per light row), "
+          f"of those not yet in the list {k[76]} ({k[76] / max(k[71], 1):.2f} per light row)")
