@@ -93,13 +93,16 @@ __global__ void __launch_bounds__(256) k_sketch(const int32_t *__restrict__ offs
 constexpr int SK_WARPS = 8;
 constexpr int SK_FG = 8;      // functions per pass over the items
 constexpr int SK_CAPW = 128;  // window words per function (4096 values)
+#ifndef C2_SK_MINB
+#define C2_SK_MINB 3
+#endif
 #ifndef C2_SK_K
 #define C2_SK_K 12  // (c5: 16 -> 1.80 ms, 12 -> 1.72, 10 -> 1.75, 20 -> 1.87)
 #endif
 constexpr int SK_K = C2_SK_K;  // target number of hashed values inside the first window
 
 template <bool POW2>
-__global__ void __launch_bounds__(SK_WARPS * 32, 3) k_sketch_w(const int32_t *__restrict__ offs,
+__global__ void __launch_bounds__(SK_WARPS * 32, C2_SK_MINB) k_sketch_w(const int32_t *__restrict__ offs,
                                                             const int32_t *__restrict__ items, int32_t n, int t,
                                                             uint32_t b, HashArgs ha, int D,
                                                             uint16_t *__restrict__ out, int64_t u0 = 0,
